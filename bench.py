@@ -1,0 +1,366 @@
+#!/usr/bin/env python3
+"""Benchmark of the spectral Poisson solve (BASELINE.json metric: Poisson
+unknowns solved/sec, fp64 FFT solve, % of HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n 1024] [--impl ours|reference]
+
+One step = one full solve (r2c 3D FFT, Poisson scale, c2r 3D FFT) of the
+BASELINE config-4 source (1024^3 fp64, 64 random Fourier modes, seed 4),
+inputs resident in HBM.  The field (8.6 GB) is far larger than L2 (126 MB),
+so no L2 flush is needed between steps.  Prints ONE JSON line on rank 0.
+
+--impl reference times the reference's own CPU solver (fft_solver.cpp:51-87
+over the FFTW3-API shim, oracle/_ref; the C restatement oracle/lib when that
+was not built) on the host cores, on a bounded 512^3 sample of the same source.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "Poisson unknowns solved/sec (fp64 FFT solve)"
+UNIT = "unknowns/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--precision", type=int, default=64, choices=(64, 32))
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-n", type=int, default=512, help="grid of the bounded CPU sample")
+    return ap.parse_args()
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes(n: int, elem: int):
+    """Per-kernel algorithmic HBM bytes: R = real field, C = half spectrum."""
+    R = n ** 3 * elem
+    C = n * n * (n // 2 + 1) * 2 * elem
+    return {"zfwd_r2c": R + C, "yfwd": 2 * C, "xmid_fwd_scale_inv": 2 * C, "yinv": 2 * C, "zinv_c2r": C + R}, 2 * R + 8 * C
+
+
+def cpu_sample(n: int, config: int, kind=None, min_seconds: float = 10.0, max_runs: int = 3):
+    """Time the oracle on a bounded sample: solve the config source at n^3 until
+    min_seconds elapsed or max_runs done; returns (unknowns/s, kind, threads, runs)."""
+    import numpy as np
+
+    import oracle
+    from paper_1408_6497_b200 import problems
+
+    kind = kind or oracle.best_kind()
+    threads = len(os.sched_getaffinity(0))
+    oracle.set_threads(threads, kind)
+    src = problems.config(config, n)
+    f = _host_source(src)
+    oracle.poisson_solve(f[:8, :8, :8].copy(), kind)  # warm the library
+    runs, t0 = 0, time.perf_counter()
+    while True:
+        oracle.poisson_solve(f, kind)
+        runs += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds or runs >= max_runs:
+            break
+    return n ** 3 * runs / el, kind, threads, runs
+
+
+def _host_source(src):
+    """Config source on the host without the GPU: separable per-mode evaluation."""
+    import numpy as np
+
+    from paper_1408_6497_b200 import problems
+
+    n = src.n
+    if isinstance(src, problems.ModeSource):
+        # Re sum a e^{2 pi i k.x} = inverse DFT of a sparse Hermitian spectrum (scipy pocketfft).
+        import scipy.fft as sf
+
+        F = np.zeros((n, n, n), dtype=np.complex128)
+        for (kx, ky, kz), c in zip(src.k, src.f_coef()):
+            F[kx % n, ky % n, kz % n] += 0.5 * c
+            F[-kx % n, -ky % n, -kz % n] += 0.5 * np.conj(c)
+        out = sf.ifftn(F, workers=len(os.sched_getaffinity(0)), overwrite_x=True).real * float(n) ** 3
+        del F
+        return np.ascontiguousarray(out)
+    return problems.eval_host(src, "f")
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU solver on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    from paper_1408_6497_b200 import problems
+
+    kind = oracle.best_kind()
+    threads = len(os.sched_getaffinity(0))
+    oracle.set_threads(threads, kind)
+    n = args.cpu_n
+    src = problems.config(args.config, n)
+    f = _host_source(src)
+    for _ in range(args.warmup):
+        oracle.poisson_solve(f, kind)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.poisson_solve(f, kind)
+    el = time.perf_counter() - t0
+    v = n ** 3 * args.steps / el
+    sample = (f"{n}^3 sample of config {args.config}'s source (same 64 modes), full solve per step; "
+              f"engine: {'reference fft_solver.cpp over FFTW3-API shim (oracle/_ref)' if kind == 'ref' else 'C restatement (oracle/lib)'}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C{args.config}: {problems.CONFIG_TEXT[args.config]}", "n": args.n,
+                   "sample_n": n},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference" if kind == "ref" else "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    import numpy as np
+    import torch
+
+    import paper_1408_6497_b200 as arena
+    from paper_1408_6497_b200 import problems
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, prec = args.n, args.precision
+    elem = 8 if prec == 64 else 4
+    dt = torch.float64 if prec == 64 else torch.float32
+    src = problems.config(args.config, n)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    # ---- inputs resident in HBM (f as fp64, rounded to fp32 for fp32 runs)
+    f64 = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+    problems.fill_device(src, "f", f64, 64, sh)
+    f64 -= f64.mean()
+    f = f64 if prec == 64 else f64.float()
+    u = torch.empty_like(f)
+    plan = arena.Plan(n, prec, local)
+    launches = plan.launches_per_solve
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        plan.solve_device(f, u, sh)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K solves, CUDA events on the launching stream, per-kernel events inside
+    plan.set_stage_timing(True)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        start.record(stream)
+        for _ in range(args.steps):
+            plan.solve_device(f, u, sh)
+        end.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms_total = start.elapsed_time(end)
+    stage_ms, nsol = plan.stage_times()
+    plan.set_stage_timing(False)
+    if dist is not None:
+        t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = t.item()
+    ms_step = ms_total / args.steps
+    value = world * n ** 3 / (ms_step / 1e3)  # replicas: every rank solves its own n^3
+
+    # ---- parity of the timed output vs the analytic solution (band-limited source: exact)
+    ua = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+    problems.fill_device(src, "u", ua, 64, sh)
+    ua -= ua.mean()
+    rel_an = (torch.linalg.vector_norm(u.double() - ua) / torch.linalg.vector_norm(ua)).item()
+    del ua
+
+    # ---- roofline of the dominant kernel
+    peak, peak_kind = _peaks()
+    per_kernel, b_solve = algorithmic_bytes(n, elem)
+    dom = max(stage_ms, key=lambda k: stage_ms[k])
+    dom_ms = stage_ms[dom] / nsol
+    achieved = per_kernel[dom] / (dom_ms / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(REPO, "profiles", "traffic_latest.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"{n}_{prec}", {}).get(dom)
+        except Exception:
+            traffic = None
+    kernels = {k: {"ms": stage_ms[k] / nsol, "alg_bytes": per_kernel[k],
+                   "gbs": per_kernel[k] / (stage_ms[k] / nsol / 1e3) / 1e9,
+                   "share": stage_ms[k] / sum(stage_ms.values())} for k in stage_ms}
+    solve_gbs = b_solve / (ms_step / 1e3) / 1e9
+
+    # ---- e2e through the public host API (pinned host f, u; H2D + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        hf = torch.empty((n, n, n), dtype=dt, pin_memory=True)
+        hf.copy_(f)
+        hu = torch.empty_like(hf, pin_memory=True)
+        plan.solve_host(hf, hu)  # warm (allocates the plan's host-path buffers)
+        ksteps = max(1, min(args.steps, 5))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(ksteps):
+            plan.solve_host(hf, hu)
+        el = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = t.item()
+        e2e = {"value": world * n ** 3 * ksteps / el, "unit": UNIT, "h2d_bytes_per_step": n ** 3 * elem,
+               "d2h_bytes_per_step": n ** 3 * elem, "steps": ksteps, "ms_per_step": el / ksteps * 1e3,
+               "api": "arena_poisson_solve_host (pinned host buffers)"}
+        e2e_ok = bool(torch.allclose(hu, u.cpu()))
+        e2e["matches_device_path"] = e2e_ok
+        del hf, hu
+
+    # ---- CPU baseline (rank 0, N=1 only), bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            v, kind, threads, runs = cpu_sample(args.cpu_n, args.config)
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference" if kind == "ref" else "port",
+                   "sample": f"{args.cpu_n}^3 solve(s) of config {args.config}'s source ({runs} run(s)), "
+                             f"{'reference fft_solver.cpp over FFTW3-API shim' if kind == 'ref' else 'C restatement'}"
+                             f", OpenMP over lines"}
+        except Exception as exc:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": None, "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+            "dtype": "f64" if prec == 64 else "f32", "data": "synthetic",
+            "config": {"workload": f"C{args.config}: {problems.CONFIG_TEXT[args.config]}", "n": n,
+                       "precision": prec, "decomposition": "single-GPU" if world == 1 else f"{world} replicas",
+                       "l2": "inputs larger than L2 (8.6 GB field), no flush",
+                       "path": "pow2" if plan.path == arena.PATH_POW2 else "generic"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "solve_alg_bytes": b_solve, "solve_achieved_gbs": solve_gbs, "solve_frac": solve_gbs / peak,
+                         "kernels": kernels},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+            "parity": {"rel_l2_vs_analytic": rel_an},
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    rank, world, local = _dist()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

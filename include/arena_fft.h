@@ -1,0 +1,111 @@
+/*
+ * arena_fft.h — C ABI of the B200-native spectral Poisson solver.
+ *
+ * This is the drop-in boundary for the reference's FFT hot path.  The
+ * reference exposes no FFI of its own: its only interface for the path is the
+ * C++ free function
+ *     arena::GridField arena::poisson_spectral_solve(const arena::GridField&)
+ *       /root/reference/proj/include/arena/fft_solver.hpp:23
+ *       /root/reference/proj/src/fft_solver.cpp:51-87
+ * plus its siblings dft3_forward / dft3_inverse (fft_solver.hpp:13,16).
+ * include/arena/fft_solver.hpp re-declares exactly those C++ signatures and
+ * paper_1408_6497_b200/csrc/fft_solver_dropin.cpp implements them over the
+ * entry points below.  Every entry point is extern "C", takes plain pointers
+ * and sizes, and never throws; errors are status codes plus a thread-local
+ * message (arena_last_error).  See INTEGRATION.md for the bindings a
+ * maintainer would add.
+ *
+ * Data layout at the boundary (identical to GridField, grid.hpp:11-27): an
+ * n x n x n row-major array of values sampled at (i/n, j/n, k/n), element
+ * (i, j, k) at ((i*n)+j)*n+k, k contiguous.  fp64 buffers are double, fp32
+ * buffers float.  Complex spectra (dft3_*) are interleaved (re, im) n^3
+ * arrays in the same row-major order, i.e. std::vector<std::complex<double>>.
+ */
+#ifndef ARENA_FFT_H
+#define ARENA_FFT_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum arena_status {
+  ARENA_OK = 0,
+  ARENA_EINVAL = 1,      /* bad argument: n < 2 (GridField throws, grid.hpp:18), NULL pointer, ... */
+  ARENA_ENOMEM = 2,      /* device or pinned-host allocation failed (std::bad_alloc analogue) */
+  ARENA_ECUDA = 3,       /* CUDA runtime / launch error */
+  ARENA_ENCCL = 4,       /* NCCL error (multi-GPU plans) */
+  ARENA_EUNSUPPORTED = 5 /* valid request this build cannot serve (e.g. no sm_100a device) */
+} arena_status;
+
+typedef struct arena_fft_plan arena_fft_plan;
+
+/* Execution path chosen for a plan (arena_fft_plan_info). */
+enum { ARENA_PATH_POW2 = 0, ARENA_PATH_GENERIC = 1 };
+
+/* Setup ("Setup" in the paper's Setup/Solve split; replaces the
+ * per-call fftw_plan_* at fft_solver.cpp:60-63 with a once-per-(n, precision,
+ * device) object): twiddle tables, the device half-spectrum workspace and
+ * kernel attributes.  precision_bits is 64 (the reference's double) or 32.
+ * device is a CUDA ordinal; -1 means the calling thread's current device. */
+arena_status arena_fft_plan_create(arena_fft_plan** plan, int n, int precision_bits, int device);
+void arena_fft_plan_destroy(arena_fft_plan* plan);
+
+/* Query: n, precision bits, path (ARENA_PATH_*), device, bytes of device workspace. */
+arena_status arena_fft_plan_info(const arena_fft_plan* plan, int* n, int* precision_bits, int* path,
+                                 int* device, size_t* workspace_bytes);
+
+/* The solve, device-resident (the timed hot path).  d_f, d_u: caller-owned
+ * device buffers of n^3 values (may alias: u may overwrite f).  stream: a
+ * cudaStream_t (NULL = legacy default stream).  Asynchronous: returns after
+ * enqueueing; errors from the launches are reported, kernel faults surface on
+ * the caller's next synchronisation.  Semantics of fft_solver.cpp:51-87:
+ * u = IFFT( FFT(f) * (k2 == 0 ? 0 : (1/n^3) / (4 pi^2 k2)) ), k2 = |signed k|^2. */
+arena_status arena_poisson_solve_device(arena_fft_plan* plan, const void* d_f, void* d_u, void* stream);
+
+/* The drop-in path: host buffers in and out (pageable or pinned), copies
+ * inside.  Synchronous.  This is what arena::poisson_spectral_solve calls. */
+arena_status arena_poisson_solve_host(arena_fft_plan* plan, const void* f, void* u);
+
+/* arena::dft3_forward (fft_solver.cpp:13-29): real n^3 -> full complex n^3
+ * spectrum (interleaved), unnormalised, sign -1.  Host and device variants. */
+arena_status arena_dft3_forward_host(arena_fft_plan* plan, const void* g, void* spec);
+arena_status arena_dft3_forward_device(arena_fft_plan* plan, const void* d_g, void* d_spec, void* stream);
+/* arena::dft3_inverse (fft_solver.cpp:31-49): complex n^3 -> Re(backward)/n^3. */
+arena_status arena_dft3_inverse_host(arena_fft_plan* plan, const void* spec, void* g);
+arena_status arena_dft3_inverse_device(arena_fft_plan* plan, const void* d_spec, void* d_g, void* stream);
+
+/* Measurement hooks (bench.py): when enabled, every solve records a CUDA event
+ * before each kernel and after the last one on the solve's stream; query the
+ * accumulated per-kernel milliseconds (sum over recorded solves; names[i] is
+ * the kernel label) with arena_fft_stage_times, which synchronises. */
+arena_status arena_fft_set_stage_timing(arena_fft_plan* plan, int enable);
+arena_status arena_fft_stage_times(arena_fft_plan* plan, double* ms, const char** names, int max_stages,
+                                   int* n_stages, int* n_solves);
+
+/* Number of kernel launches one arena_poisson_solve_device call enqueues. */
+int arena_poisson_launches_per_solve(const arena_fft_plan* plan);
+
+/* Device-side input generation (replaces host sampling
+ * through std::function, grid.cpp:21-27, which is infeasible at 1024^3+).
+ * Not part of the solve.  d_out: device buffer of n^3 values.
+ *   arena_source_modes:    out = sum_m Re(coef_m exp(2 pi i k_m . x)), x = (i,j,k)/n;
+ *                          k: 3*nmodes host ints, coef: 2*nmodes host doubles (re, im).
+ *   arena_source_gaussian: periodised Gaussian over the 27 nearest images,
+ *                          which = 0: u = sum exp(-alpha r^2), 1: f = -Lap u. */
+arena_status arena_source_modes(int n, int precision_bits, int nmodes, const int* k, const double* coef, void* d_out,
+                                void* stream);
+arena_status arena_source_gaussian(int n, int precision_bits, double alpha, double cx, double cy, double cz, int which,
+                                   void* d_out, void* stream);
+
+/* Thread-local description of the last failure on this thread ("" if none). */
+const char* arena_last_error(void);
+
+/* ABI version of this library (major * 100 + minor). */
+int arena_fft_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,252 @@
+"""B200-native spectral Poisson solver — Python host mirror of the reference API.
+
+The product is the C ABI in ``include/arena_fft.h`` (``lib/libarena_fft.so``,
+sm_100a CUDA kernels) and the C++ drop-in ``include/arena/fft_solver.hpp``
+(``lib/libarena_core.so``).  This module is a thin ctypes binding used by the
+tests and by ``bench.py``; it mirrors the reference's function names and
+error behaviour (/root/reference/proj/include/arena/fft_solver.hpp:11-23):
+
+    poisson_spectral_solve(f)   fft_solver.cpp:51-87
+    dft3_forward(g)             fft_solver.cpp:13-29
+    dft3_inverse(spec, n)       fft_solver.cpp:31-49
+    signed_freq(k, n)           fft_solver.hpp:19
+
+n < 2 raises ValueError (std::invalid_argument in the reference, grid.hpp:18).
+There is no CPU path: if the shared library is missing this import fails, and
+without an sm_100a device every solve raises RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(_HERE, "lib")
+LIB_PATH = os.path.join(LIB_DIR, "libarena_fft.so")
+CORE_PATH = os.path.join(LIB_DIR, "libarena_core.so")
+REPO_ROOT = os.path.dirname(_HERE)
+HEADER_PATH = os.path.join(REPO_ROOT, "include", "arena_fft.h")
+
+ARENA_OK, ARENA_EINVAL, ARENA_ENOMEM, ARENA_ECUDA, ARENA_ENCCL, ARENA_EUNSUPPORTED = range(6)
+PATH_POW2, PATH_GENERIC = 0, 1
+_STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "EUNSUPPORTED"}
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(or `make -C paper_1408_6497_b200`). There is no CPU fallback."
+    )
+
+lib = ctypes.CDLL(LIB_PATH)
+
+_vp = ctypes.c_void_p
+_i = ctypes.c_int
+_sig = {
+    "arena_fft_plan_create": (_i, [ctypes.POINTER(_vp), _i, _i, _i]),
+    "arena_fft_plan_destroy": (None, [_vp]),
+    "arena_fft_plan_info": (_i, [_vp, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(_i),
+                                  ctypes.POINTER(_i), ctypes.POINTER(ctypes.c_size_t)]),
+    "arena_poisson_solve_device": (_i, [_vp, _vp, _vp, _vp]),
+    "arena_poisson_solve_host": (_i, [_vp, _vp, _vp]),
+    "arena_dft3_forward_host": (_i, [_vp, _vp, _vp]),
+    "arena_dft3_forward_device": (_i, [_vp, _vp, _vp, _vp]),
+    "arena_dft3_inverse_host": (_i, [_vp, _vp, _vp]),
+    "arena_dft3_inverse_device": (_i, [_vp, _vp, _vp, _vp]),
+    "arena_fft_set_stage_timing": (_i, [_vp, _i]),
+    "arena_fft_stage_times": (_i, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_char_p), _i,
+                                   ctypes.POINTER(_i), ctypes.POINTER(_i)]),
+    "arena_poisson_launches_per_solve": (_i, [_vp]),
+    "arena_source_modes": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp]),
+    "arena_source_gaussian": (_i, [_i, _i, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                   _i, _vp, _vp]),
+    "arena_last_error": (ctypes.c_char_p, []),
+    "arena_fft_abi_version": (_i, []),
+}
+for _name, (_res, _args) in _sig.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+class ArenaError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        msg = lib.arena_last_error().decode(errors="replace")
+        super().__init__(f"{what}: {_STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _check(status: int, what: str) -> None:
+    if status == ARENA_OK:
+        return
+    if status == ARENA_EINVAL:
+        raise ValueError(f"{what}: {lib.arena_last_error().decode(errors='replace')}")
+    if status == ARENA_ENOMEM:
+        raise MemoryError(f"{what}: {lib.arena_last_error().decode(errors='replace')}")
+    raise ArenaError(status, what)
+
+
+def signed_freq(k: int, n: int) -> int:
+    """fft_solver.hpp:19 — signed frequency in (-n/2, n/2]."""
+    return k if k <= n // 2 else k - n
+
+
+def _ptr(x) -> int:
+    """Raw pointer of a numpy array or torch tensor."""
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+class Plan:
+    """Owns an ``arena_fft_plan`` (Setup: twiddles + device half-spectrum workspace)."""
+
+    def __init__(self, n: int, precision: int = 64, device: int = -1):
+        self._p = _vp()
+        _check(lib.arena_fft_plan_create(ctypes.byref(self._p), int(n), int(precision), int(device)),
+               "arena_fft_plan_create")
+        self.n = int(n)
+        self.precision = int(precision)
+        self.dtype = np.float64 if precision == 64 else np.float32
+        self.lock = threading.Lock()
+        nn, pb, path, dev, ws = _i(), _i(), _i(), _i(), ctypes.c_size_t()
+        _check(lib.arena_fft_plan_info(self._p, ctypes.byref(nn), ctypes.byref(pb), ctypes.byref(path),
+                                       ctypes.byref(dev), ctypes.byref(ws)), "arena_fft_plan_info")
+        self.path, self.device, self.workspace_bytes = path.value, dev.value, ws.value
+
+    @property
+    def handle(self) -> _vp:
+        return self._p
+
+    def close(self) -> None:
+        if getattr(self, "_p", None) and self._p.value:
+            lib.arena_fft_plan_destroy(self._p)
+            self._p = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches_per_solve(self) -> int:
+        return lib.arena_poisson_launches_per_solve(self._p)
+
+    # ---- device-resident solve (the timed hot path)
+    def solve_device(self, f, u, stream: Optional[int] = None) -> None:
+        """Enqueue u = solve(f) on `stream` (cudaStream_t as int; None = torch's current stream).
+        f, u: CUDA tensors of n^3 values of the plan's precision (may be the same tensor)."""
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(f.device).cuda_stream
+        _check(lib.arena_poisson_solve_device(self._p, _vp(_ptr(f)), _vp(_ptr(u)), _vp(stream)),
+               "arena_poisson_solve_device")
+
+    # ---- host boundary (the drop-in path)
+    def solve_host(self, f, u) -> None:
+        _check(lib.arena_poisson_solve_host(self._p, _vp(_ptr(f)), _vp(_ptr(u))), "arena_poisson_solve_host")
+
+    def dft3_forward_host(self, g: np.ndarray) -> np.ndarray:
+        out = np.empty(g.shape, dtype=np.complex128 if self.precision == 64 else np.complex64)
+        _check(lib.arena_dft3_forward_host(self._p, _vp(g.ctypes.data), _vp(out.ctypes.data)), "dft3_forward")
+        return out
+
+    def dft3_inverse_host(self, spec: np.ndarray) -> np.ndarray:
+        out = np.empty(spec.shape, dtype=self.dtype)
+        _check(lib.arena_dft3_inverse_host(self._p, _vp(spec.ctypes.data), _vp(out.ctypes.data)), "dft3_inverse")
+        return out
+
+    # ---- measurement hooks
+    def set_stage_timing(self, enable: bool) -> None:
+        _check(lib.arena_fft_set_stage_timing(self._p, int(bool(enable))), "arena_fft_set_stage_timing")
+
+    def stage_times(self):
+        """-> (dict name -> total ms over recorded solves, number of solves)."""
+        ms = (ctypes.c_double * 16)()
+        names = (ctypes.c_char_p * 16)()
+        ns, nsol = _i(), _i()
+        _check(lib.arena_fft_stage_times(self._p, ms, names, 16, ctypes.byref(ns), ctypes.byref(nsol)),
+               "arena_fft_stage_times")
+        return {names[i].decode(): ms[i] for i in range(ns.value)}, nsol.value
+
+
+_plans: dict = {}
+_plans_lock = threading.Lock()
+
+
+def get_plan(n: int, precision: int = 64, device: int = -1) -> Plan:
+    """Plan cache keyed by (n, precision, device) — the analogue of the reference's
+    planner mutex (fft_solver.cpp:10-11), created once instead of per call."""
+    key = (int(n), int(precision), int(device))
+    with _plans_lock:
+        p = _plans.get(key)
+        if p is None:
+            p = Plan(n, precision, device)
+            _plans[key] = p
+        return p
+
+
+def _as_grid(f: np.ndarray, dtype) -> np.ndarray:
+    f = np.ascontiguousarray(f, dtype=dtype)
+    if f.ndim != 3 or not (f.shape[0] == f.shape[1] == f.shape[2]):
+        raise ValueError("GridField: expected an n x n x n array")
+    if f.shape[0] < 2:
+        raise ValueError("GridField: n >= 2 required")
+    return f
+
+
+def poisson_spectral_solve(f: np.ndarray, precision: int = 64) -> np.ndarray:
+    """u with -Lap u = f - mean(f), mean(u) = 0 (fft_solver.cpp:51-87) — host arrays in/out."""
+    dtype = np.float64 if precision == 64 else np.float32
+    f = _as_grid(f, dtype)
+    u = np.empty_like(f)
+    p = get_plan(f.shape[0], precision)
+    with p.lock:
+        p.solve_host(f, u)
+    return u
+
+
+def dft3_forward(g: np.ndarray) -> np.ndarray:
+    """Full n^3 complex spectrum, unnormalised, sign -1 (fft_solver.cpp:13-29)."""
+    g = _as_grid(g, np.float64)
+    p = get_plan(g.shape[0], 64)
+    with p.lock:
+        return p.dft3_forward_host(g)
+
+
+def dft3_inverse(spec: np.ndarray, n: int) -> np.ndarray:
+    """Re(backward DFT)/n^3 (fft_solver.cpp:31-49); size mismatch -> ValueError."""
+    spec = np.ascontiguousarray(spec, dtype=np.complex128)
+    if spec.size != n * n * n:
+        raise ValueError("dft3_inverse: size mismatch")
+    if n < 2:
+        raise ValueError("GridField: n >= 2 required")
+    p = get_plan(n, 64)
+    with p.lock:
+        return p.dft3_inverse_host(spec.reshape(n, n, n))
+
+
+def source_modes(n: int, kvec: np.ndarray, coef: np.ndarray, out, precision: int = 64, stream: int = 0) -> None:
+    """Device buffer `out` (n^3) = sum_m Re(coef_m e^{2 pi i k_m.x}).  kvec: (M, 3) ints, coef: (M,) complex."""
+    kvec = np.ascontiguousarray(kvec, dtype=np.int32).reshape(-1, 3)
+    c = np.ascontiguousarray(np.stack([np.real(coef), np.imag(coef)], axis=-1), dtype=np.float64)
+    _check(lib.arena_source_modes(int(n), int(precision), int(kvec.shape[0]), _vp(kvec.ctypes.data),
+                                  _vp(c.ctypes.data), _vp(_ptr(out)), _vp(stream)), "arena_source_modes")
+
+
+def source_gaussian(n: int, alpha: float, center, which: int, out, precision: int = 64, stream: int = 0) -> None:
+    """Device buffer `out` = periodised Gaussian u (which=0) or f = -Lap u (which=1)."""
+    cx, cy, cz = (float(c) for c in center)
+    _check(lib.arena_source_gaussian(int(n), int(precision), float(alpha), cx, cy, cz, int(which), _vp(_ptr(out)),
+                                     _vp(stream)), "arena_source_gaussian")
+
+
+__all__ = [
+    "Plan", "get_plan", "poisson_spectral_solve", "dft3_forward", "dft3_inverse", "signed_freq",
+    "source_modes", "source_gaussian", "ArenaError", "lib", "LIB_PATH", "CORE_PATH", "HEADER_PATH",
+    "PATH_POW2", "PATH_GENERIC",
+]

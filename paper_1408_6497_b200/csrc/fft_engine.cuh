@@ -1,0 +1,288 @@
+// fft_engine.cuh — register/shared-memory FFT line engine for sm_100a.
+//
+// Replaces the FFTW codelets the reference calls at
+// /root/reference/proj/src/fft_solver.cpp:65 (r2c execute) and :80 (c2r
+// execute).  Same DFT conventions (FFTW's published definitions): forward is
+// exp(-2 pi i k x / n), unnormalised; backward exp(+...), unnormalised.
+//
+// Formulation: Stockham autosort, radix-2^k stages (Govindaraju et al. 2008).
+// One "tile" = L independent lines of length N, processed by L*P threads
+// (P = N/E threads per line, each thread holding E points in registers).
+// Thread (l, t) — l fastest in threadIdx.x — always holds line-l elements
+// t + P*e, e in [0, E), both before the first stage and after the last stage,
+// so global loads and stores use the same (coalesced) pattern, and a forward
+// transform can feed an inverse one without leaving registers (the fused
+// x-pass).  Between stages the tile is exchanged through shared memory laid
+// out [position][line] so that the 8 lanes of a 16-byte shared-memory phase
+// hit 8 distinct bank groups.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace arena_fft {
+
+// ---------------------------------------------------------------- complex ops
+template <typename T>
+struct Vec2;
+template <>
+struct Vec2<double> {
+  using type = double2;
+};
+template <>
+struct Vec2<float> {
+  using type = float2;
+};
+template <typename T>
+using vec2_t = typename Vec2<T>::type;
+
+template <typename V>
+__device__ __forceinline__ V cadd(V a, V b) {
+  return V{a.x + b.x, a.y + b.y};
+}
+template <typename V>
+__device__ __forceinline__ V csub(V a, V b) {
+  return V{a.x - b.x, a.y - b.y};
+}
+// a * w
+template <typename V>
+__device__ __forceinline__ V cmul(V a, V w) {
+  return V{fma(a.x, w.x, -a.y * w.y), fma(a.x, w.y, a.y * w.x)};
+}
+// a * conj(w)
+template <typename V>
+__device__ __forceinline__ V cmulc(V a, V w) {
+  return V{fma(a.x, w.x, a.y * w.y), fma(a.y, w.x, -a.x * w.y)};
+}
+// a * (S * i), S = +-1
+template <int S, typename V>
+__device__ __forceinline__ V cmul_si(V a) {
+  return S > 0 ? V{-a.y, a.x} : V{a.y, -a.x};
+}
+
+// cos(2 pi m / 64), m = 0..16 (first quadrant), double-rounded.
+constexpr double kCos64[17] = {1.0,
+                               0.9951847266721969,
+                               0.9807852804032304,
+                               0.9569403357322088,
+                               0.9238795325112867,
+                               0.881921264348355,
+                               0.8314696123025452,
+                               0.773010453362737,
+                               0.7071067811865476,
+                               0.6343932841636455,
+                               0.5555702330196022,
+                               0.47139673682599764,
+                               0.3826834323650898,
+                               0.2902846772544624,
+                               0.19509032201612828,
+                               0.0980171403295606,
+                               0.0};
+
+constexpr double cos64(int m) {
+  m = ((m % 64) + 64) % 64;
+  const int q = m / 16, r = m % 16;
+  return q == 0 ? kCos64[r] : q == 1 ? -kCos64[16 - r] : q == 2 ? -kCos64[r] : kCos64[16 - r];
+}
+constexpr double sin64(int m) { return cos64(m - 16); }
+
+// a * exp(S * 2 pi i * E / R), R | 64, all compile-time.
+template <int R, int E, int S, typename V>
+__device__ __forceinline__ V cmul_const(V a) {
+  constexpr int m = ((E * (64 / R)) % 64 + 64) % 64;
+  if constexpr (m == 0) {
+    return a;
+  } else if constexpr (m == 16) {
+    return cmul_si<S>(a);
+  } else if constexpr (m == 32) {
+    return V{-a.x, -a.y};
+  } else if constexpr (m == 48) {
+    return cmul_si<-S>(a);
+  } else {
+    using T = decltype(a.x);
+    constexpr T c = T(cos64(m));
+    constexpr T s = T(S * sin64(m));
+    return V{fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c)};
+  }
+}
+
+// ---------------------------------------------------------- in-register DFTs
+// In-place DFT of x[0..R) with sign S (-1 forward, +1 backward), natural order
+// in and out.  R = 1, 2, 4 directly; larger powers of two by one radix-4 (or
+// radix-2) decimation-in-time step over recursive sub-DFTs, all indices and
+// twiddles compile-time so everything stays in registers.
+template <int R, int S>
+struct Dft;
+
+template <int S>
+struct Dft<1, S> {
+  template <typename V>
+  __device__ __forceinline__ static void run(V*) {}
+};
+
+template <int S>
+struct Dft<2, S> {
+  template <typename V>
+  __device__ __forceinline__ static void run(V* x) {
+    const V t = x[1];
+    x[1] = csub(x[0], t);
+    x[0] = cadd(x[0], t);
+  }
+};
+
+template <int S>
+struct Dft<4, S> {
+  template <typename V>
+  __device__ __forceinline__ static void run(V* x) {
+    const V s02 = cadd(x[0], x[2]), d02 = csub(x[0], x[2]);
+    const V s13 = cadd(x[1], x[3]), d13 = cmul_si<S>(csub(x[1], x[3]));
+    x[0] = cadd(s02, s13);
+    x[2] = csub(s02, s13);
+    x[1] = cadd(d02, d13);
+    x[3] = csub(d02, d13);
+  }
+};
+
+template <int R, int S>
+struct Dft {
+  static_assert(R % 4 == 0 && R <= 64, "power-of-two radix <= 64");
+  template <typename V>
+  __device__ __forceinline__ static void run(V* x) {
+    constexpr int Q = R / 4;
+    V a[4][Q];
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1)
+#pragma unroll
+      for (int n2 = 0; n2 < Q; ++n2) a[n1][n2] = x[4 * n2 + n1];
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) Dft<Q, S>::run(a[n1]);
+    twiddle_all<1, 0>(a);
+#pragma unroll
+    for (int k1 = 0; k1 < Q; ++k1) {
+      V b[4] = {a[0][k1], a[1][k1], a[2][k1], a[3][k1]};
+      Dft<4, S>::run(b);
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) x[k1 + Q * k2] = b[k2];
+    }
+  }
+  // compile-time loop applying W_R^{S n1 k1}
+  template <int N1, int K1, typename V, int Q>
+  __device__ __forceinline__ static void twiddle_all(V (&a)[4][Q]) {
+    if constexpr (N1 < 4) {
+      if constexpr (K1 < Q) {
+        a[N1][K1] = cmul_const<R, N1 * K1, S>(a[N1][K1]);
+        twiddle_all<N1, K1 + 1>(a);
+      } else {
+        twiddle_all<N1 + 1, 0>(a);
+      }
+    }
+  }
+};
+
+// ------------------------------------------------------------- stage plans
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
+constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// Number of Stockham stages for an N-point line with E points per thread,
+// and the radix (log2) of stage s: bits split as evenly as possible, larger
+// radices first.
+constexpr int num_stages(int N, int E) { return N <= 1 ? 0 : cdiv(ilog2(N), ilog2(E)); }
+constexpr int stage_log2(int N, int E, int s) {
+  const int ns = num_stages(N, E), b = ilog2(N);
+  return b / ns + (s < b % ns ? 1 : 0);
+}
+constexpr int stage_ns(int N, int E, int s) {  // product of radices before stage s
+  return s == 0 ? 1 : stage_ns(N, E, s - 1) << stage_log2(N, E, s - 1);
+}
+
+// Shared-memory element index of (position, line).  A 128-byte shared-memory
+// phase covers G = 128/sizeof(V)/L positions; when G > 1 XOR-swizzle the low
+// bits of the position with bits above the first-stage radix so both the
+// natural-order reads and the first stage's stride-R writes are conflict-free.
+template <int L, int SW, typename V>
+__device__ __forceinline__ int smem_idx(int pos, int l) {
+  constexpr int G = int(128 / sizeof(V)) / L;  // positions per shared-memory phase
+  if constexpr (G <= 1 || SW == 0) {
+    return pos * L + l;
+  } else {
+    return (pos ^ ((pos >> SW) & (G - 1))) * L + l;
+  }
+}
+
+// Table twiddle W_N^m (forward) for an N-point line; `tw` holds W_NT^j for
+// j in [0, NT) and TWMUL = NT / N.
+template <int S, typename V>
+__device__ __forceinline__ V tw_apply(V a, const V* __restrict__ tw, int idx) {
+  const V w = __ldg(tw + idx);
+  return S < 0 ? cmul(a, w) : cmulc(a, w);
+}
+
+// One Stockham stage on registers (no exchange).  Thread holds elements
+// t + P*e; butterfly q uses v[q + NB*r], r < R.
+template <int N, int E, int R, int NS, int S, typename V>
+__device__ __forceinline__ void stage_compute(V (&v)[E], int t, const V* __restrict__ tw, int twmul) {
+  constexpr int P = N / E, NB = E / R;
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    V a[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) a[r] = v[q + NB * r];
+    if constexpr (NS > 1) {
+      const int jj = (t + P * q) & (NS - 1);
+      const int base = jj * (N / (NS * R)) * twmul;
+#pragma unroll
+      for (int r = 1; r < R; ++r) a[r] = tw_apply<S>(a[r], tw, base * r);
+    }
+    Dft<R, S>::run(a);
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[q + NB * r] = a[r];
+  }
+}
+
+// Write stage outputs to shared memory at their Stockham destinations and
+// read back the natural-order inputs of the next stage.
+template <int N, int E, int L, int R, int NS, int SW, typename V>
+__device__ __forceinline__ void stage_exchange(V (&v)[E], V* sm, int t, int l) {
+  constexpr int P = N / E, NB = E / R;
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    const int b = t + P * q;
+    const int dst = (b & ~(NS - 1)) * R + (b & (NS - 1));
+#pragma unroll
+    for (int r = 0; r < R; ++r) sm[smem_idx<L, SW, V>(dst + r * NS, l)] = v[q + NB * r];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = sm[smem_idx<L, SW, V>(t + P * e, l)];
+  __syncthreads();
+}
+
+template <int N, int E, int L, int S, int STAGE, typename V>
+__device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, const V* __restrict__ tw, int twmul, int t, int l) {
+  constexpr int NSTAGE = num_stages(N, E);
+  if constexpr (STAGE < NSTAGE) {
+    constexpr int R = 1 << stage_log2(N, E, STAGE);
+    constexpr int NS = stage_ns(N, E, STAGE);
+    constexpr int SW = stage_log2(N, E, 0);
+    stage_compute<N, E, R, NS, S>(v, t, tw, twmul);
+    if constexpr (STAGE + 1 < NSTAGE) stage_exchange<N, E, L, R, NS, SW>(v, sm, t, l);
+    fft_stages<N, E, L, S, STAGE + 1>(v, sm, tw, twmul, t, l);
+  }
+}
+
+// Full N-point line FFT of the tile.  On entry and exit thread (l, t) holds
+// line-l elements t + P*e (natural order).  `sm` must hold N*L elements and
+// be free (all threads past their last access) on entry; on exit it is free.
+template <int N, int E, int L, int S, typename V>
+__device__ __forceinline__ void line_fft(V (&v)[E], V* sm, const V* __restrict__ tw, int twmul, int t, int l) {
+  fft_stages<N, E, L, S, 0>(v, sm, tw, twmul, t, l);
+}
+
+// Swizzle parameter callers must use when they stage data in `sm` in the
+// engine's layout (natural position order).
+template <int N, int E>
+constexpr int engine_swizzle() {
+  return N <= 1 ? 0 : stage_log2(N, E, 0);
+}
+
+}  // namespace arena_fft

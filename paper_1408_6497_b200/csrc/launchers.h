@@ -1,0 +1,55 @@
+// launchers.h — host-side entry points of the kernel translation units
+// (no device code; included by plan.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace arena_fft {
+
+constexpr int kPow2MaxN = 2048;
+constexpr int kPow2Launches = 5;
+
+struct Pow2Args {
+  const void* f;
+  void* u;
+  void* spec;
+  const void* tw;
+  int n, nc, ncp;
+  cudaStream_t stream;
+  cudaEvent_t* ev;  // nullable; kPow2Launches + 1 events: before each kernel and after the last
+};
+
+cudaError_t launch_pow2_f64(const Pow2Args& a);
+cudaError_t launch_pow2_f32(const Pow2Args& a);
+
+// Generic mixed-radix path (any n >= 2).  One Stockham plan for an n-point line.
+constexpr int kGenMaxStages = 40;
+struct GenPlan {
+  int n;
+  int nst;
+  int radix[kGenMaxStages];
+};
+bool gen_plan_make(int n, GenPlan* p);
+size_t gen_smem_bytes(int n, int elem_bytes);
+int gen_max_n(int elem_bytes);
+
+struct GenArgs {
+  const GenPlan* plan;
+  const void* tw;  // W_n^m, m in [0, n), vec2 of the precision
+  int n, nc, ncp;
+  cudaStream_t stream;
+  cudaEvent_t* ev;  // nullable
+};
+
+// Poisson solve f -> u (device, n^3 real) via the half-spectrum workspace spec.
+cudaError_t gen_poisson_f64(const GenArgs& a, const void* f, void* u, void* spec);
+cudaError_t gen_poisson_f32(const GenArgs& a, const void* f, void* u, void* spec);
+constexpr int kGenLaunches = 7;
+// dft3_forward: real g (n^3) -> complex spec (n^3, interleaved).  dft3_inverse:
+// complex spec -> real g = Re(backward)/n^3 using `work` (n^3 complex) as scratch.
+cudaError_t gen_dft3_forward_f64(const GenArgs& a, const void* g, void* spec);
+cudaError_t gen_dft3_inverse_f64(const GenArgs& a, const void* spec, void* g, void* work);
+cudaError_t gen_dft3_forward_f32(const GenArgs& a, const void* g, void* spec);
+cudaError_t gen_dft3_inverse_f32(const GenArgs& a, const void* spec, void* g, void* work);
+
+}  // namespace arena_fft

@@ -1,0 +1,369 @@
+// plan.cu — the C ABI (include/arena_fft.h): plans, workspace, host boundary.
+//
+// Replaces the per-call FFTW planning/execution of
+// /root/reference/proj/src/fft_solver.cpp:51-87 with a once-per-(n, precision,
+// device) plan ("Setup") whose solve only enqueues kernels.
+// No CPU fallback: a plan can only be created on a device this library was
+// compiled for (sm_100a); anything else is ARENA_EUNSUPPORTED.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/arena_fft.h"
+#include "launchers.h"
+
+using namespace arena_fft;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+arena_status fail(arena_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+arena_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(ARENA_ECUDA, std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+
+bool is_pow2(int n) { return n >= 2 && (n & (n - 1)) == 0; }
+
+const char* kPow2Names[kPow2Launches] = {"zfwd_r2c", "yfwd", "xmid_fwd_scale_inv", "yinv", "zinv_c2r"};
+const char* kGenNames[kGenLaunches] = {"gen_z_r2c", "gen_y_fwd", "gen_x_fwd", "gen_scale",
+                                       "gen_x_inv", "gen_y_inv", "gen_z_c2r"};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct arena_fft_plan {
+  int n = 0, prec = 64, device = 0, path = ARENA_PATH_POW2;
+  int nc = 0, ncp = 0;
+  size_t elem = 8;  // bytes per real
+  void* spec = nullptr;  // half spectrum workspace
+  size_t spec_bytes = 0;
+  void* tw = nullptr;  // W_n^m table, vec2 of the precision
+  GenPlan gplan{};
+  // host-boundary resources (lazily allocated)
+  void* d_in = nullptr;
+  void* d_out = nullptr;
+  void* d_work = nullptr;  // n^3 complex, dft3 only
+  cudaStream_t hstream = nullptr;
+  std::mutex host_mu;  // one host-path call in flight per plan
+  // stage timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  int ev_sets_used = 0;
+  std::vector<double> stage_ms;
+  int solves = 0;
+  std::mutex ev_mu;
+
+  int launches() const { return path == ARENA_PATH_POW2 ? kPow2Launches : kGenLaunches; }
+  size_t real_bytes() const { return size_t(n) * n * n * elem; }
+};
+
+namespace {
+
+arena_status make_twiddles(arena_fft_plan* p) {
+  // W_n^m = exp(-2 pi i m / n), m in [0, n), computed in 80-bit long double
+  // and rounded once to the plan's precision.
+  const int n = p->n;
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  const size_t vb = 2 * p->elem;
+  std::vector<unsigned char> host(size_t(n) * vb);
+  for (int m = 0; m < n; ++m) {
+    const long double a = two_pi * (long double)m / (long double)n;
+    const long double c = cosl(a), s = -sinl(a);
+    if (p->prec == 64) {
+      double v[2] = {double(c), double(s)};
+      memcpy(host.data() + m * vb, v, vb);
+    } else {
+      float v[2] = {float(c), float(s)};
+      memcpy(host.data() + m * vb, v, vb);
+    }
+  }
+  cudaError_t e = cudaMalloc(&p->tw, host.size());
+  if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? fail(ARENA_ENOMEM, "twiddle table") : cuda_fail(e, "cudaMalloc");
+  e = cudaMemcpy(p->tw, host.data(), host.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "twiddle upload");
+  return ARENA_OK;
+}
+
+void free_plan(arena_fft_plan* p) {
+  if (!p) return;
+  DeviceGuard g(p->device);
+  if (p->spec) cudaFree(p->spec);
+  if (p->tw) cudaFree(p->tw);
+  if (p->d_in) cudaFree(p->d_in);
+  if (p->d_out) cudaFree(p->d_out);
+  if (p->d_work) cudaFree(p->d_work);
+  if (p->hstream) cudaStreamDestroy(p->hstream);
+  for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
+  delete p;
+}
+
+// Events for one timed solve (launches + 1), recycled after each query.
+cudaEvent_t* timing_events(arena_fft_plan* p) {
+  if (!p->timing) return nullptr;
+  std::lock_guard<std::mutex> lk(p->ev_mu);
+  const int per = p->launches() + 1;
+  const int need = (p->ev_sets_used + 1) * per;
+  while (int(p->ev_pool.size()) < need) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    p->ev_pool.push_back(e);
+  }
+  cudaEvent_t* ev = p->ev_pool.data() + p->ev_sets_used * per;
+  ++p->ev_sets_used;
+  return ev;
+}
+
+arena_status enqueue_solve(arena_fft_plan* p, const void* d_f, void* d_u, cudaStream_t s) {
+  cudaError_t e;
+  cudaEvent_t* ev = timing_events(p);
+  if (p->path == ARENA_PATH_POW2) {
+    Pow2Args a{d_f, d_u, p->spec, p->tw, p->n, p->nc, p->ncp, s, ev};
+    e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
+  } else {
+    GenArgs a{&p->gplan, p->tw, p->n, p->nc, p->ncp, s, ev};
+    e = p->prec == 64 ? gen_poisson_f64(a, d_f, d_u, p->spec) : gen_poisson_f32(a, d_f, d_u, p->spec);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "poisson solve launch");
+  return ARENA_OK;
+}
+
+arena_status ensure_host_buffers(arena_fft_plan* p, bool work) {
+  cudaError_t e;
+  if (!p->hstream && (e = cudaStreamCreateWithFlags(&p->hstream, cudaStreamNonBlocking)) != cudaSuccess)
+    return cuda_fail(e, "cudaStreamCreate");
+  const size_t cb = size_t(p->n) * p->n * p->n * 2 * p->elem;  // n^3 complex (covers n^3 real)
+  if (!p->d_in && (e = cudaMalloc(&p->d_in, cb)) != cudaSuccess)
+    return fail(ARENA_ENOMEM, "device input buffer: " + std::string(cudaGetErrorString(e)));
+  if (!p->d_out && (e = cudaMalloc(&p->d_out, cb)) != cudaSuccess)
+    return fail(ARENA_ENOMEM, "device output buffer: " + std::string(cudaGetErrorString(e)));
+  if (work && !p->d_work && (e = cudaMalloc(&p->d_work, cb)) != cudaSuccess)
+    return fail(ARENA_ENOMEM, "device work buffer: " + std::string(cudaGetErrorString(e)));
+  return ARENA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* arena_last_error(void) { return g_last_error.c_str(); }
+
+int arena_fft_abi_version(void) { return 100; }
+
+arena_status arena_fft_plan_create(arena_fft_plan** out, int n, int precision_bits, int device) {
+  if (!out) return fail(ARENA_EINVAL, "plan pointer is NULL");
+  *out = nullptr;
+  if (n < 2) return fail(ARENA_EINVAL, "GridField: n >= 2 required");  // grid.hpp:18
+  if (precision_bits != 64 && precision_bits != 32) return fail(ARENA_EINVAL, "precision_bits must be 64 or 32");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return fail(ARENA_EUNSUPPORTED, "no CUDA device visible (this library has no CPU path)");
+  if (device < 0 && cudaGetDevice(&device) != cudaSuccess) return fail(ARENA_ECUDA, "cudaGetDevice");
+  if (device >= ndev) return fail(ARENA_EINVAL, "device ordinal out of range");
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(ARENA_EUNSUPPORTED, "device is sm_" + std::to_string(prop.major * 10 + prop.minor) +
+                                        "; this library is built for sm_100a (B200) only");
+  DeviceGuard g(device);
+  arena_fft_plan* p = new (std::nothrow) arena_fft_plan;
+  if (!p) return fail(ARENA_ENOMEM, "plan");
+  p->n = n;
+  p->prec = precision_bits;
+  p->device = device;
+  p->elem = precision_bits == 64 ? 8 : 4;
+  p->nc = n / 2 + 1;
+  p->ncp = (p->nc + 7) / 8 * 8;
+  if (is_pow2(n) && n <= kPow2MaxN) {
+    p->path = ARENA_PATH_POW2;
+  } else {
+    p->path = ARENA_PATH_GENERIC;
+    if (!gen_plan_make(n, &p->gplan)) {
+      free_plan(p);
+      return fail(ARENA_EUNSUPPORTED, "cannot factor n");
+    }
+    if (n > gen_max_n(int(2 * p->elem))) {
+      free_plan(p);
+      return fail(ARENA_EUNSUPPORTED, "n = " + std::to_string(n) + " exceeds the generic path's shared-memory line limit");
+    }
+  }
+  arena_status st = make_twiddles(p);
+  if (st != ARENA_OK) {
+    free_plan(p);
+    return st;
+  }
+  p->spec_bytes = size_t(n) * n * p->ncp * 2 * p->elem;
+  if ((e = cudaMalloc(&p->spec, p->spec_bytes)) != cudaSuccess) {
+    free_plan(p);
+    return fail(ARENA_ENOMEM, "half-spectrum workspace (" + std::to_string(p->spec_bytes) + " B): " + cudaGetErrorString(e));
+  }
+  *out = p;
+  g_last_error.clear();
+  return ARENA_OK;
+}
+
+void arena_fft_plan_destroy(arena_fft_plan* plan) { free_plan(plan); }
+
+arena_status arena_fft_plan_info(const arena_fft_plan* p, int* n, int* precision_bits, int* path, int* device,
+                                 size_t* workspace_bytes) {
+  if (!p) return fail(ARENA_EINVAL, "plan is NULL");
+  if (n) *n = p->n;
+  if (precision_bits) *precision_bits = p->prec;
+  if (path) *path = p->path;
+  if (device) *device = p->device;
+  if (workspace_bytes) *workspace_bytes = p->spec_bytes;
+  return ARENA_OK;
+}
+
+int arena_poisson_launches_per_solve(const arena_fft_plan* p) { return p ? p->launches() : 0; }
+
+arena_status arena_poisson_solve_device(arena_fft_plan* p, const void* d_f, void* d_u, void* stream) {
+  if (!p || !d_f || !d_u) return fail(ARENA_EINVAL, "NULL plan or buffer");
+  DeviceGuard g(p->device);
+  return enqueue_solve(p, d_f, d_u, static_cast<cudaStream_t>(stream));
+}
+
+arena_status arena_poisson_solve_host(arena_fft_plan* p, const void* f, void* u) {
+  if (!p || !f || !u) return fail(ARENA_EINVAL, "NULL plan or buffer");
+  DeviceGuard g(p->device);
+  std::lock_guard<std::mutex> lk(p->host_mu);
+  arena_status st = ensure_host_buffers(p, false);
+  if (st != ARENA_OK) return st;
+  const size_t bytes = p->real_bytes();
+  cudaError_t e = cudaMemcpyAsync(p->d_in, f, bytes, cudaMemcpyHostToDevice, p->hstream);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D f");
+  if ((st = enqueue_solve(p, p->d_in, p->d_out, p->hstream)) != ARENA_OK) return st;
+  if ((e = cudaMemcpyAsync(u, p->d_out, bytes, cudaMemcpyDeviceToHost, p->hstream)) != cudaSuccess)
+    return cuda_fail(e, "D2H u");
+  if ((e = cudaStreamSynchronize(p->hstream)) != cudaSuccess) return cuda_fail(e, "poisson solve");
+  return ARENA_OK;
+}
+
+static arena_status dft3_fwd_enqueue(arena_fft_plan* p, const void* d_g, void* d_spec, cudaStream_t s) {
+  GenArgs a{nullptr, p->tw, p->n, p->nc, p->ncp, s, nullptr};
+  GenPlan gp;
+  if (!gen_plan_make(p->n, &gp)) return fail(ARENA_EUNSUPPORTED, "cannot factor n");
+  if (p->n > gen_max_n(int(2 * p->elem))) return fail(ARENA_EUNSUPPORTED, "n too large for dft3");
+  a.plan = &gp;
+  cudaError_t e = p->prec == 64 ? gen_dft3_forward_f64(a, d_g, d_spec) : gen_dft3_forward_f32(a, d_g, d_spec);
+  return e == cudaSuccess ? ARENA_OK : cuda_fail(e, "dft3_forward");
+}
+
+static arena_status dft3_inv_enqueue(arena_fft_plan* p, const void* d_spec, void* d_g, void* d_work, cudaStream_t s) {
+  GenArgs a{nullptr, p->tw, p->n, p->nc, p->ncp, s, nullptr};
+  GenPlan gp;
+  if (!gen_plan_make(p->n, &gp)) return fail(ARENA_EUNSUPPORTED, "cannot factor n");
+  if (p->n > gen_max_n(int(2 * p->elem))) return fail(ARENA_EUNSUPPORTED, "n too large for dft3");
+  a.plan = &gp;
+  cudaError_t e = p->prec == 64 ? gen_dft3_inverse_f64(a, d_spec, d_g, d_work)
+                                : gen_dft3_inverse_f32(a, d_spec, d_g, d_work);
+  return e == cudaSuccess ? ARENA_OK : cuda_fail(e, "dft3_inverse");
+}
+
+arena_status arena_dft3_forward_device(arena_fft_plan* p, const void* d_g, void* d_spec, void* stream) {
+  if (!p || !d_g || !d_spec) return fail(ARENA_EINVAL, "NULL plan or buffer");
+  DeviceGuard g(p->device);
+  return dft3_fwd_enqueue(p, d_g, d_spec, static_cast<cudaStream_t>(stream));
+}
+
+arena_status arena_dft3_inverse_device(arena_fft_plan* p, const void* d_spec, void* d_g, void* stream) {
+  if (!p || !d_spec || !d_g) return fail(ARENA_EINVAL, "NULL plan or buffer");
+  DeviceGuard g(p->device);
+  std::lock_guard<std::mutex> lk(p->host_mu);  // d_work is plan-owned
+  arena_status st = ensure_host_buffers(p, true);
+  if (st != ARENA_OK) return st;
+  return dft3_inv_enqueue(p, d_spec, d_g, p->d_work, static_cast<cudaStream_t>(stream));
+}
+
+arena_status arena_dft3_forward_host(arena_fft_plan* p, const void* g_host, void* spec_host) {
+  if (!p || !g_host || !spec_host) return fail(ARENA_EINVAL, "NULL plan or buffer");
+  DeviceGuard g(p->device);
+  std::lock_guard<std::mutex> lk(p->host_mu);
+  arena_status st = ensure_host_buffers(p, false);
+  if (st != ARENA_OK) return st;
+  cudaError_t e = cudaMemcpyAsync(p->d_in, g_host, p->real_bytes(), cudaMemcpyHostToDevice, p->hstream);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D g");
+  if ((st = dft3_fwd_enqueue(p, p->d_in, p->d_out, p->hstream)) != ARENA_OK) return st;
+  if ((e = cudaMemcpyAsync(spec_host, p->d_out, 2 * p->real_bytes(), cudaMemcpyDeviceToHost, p->hstream)))
+    return cuda_fail(e, "D2H spec");
+  if ((e = cudaStreamSynchronize(p->hstream)) != cudaSuccess) return cuda_fail(e, "dft3_forward");
+  return ARENA_OK;
+}
+
+arena_status arena_dft3_inverse_host(arena_fft_plan* p, const void* spec_host, void* g_host) {
+  if (!p || !spec_host || !g_host) return fail(ARENA_EINVAL, "NULL plan or buffer");
+  DeviceGuard g(p->device);
+  std::lock_guard<std::mutex> lk(p->host_mu);
+  arena_status st = ensure_host_buffers(p, true);
+  if (st != ARENA_OK) return st;
+  cudaError_t e = cudaMemcpyAsync(p->d_in, spec_host, 2 * p->real_bytes(), cudaMemcpyHostToDevice, p->hstream);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D spec");
+  if ((st = dft3_inv_enqueue(p, p->d_in, p->d_out, p->d_work, p->hstream)) != ARENA_OK) return st;
+  if ((e = cudaMemcpyAsync(g_host, p->d_out, p->real_bytes(), cudaMemcpyDeviceToHost, p->hstream)))
+    return cuda_fail(e, "D2H g");
+  if ((e = cudaStreamSynchronize(p->hstream)) != cudaSuccess) return cuda_fail(e, "dft3_inverse");
+  return ARENA_OK;
+}
+
+arena_status arena_fft_set_stage_timing(arena_fft_plan* p, int enable) {
+  if (!p) return fail(ARENA_EINVAL, "plan is NULL");
+  std::lock_guard<std::mutex> lk(p->ev_mu);
+  p->timing = enable != 0;
+  p->ev_sets_used = 0;
+  p->stage_ms.assign(p->launches(), 0.0);
+  p->solves = 0;
+  return ARENA_OK;
+}
+
+arena_status arena_fft_stage_times(arena_fft_plan* p, double* ms, const char** names, int max_stages, int* n_stages,
+                                   int* n_solves) {
+  if (!p) return fail(ARENA_EINVAL, "plan is NULL");
+  DeviceGuard g(p->device);
+  std::lock_guard<std::mutex> lk(p->ev_mu);
+  const int L = p->launches(), per = L + 1;
+  if (int(p->stage_ms.size()) != L) p->stage_ms.assign(L, 0.0);
+  for (int s = 0; s < p->ev_sets_used; ++s) {
+    cudaEvent_t* ev = p->ev_pool.data() + s * per;
+    cudaError_t e = cudaEventSynchronize(ev[L]);
+    if (e != cudaSuccess) return cuda_fail(e, "stage timing sync");
+    for (int k = 0; k < L; ++k) {
+      float t = 0;
+      if ((e = cudaEventElapsedTime(&t, ev[k], ev[k + 1])) != cudaSuccess) return cuda_fail(e, "cudaEventElapsedTime");
+      p->stage_ms[k] += t;
+    }
+    ++p->solves;
+  }
+  p->ev_sets_used = 0;
+  const char** nm = p->path == ARENA_PATH_POW2 ? kPow2Names : kGenNames;
+  for (int k = 0; k < L && k < max_stages; ++k) {
+    if (ms) ms[k] = p->stage_ms[k];
+    if (names) names[k] = nm[k];
+  }
+  if (n_stages) *n_stages = L;
+  if (n_solves) *n_solves = p->solves;
+  return ARENA_OK;
+}
+
+}  // extern "C"

@@ -99,6 +99,12 @@ arena_status arena_source_modes(int n, int precision_bits, int nmodes, const int
 arena_status arena_source_gaussian(int n, int precision_bits, double alpha, double cx, double cy, double cz, int which,
                                    void* d_out, void* stream);
 
+/* Tile geometry of the power-of-two kernels for (n, precision): out15[0..4] =
+ * {line length, points/thread, lines/CTA, threads/CTA, shared bytes} of the
+ * contiguous-axis (z) kernels, out15[5..9] the y kernels, out15[10..14] the x
+ * kernel.  Host-only (no device needed); used by the CPU index-model tests. */
+int arena_pow2_kernel_geometry(int n, int precision_bits, int* out15);
+
 /* Thread-local description of the last failure on this thread ("" if none). */
 const char* arena_last_error(void);
 

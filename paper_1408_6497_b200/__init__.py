@@ -25,7 +25,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_DIR = os.path.join(_HERE, "lib")
+LIB_DIR = os.environ.get("ARENA_FFT_LIB_DIR", os.path.join(_HERE, "lib"))  # override: kernel-variant experiments
 LIB_PATH = os.path.join(LIB_DIR, "libarena_fft.so")
 CORE_PATH = os.path.join(LIB_DIR, "libarena_core.so")
 REPO_ROOT = os.path.dirname(_HERE)

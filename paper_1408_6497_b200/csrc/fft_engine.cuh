@@ -209,11 +209,25 @@ __device__ __forceinline__ int smem_idx(int pos, int l) {
   }
 }
 
+// Twiddle table reads: read-only global path, or a plain load when the table
+// was staged in shared memory (ARENA_TW_SMEM).
+#ifndef ARENA_TW_SMEM
+#define ARENA_TW_SMEM 0
+#endif
+template <typename V>
+__device__ __forceinline__ V tw_load(const V* __restrict__ tw, int idx) {
+#if ARENA_TW_SMEM
+  return tw[idx];
+#else
+  return __ldg(tw + idx);
+#endif
+}
+
 // Table twiddle W_N^m (forward) for an N-point line; `tw` holds W_NT^j for
 // j in [0, NT) and TWMUL = NT / N.
 template <int S, typename V>
 __device__ __forceinline__ V tw_apply(V a, const V* __restrict__ tw, int idx) {
-  const V w = __ldg(tw + idx);
+  const V w = tw_load(tw, idx);
   return S < 0 ? cmul(a, w) : cmulc(a, w);
 }
 

@@ -9,6 +9,14 @@ namespace arena_fft {
 constexpr int kPow2MaxN = 2048;
 constexpr int kPow2Launches = 5;
 
+// Plan-owned cache of the TMA descriptors over the half spectrum (encoded on
+// first use; they depend only on the workspace address and n).
+struct alignas(64) TmaCache {
+  unsigned char maps[2][128];  // CUtensorMap for the y and the x boxes
+  const void* spec = nullptr;  // workspace the maps were encoded for
+  int n = 0;
+};
+
 struct Pow2Args {
   const void* f;
   void* u;
@@ -17,10 +25,20 @@ struct Pow2Args {
   int n, nc, ncp;
   cudaStream_t stream;
   cudaEvent_t* ev;  // nullable; kPow2Launches + 1 events: before each kernel and after the last
+  TmaCache* tma;    // nullable: classic (non-TMA) strided kernels
+  int sm_count;
 };
 
 cudaError_t launch_pow2_f64(const Pow2Args& a);
 cudaError_t launch_pow2_f32(const Pow2Args& a);
+
+// Line length, points per thread, lines per CTA, threads, shared bytes.
+struct KernelGeom {
+  int line, E, L, threads, smem;
+};
+// g[0]: z kernels (M = n/2 point lines), g[1]: y kernels, g[2]: x kernel (n-point lines).
+bool pow2_config_f64(int n, KernelGeom* g);
+bool pow2_config_f32(int n, KernelGeom* g);
 
 // Generic mixed-radix path (any n >= 2).  One Stockham plan for an n-point line.
 constexpr int kGenMaxStages = 40;

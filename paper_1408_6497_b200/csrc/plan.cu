@@ -9,6 +9,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -62,6 +63,8 @@ struct arena_fft_plan {
   size_t spec_bytes = 0;
   void* tw = nullptr;  // W_n^m table, vec2 of the precision
   GenPlan gplan{};
+  TmaCache* tma = nullptr;  // TMA descriptors (power-of-two path), nullptr = classic kernels
+  int sm_count = 148;
   // host-boundary resources (lazily allocated)
   void* d_in = nullptr;
   void* d_out = nullptr;
@@ -116,6 +119,7 @@ void free_plan(arena_fft_plan* p) {
   if (p->d_out) cudaFree(p->d_out);
   if (p->d_work) cudaFree(p->d_work);
   if (p->hstream) cudaStreamDestroy(p->hstream);
+  delete p->tma;
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   delete p;
 }
@@ -140,7 +144,7 @@ arena_status enqueue_solve(arena_fft_plan* p, const void* d_f, void* d_u, cudaSt
   cudaError_t e;
   cudaEvent_t* ev = timing_events(p);
   if (p->path == ARENA_PATH_POW2) {
-    Pow2Args a{d_f, d_u, p->spec, p->tw, p->n, p->nc, p->ncp, s, ev};
+    Pow2Args a{d_f, d_u, p->spec, p->tw, p->n, p->nc, p->ncp, s, ev, p->tma, p->sm_count};
     e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
   } else {
     GenArgs a{&p->gplan, p->tw, p->n, p->nc, p->ncp, s, ev};
@@ -196,8 +200,11 @@ arena_status arena_fft_plan_create(arena_fft_plan** out, int n, int precision_bi
   p->elem = precision_bits == 64 ? 8 : 4;
   p->nc = n / 2 + 1;
   p->ncp = (p->nc + 7) / 8 * 8;
+  p->sm_count = prop.multiProcessorCount;
   if (is_pow2(n) && n <= kPow2MaxN) {
     p->path = ARENA_PATH_POW2;
+    const char* kern = std::getenv("ARENA_FFT_KERNELS");  // "classic" selects the non-TMA strided kernels
+    if (!(kern && std::string(kern) == "classic")) p->tma = new (std::nothrow) TmaCache;
   } else {
     p->path = ARENA_PATH_GENERIC;
     if (!gen_plan_make(n, &p->gplan)) {
@@ -238,6 +245,21 @@ arena_status arena_fft_plan_info(const arena_fft_plan* p, int* n, int* precision
 }
 
 int arena_poisson_launches_per_solve(const arena_fft_plan* p) { return p ? p->launches() : 0; }
+
+int arena_pow2_kernel_geometry(int n, int precision_bits, int* out15) {
+  KernelGeom g[3];
+  const bool ok = precision_bits == 64 ? pow2_config_f64(n, g) : pow2_config_f32(n, g);
+  if (!ok || !out15) return ARENA_EINVAL;
+  int* out10 = out15;
+  for (int i = 0; i < 3; ++i) {
+    out10[5 * i + 0] = g[i].line;
+    out10[5 * i + 1] = g[i].E;
+    out10[5 * i + 2] = g[i].L;
+    out10[5 * i + 3] = g[i].threads;
+    out10[5 * i + 4] = g[i].smem;
+  }
+  return ARENA_OK;
+}
 
 arena_status arena_poisson_solve_device(arena_fft_plan* p, const void* d_f, void* d_u, void* stream) {
   if (!p || !d_f || !d_u) return fail(ARENA_EINVAL, "NULL plan or buffer");

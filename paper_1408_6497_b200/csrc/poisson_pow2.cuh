@@ -24,36 +24,79 @@ namespace arena_fft {
 
 __host__ __device__ constexpr int imin(int a, int b) { return a < b ? a : b; }
 __host__ __device__ constexpr int imax(int a, int b) { return a > b ? a : b; }
+__host__ __device__ constexpr int pow2_floor(int x) { return x <= 1 ? 1 : 2 * pow2_floor(x / 2); }
+
+// Row pitch (complex elements) of the half spectrum for an n-point grid; the
+// plan allocates with the same formula (plan.cu).
+__host__ __device__ constexpr int spec_pitch(int n) { return (n / 2 + 1 + 7) / 8 * 8; }
+
+// Tuning knobs (compile-time; variants are built side by side for A/B runs).
+#ifndef ARENA_STRIDED_MINB
+#define ARENA_STRIDED_MINB 2  // min CTAs/SM hint for the strided (y, x) kernels
+#endif
+#ifndef ARENA_CONTIG_MINB
+#define ARENA_CONTIG_MINB 2  // min CTAs/SM hint for the contiguous (z) kernels
+#endif
+#ifndef ARENA_STRIDED_E
+#define ARENA_STRIDED_E 16  // points per thread, y / x kernels
+#endif
+#ifndef ARENA_CONTIG_E
+#define ARENA_CONTIG_E 16  // points per thread, z kernels
+#endif
+#ifndef ARENA_Y_SMEM
+#define ARENA_Y_SMEM (64 * 1024)  // shared-memory budget per y tile (sets its width L)
+#endif
+#ifndef ARENA_X_SMEM
+#define ARENA_X_SMEM (64 * 1024)  // shared-memory budget per x tile
+#endif
+#ifndef ARENA_JBLOCK
+#define ARENA_JBLOCK 8  // j-block of the half-spectrum layout (see row_off)
+#endif
 
 // ------------------------------------------------------------ configuration
 // E: points per thread; L: lines per CTA.  Shared memory per CTA is
 // N*L*sizeof(V) (<= 64 KB so two or more CTAs fit per SM).
-template <typename T, int N>
-struct StridedCfg {  // y / x passes: lines along a strided axis, L adjacent k
-  static constexpr int E = imin(16, N);
+template <typename T, int N, int PASS = 0>
+struct StridedCfg {  // y (PASS 0) / x (PASS 1) passes: lines along a strided axis, L adjacent k
+  static constexpr int E = imin(ARENA_STRIDED_E, N);
   static constexpr int VB = 2 * sizeof(T);
-  static constexpr int L = imax(1, imin(8, (64 * 1024) / (N * VB)));
+  static constexpr int BUDGET = PASS == 0 ? ARENA_Y_SMEM : ARENA_X_SMEM;
+  static constexpr int L = pow2_floor(imax(1, imin(8, BUDGET / (N * VB))));
   static constexpr int P = N / E;
   static constexpr int THREADS = L * P;
-  static constexpr int SMEM = N * L * VB;
+  static constexpr int SMEM_X = N * L * VB;                   // exchange buffer bytes
+  static constexpr int SMEM = SMEM_X + (ARENA_TW_SMEM ? N * VB : 0);
 };
 
 template <typename T, int NR>
 struct ContigCfg {  // z passes: rows of NR reals = M = NR/2 complex
   static constexpr int M = NR / 2;
-  static constexpr int E = imin(16, M);
+  static constexpr int E = imin(ARENA_CONTIG_E, M);
   static constexpr int P = M / E;
   static constexpr int VB = 2 * sizeof(T);
-  // rows per CTA: aim for 256 threads, at least 8 rows, at most 64 KB smem,
-  // never more rows than the grid has (n^2).
+  // rows per CTA (a power of two, so it divides the n^2 rows): aim for 256
+  // threads and at least 8 rows, at most ~96 KB of shared memory.
   static constexpr int L0 = imax(8, 256 / P);
-  static constexpr int L1 = imin(L0, imax(1, (64 * 1024) / ((M + 1) * VB)));
-  static constexpr int L = imin(L1, NR * NR);
+  static constexpr int L1 = imin(L0, imax(1, (96 * 1024) / ((M + 1) * VB)));
+  static constexpr int L = pow2_floor(imin(L1, NR * NR));
   static constexpr int THREADS = L * P;
-  static constexpr int SMEM = (M * L + L) * VB;
+  static constexpr int SMEM_X = (M * L + L) * VB;
+  static constexpr int SMEM = SMEM_X + (ARENA_TW_SMEM ? NR * VB : 0);
 };
 
 __device__ __forceinline__ int signed_freq(int k, int n) { return k <= n / 2 ? k : k - n; }  // fft_solver.hpp:19
+
+// Half-spectrum row (i, j) offset in elements.  Rows are grouped in blocks of
+// JB consecutive j: S[(((j / JB) * n + i) * JB + j % JB) * ncp + k].  A y tile
+// (fixed i) then reads n/JB contiguous JB-row chunks and an x tile (fixed j)
+// reads rows JB*ncp apart, so both strided passes touch O(n/JB) and
+// O(JB*ncp*16 B*n / 2 MB) pages instead of 5 and n (the row-major x pass ran
+// at 3.1 TB/s on B200, TLB-bound; tools/pattern_bw.cu).
+template <int N>
+__host__ __device__ __forceinline__ size_t row_off(int i, int j) {
+  constexpr int JB = ARENA_JBLOCK < N ? ARENA_JBLOCK : N;
+  return ((size_t(j / JB) * N + i) * JB + (j % JB)) * size_t(spec_pitch(N));
+}
 
 template <typename V>
 __device__ __forceinline__ V* smem_base() {
@@ -61,21 +104,38 @@ __device__ __forceinline__ V* smem_base() {
   return reinterpret_cast<V*>(arena_smem_raw);
 }
 
+// The twiddle table the engine reads: the global table, or (ARENA_TW_SMEM) a
+// copy staged once per CTA after the exchange buffer (SX bytes).
+template <typename V, int NT, int SX>
+__device__ __forceinline__ const V* stage_twiddles(const V* __restrict__ tw) {
+#if ARENA_TW_SMEM
+  V* t = reinterpret_cast<V*>(reinterpret_cast<unsigned char*>(smem_base<V>()) + SX);
+  for (int i = threadIdx.x; i < NT; i += blockDim.x) t[i] = __ldg(tw + i);
+  __syncthreads();
+  return t;
+#else
+  return tw;
+#endif
+}
+
 // ------------------------------------------------------------------- K1 zfwd
 // Rows of NR reals: z[m] = f[2m] + i f[2m+1] (one vector load), M-point FFT,
 // then X[k] = 1/2 (A + B) - 1/2 i W_n^k (A - B), A = Z[k], B = conj(Z[M-k]),
 // for k in [0, M]; X[M] = Re Z0 - Im Z0.
 template <typename T, int NR>
-__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS)
-    k_zfwd(const T* __restrict__ f, vec2_t<T>* __restrict__ S, int ncp, const vec2_t<T>* __restrict__ tw) {
+__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
+    k_zfwd(const T* __restrict__ f, vec2_t<T>* __restrict__ S, const vec2_t<T>* tw) {
   using V = vec2_t<T>;
   using C = ContigCfg<T, NR>;
   constexpr int M = C::M, E = C::E, P = C::P, L = C::L;
+  constexpr int ncp = spec_pitch(NR);
   constexpr int SW = engine_swizzle<M, E>();
   V* sm = smem_base<V>();
+  tw = stage_twiddles<V, NR, C::SMEM_X>(tw);
   const int l = threadIdx.x % L, t = threadIdx.x / L;
   const size_t row = size_t(blockIdx.x) * L + l;
   const V* src = reinterpret_cast<const V*>(f + row * NR);
+  (void)ncp;
   V v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = __ldcs(src + t + P * e);
@@ -83,14 +143,14 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS)
 #pragma unroll
   for (int e = 0; e < E; ++e) sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
   __syncthreads();
-  V* dst = S + row * ncp;
+  V* dst = S + row_off<NR>(int(row / NR), int(row % NR));
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int k = t + P * e;
     const V A = v[e];
     const V Bc = sm[smem_idx<L, SW, V>((M - k) & (M - 1), l)];
     const V B{Bc.x, -Bc.y};
-    const V W = __ldg(tw + k);  // W_n^k
+    const V W = tw_load(tw, k);  // W_n^k
     const V WD = cmul(W, csub(A, B));
     dst[k] = V{T(0.5) * (A.x + B.x + WD.y), T(0.5) * (A.y + B.y - WD.x)};
     if (k == 0) dst[M] = V{A.x - A.y, T(0)};
@@ -102,17 +162,20 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS)
 // ignored): Z[k] = (A + B) + i (A - B) conj(W_n^k), A = X[k], B = conj(X[M-k]),
 // M-point backward FFT, u[2m] = Re z[m], u[2m+1] = Im z[m].
 template <typename T, int NR>
-__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS)
-    k_zinv(const vec2_t<T>* __restrict__ S, T* __restrict__ u, int ncp, const vec2_t<T>* __restrict__ tw) {
+__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
+    k_zinv(const vec2_t<T>* __restrict__ S, T* __restrict__ u, const vec2_t<T>* tw) {
   using V = vec2_t<T>;
   using C = ContigCfg<T, NR>;
   constexpr int M = C::M, E = C::E, P = C::P, L = C::L;
+  constexpr int ncp = spec_pitch(NR);
   constexpr int SW = engine_swizzle<M, E>();
   V* sm = smem_base<V>();
+  tw = stage_twiddles<V, NR, C::SMEM_X>(tw);
   V* xm = sm + M * L;  // X[M] per line
   const int l = threadIdx.x % L, t = threadIdx.x / L;
   const size_t row = size_t(blockIdx.x) * L + l;
-  const V* src = S + row * ncp;
+  const V* src = S + row_off<NR>(int(row / NR), int(row % NR));
+  (void)ncp;
   V v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -131,7 +194,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS)
       Bs.y = T(0);
     }
     const V B{Bs.x, -Bs.y};
-    const V W = __ldg(tw + k);
+    const V W = tw_load(tw, k);
     const V Ep = cadd(A, B);
     const V Op = cmulc(csub(A, B), W);
     v[e] = V{Ep.x - Op.y, Ep.y + Op.x};
@@ -145,23 +208,27 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS)
 
 // --------------------------------------------------------------- K2/K4 ypass
 template <typename T, int N, int S>
-__global__ void __launch_bounds__(StridedCfg<T, N>::THREADS)
-    k_ypass(vec2_t<T>* __restrict__ spec, int ncp, int nc, const vec2_t<T>* __restrict__ tw) {
+__global__ void __launch_bounds__(StridedCfg<T, N, 0>::THREADS, ARENA_STRIDED_MINB)
+    k_ypass(vec2_t<T>* __restrict__ spec, const vec2_t<T>* tw) {
   using V = vec2_t<T>;
-  using C = StridedCfg<T, N>;
+  using C = StridedCfg<T, N, 0>;
   constexpr int E = C::E, P = C::P, L = C::L;
+  constexpr int ncp = spec_pitch(N), nc = N / 2 + 1;
   V* sm = smem_base<V>();
+  tw = stage_twiddles<V, N, C::SMEM_X>(tw);
   const int l = threadIdx.x % L, t = threadIdx.x / L;
   const int k = blockIdx.x * L + l;
   const bool valid = k < nc;
-  V* base = spec + size_t(blockIdx.y) * N * ncp + k;
+  V* base = spec + k;
+  const int i = blockIdx.y;
+  (void)ncp;
   V v[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) v[e] = valid ? __ldcs(base + size_t(t + P * e) * ncp) : V{T(0), T(0)};
+  for (int e = 0; e < E; ++e) v[e] = valid ? __ldcs(base + row_off<N>(i, t + P * e)) : V{T(0), T(0)};
   line_fft<N, E, L, S>(v, sm, tw, 1, t, l);
   if (valid) {
 #pragma unroll
-    for (int e = 0; e < E; ++e) __stcs(base + size_t(t + P * e) * ncp, v[e]);
+    for (int e = 0; e < E; ++e) __stcs(base + row_off<N>(i, t + P * e), v[e]);
   }
 }
 
@@ -171,18 +238,20 @@ __global__ void __launch_bounds__(StridedCfg<T, N>::THREADS)
 // exact integer squares), backward FFT along i.  The data never leaves
 // registers between the two transforms.
 template <typename T, int N>
-__global__ void __launch_bounds__(StridedCfg<T, N>::THREADS)
-    k_xmid(vec2_t<T>* __restrict__ spec, int ncp, int nc, const vec2_t<T>* __restrict__ tw, T scale, T four_pi2) {
+__global__ void __launch_bounds__(StridedCfg<T, N, 1>::THREADS, ARENA_STRIDED_MINB)
+    k_xmid(vec2_t<T>* __restrict__ spec, const vec2_t<T>* tw, T scale, T four_pi2) {
   using V = vec2_t<T>;
-  using C = StridedCfg<T, N>;
+  using C = StridedCfg<T, N, 1>;
   constexpr int E = C::E, P = C::P, L = C::L;
+  constexpr int ncp = spec_pitch(N), nc = N / 2 + 1;
   V* sm = smem_base<V>();
+  tw = stage_twiddles<V, N, C::SMEM_X>(tw);
   const int l = threadIdx.x % L, t = threadIdx.x / L;
   const int k = blockIdx.x * L + l;
   const int j = blockIdx.y;
   const bool valid = k < nc;
-  const size_t istride = size_t(N) * ncp;
-  V* base = spec + size_t(j) * ncp + k;
+  const size_t istride = row_off<N>(1, j) - row_off<N>(0, j);  // JB * ncp
+  V* base = spec + row_off<N>(0, j) + k;
   V v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = valid ? __ldcs(base + size_t(t + P * e) * istride) : V{T(0), T(0)};
@@ -201,6 +270,122 @@ __global__ void __launch_bounds__(StridedCfg<T, N>::THREADS)
   if (valid) {
 #pragma unroll
     for (int e = 0; e < E; ++e) __stcs(base + size_t(t + P * e) * istride, v[e]);
+  }
+}
+
+}  // namespace arena_fft
+
+// ===================================================================== TMA path
+// Persistent, software-pipelined versions of the strided passes: one CTA per
+// SM walks the tiles; while it transforms tile g (registers + the tile's own
+// shared buffer as exchange scratch), the tensor-memory accelerator streams
+// tile g + gridDim.x into the other buffer.  Loads therefore never stall the
+// FFT and need no per-thread address arithmetic; stores go straight from
+// registers.
+#include "async_copy.cuh"
+
+namespace arena_fft {
+
+template <typename T, int N>
+struct TmaCfg {
+  static constexpr int VB = 2 * sizeof(T);
+  static constexpr int E = imin(ARENA_STRIDED_E, N);
+  static constexpr int P = N / E;
+  static constexpr int L = pow2_floor(imax(2, imin(8, (64 * 1024) / (N * VB))));
+  static constexpr int THREADS = L * P;
+  static constexpr int NC = N / 2 + 1;
+  static constexpr int KT = (NC + L - 1) / L;  // k tiles per (i) or (j)
+  static constexpr int TILE = N * L;          // elements per tile
+  static constexpr int JB = ARENA_JBLOCK < N ? ARENA_JBLOCK : N;
+  static constexpr int IB = N < 256 ? N : 256;  // TMA box rows for the x pass
+  static constexpr int SMEM = 2 * TILE * VB + 16;
+};
+
+// PASS 0: y forward, 1: y backward, 2: x forward * Poisson symbol * x backward.
+template <typename T, int N, int PASS>
+__global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, 1)
+    k_strided_tma(const __grid_constant__ CUtensorMap tmap, vec2_t<T>* __restrict__ spec,
+                  const vec2_t<T>* __restrict__ tw, T scale, T four_pi2) {
+  using V = vec2_t<T>;
+  using C = TmaCfg<T, N>;
+  constexpr int E = C::E, P = C::P, L = C::L, KT = C::KT, TILE = C::TILE;
+  constexpr int NT = N * KT;
+  constexpr uint32_t TILE_BYTES = TILE * sizeof(V);
+  V* buf0 = smem_base<V>();
+  V* buf1 = buf0 + TILE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(buf1 + TILE);
+  const int tid = threadIdx.x;
+  const int l = tid % L, t = tid / L;
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int g, V* dst, uint64_t* b) {
+    const int outer = g / KT, kt = g % KT;
+    mbar_arrive_expect_tx(b, TILE_BYTES);
+    if constexpr (PASS < 2) {  // y tile: fixed i = outer, all j (JB-row chunks)
+      tma_load_4d(dst, &tmap, b, 2 * kt * L, 0, outer, 0);
+    } else {  // x tile: fixed j = outer, all i in boxes of IB rows
+#pragma unroll
+      for (int q = 0; q < N / C::IB; ++q)
+        tma_load_4d(dst + q * C::IB * L, &tmap, b, 2 * kt * L, outer % C::JB, q * C::IB, outer / C::JB);
+    }
+  };
+
+  int g = blockIdx.x;
+  if (tid == 0 && g < NT) issue(g, buf0, &bar[0]);
+  for (int it = 0; g < NT; ++it, g += gridDim.x) {
+    V* cur = (it & 1) ? buf1 : buf0;
+    V* nxt = (it & 1) ? buf0 : buf1;
+    const int gn = g + gridDim.x;
+    if (tid == 0 && gn < NT) {
+      fence_proxy_async_smem();
+      issue(gn, nxt, &bar[(it & 1) ^ 1]);
+    }
+    mbar_wait(&bar[it & 1], (it >> 1) & 1);
+    V v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = cur[(t + P * e) * L + l];
+    __syncthreads();  // the tile buffer becomes exchange scratch
+    const int outer = g / KT;
+    const int k = (g % KT) * L + l;
+    if constexpr (PASS == 0) {
+      line_fft<N, E, L, -1>(v, cur, tw, 1, t, l);
+    } else if constexpr (PASS == 1) {
+      line_fft<N, E, L, +1>(v, cur, tw, 1, t, l);
+    } else {
+      line_fft<N, E, L, -1>(v, cur, tw, 1, t, l);
+      const int j = outer;
+      const T kj = T(signed_freq(j, N)), kk = T(k);
+      const T c = kj * kj + kk * kk;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const T ki = T(signed_freq(t + P * e, N));
+        const T k2 = ki * ki + c;
+        const T m = (k2 == T(0)) ? T(0) : scale / (four_pi2 * k2);
+        v[e].x *= m;
+        v[e].y *= m;
+      }
+      line_fft<N, E, L, +1>(v, cur, tw, 1, t, l);
+    }
+    if (k < C::NC) {
+      if constexpr (PASS < 2) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) __stcs(spec + row_off<N>(outer, t + P * e) + k, v[e]);
+      } else {
+        V* base = spec + row_off<N>(0, outer) + k;
+        constexpr size_t istride = size_t(C::JB) * spec_pitch(N);
+#pragma unroll
+        for (int e = 0; e < E; ++e) __stcs(base + size_t(t + P * e) * istride, v[e]);
+      }
+    }
+    // No barrier needed here: every thread's last access to `cur` (the tile
+    // read, or the last exchange read) is followed by a __syncthreads, so
+    // thread 0 only refills it next iteration after all threads are done.
   }
 }
 

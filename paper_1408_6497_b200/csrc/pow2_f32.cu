@@ -3,4 +3,5 @@
 
 namespace arena_fft {
 cudaError_t launch_pow2_f32(const Pow2Args& a) { return launch_pow2<float>(a); }
+bool pow2_config_f32(int n, KernelGeom* g) { return pow2_config<float>(n, g); }
 }  // namespace arena_fft

@@ -3,4 +3,5 @@
 
 namespace arena_fft {
 cudaError_t launch_pow2_f64(const Pow2Args& a) { return launch_pow2<double>(a); }
+bool pow2_config_f64(int n, KernelGeom* g) { return pow2_config<double>(n, g); }
 }  // namespace arena_fft

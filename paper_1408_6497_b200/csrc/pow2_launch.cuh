@@ -5,15 +5,19 @@
 
 #include <atomic>
 
+#include <cudaTypedefs.h>
+
 #include "launchers.h"
 #include "poisson_pow2.cuh"
 
 namespace arena_fft {
 
-// Raise the dynamic shared-memory limit of a kernel once per device (the
-// kernel is a template argument so each instantiation has its own flag).
+// Raise the dynamic shared-memory limit of a kernel once per device and pick
+// the smallest shared-memory carveout that still holds every CTA the register
+// file allows (the rest stays L1).  The kernel is a template argument so each
+// instantiation has its own flag.
 template <auto kernel>
-inline cudaError_t ensure_smem(int bytes) {
+inline cudaError_t ensure_smem(int bytes, int threads) {
   static std::atomic<unsigned long long> done_mask{0};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -24,8 +28,72 @@ inline cudaError_t ensure_smem(int bytes) {
     e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return e;
   }
+  int blocks = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, bytes);
+  if (e != cudaSuccess) return e;
+  const int per_block = bytes + 1024;  // + driver-reserved shared memory per CTA
+  int pct = (blocks * per_block * 100 + 228 * 1024 - 1) / (228 * 1024);
+  pct = pct < 0 ? 0 : (pct > 100 ? 100 : pct);
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  if (e != cudaSuccess) return e;
   done_mask.fetch_or(bit);
   return cudaSuccess;
+}
+
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Half spectrum as a 4-D tensor of reals: {2*nc (re/im of k), JB (j % JB),
+// n (i), n/JB (j / JB)} — the blocked layout of row_off().
+template <typename T, int N>
+cudaError_t encode_spec_maps(TmaCache* c, void* spec) {
+  using C = TmaCfg<T, N>;
+  auto enc = tensor_map_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  const CUtensorMapDataType dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const cuuint64_t row = cuuint64_t(spec_pitch(N)) * 2 * sizeof(T);
+  const cuuint64_t dims[4] = {cuuint64_t(2 * C::NC), cuuint64_t(C::JB), cuuint64_t(N), cuuint64_t(N / C::JB)};
+  const cuuint64_t strides[3] = {row, row * C::JB, row * C::JB * N};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const cuuint32_t box_y[4] = {cuuint32_t(2 * C::L), cuuint32_t(C::JB), 1, cuuint32_t(N / C::JB)};
+  const cuuint32_t box_x[4] = {cuuint32_t(2 * C::L), 1, cuuint32_t(C::IB), 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(c->maps[0]), dt, 4, spec, dims, strides, box_y, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  r = enc(reinterpret_cast<CUtensorMap*>(c->maps[1]), dt, 4, spec, dims, strides, box_x, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  c->spec = spec;
+  c->n = N;
+  return cudaSuccess;
+}
+
+template <typename T, int N, int PASS>
+cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, T scale, T four_pi2) {
+  using C = TmaCfg<T, N>;
+  using V = vec2_t<T>;
+  auto kern = k_strided_tma<T, N, PASS>;
+  cudaError_t e = ensure_smem<k_strided_tma<T, N, PASS>>(C::SMEM, C::THREADS);
+  if (e) return e;
+  int per_sm = 1;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM))) return e;
+  const int tiles = N * C::KT;
+  int grid = a.sm_count * (per_sm > 0 ? per_sm : 1);
+  if (grid > tiles) grid = tiles;
+  kern<<<grid, C::THREADS, C::SMEM, a.stream>>>(map, static_cast<V*>(a.spec), static_cast<const V*>(a.tw), scale,
+                                               four_pi2);
+  return cudaGetLastError();
 }
 
 inline void mark(const Pow2Args& a, int i) {
@@ -36,31 +104,80 @@ template <typename T, int NR>
 cudaError_t launch_pow2_n(const Pow2Args& a) {
   using V = vec2_t<T>;
   using CC = ContigCfg<T, NR>;
-  using SC = StridedCfg<T, NR>;
+  using SC = StridedCfg<T, NR, 0>;
+  using XC = StridedCfg<T, NR, 1>;
   const V* tw = static_cast<const V*>(a.tw);
   V* S = static_cast<V*>(a.spec);
   cudaError_t e;
-  if ((e = ensure_smem<k_zfwd<T, NR>>(CC::SMEM))) return e;
-  if ((e = ensure_smem<k_zinv<T, NR>>(CC::SMEM))) return e;
-  if ((e = ensure_smem<k_ypass<T, NR, -1>>(SC::SMEM))) return e;
-  if ((e = ensure_smem<k_ypass<T, NR, +1>>(SC::SMEM))) return e;
-  if ((e = ensure_smem<k_xmid<T, NR>>(SC::SMEM))) return e;
+  if ((e = ensure_smem<k_zfwd<T, NR>>(CC::SMEM, CC::THREADS))) return e;
+  if ((e = ensure_smem<k_zinv<T, NR>>(CC::SMEM, CC::THREADS))) return e;
+  if ((e = ensure_smem<k_ypass<T, NR, -1>>(SC::SMEM, SC::THREADS))) return e;
+  if ((e = ensure_smem<k_ypass<T, NR, +1>>(SC::SMEM, SC::THREADS))) return e;
+  if ((e = ensure_smem<k_xmid<T, NR>>(XC::SMEM, XC::THREADS))) return e;
+  static_assert((size_t(NR) * NR) % CC::L == 0, "rows per CTA must divide n^2");
+  if (a.ncp != spec_pitch(NR) || a.nc != NR / 2 + 1) return cudaErrorInvalidValue;
+  static_assert((CC::L & (CC::L - 1)) == 0 && (SC::L & (SC::L - 1)) == 0, "tile widths are powers of two");
   const unsigned zgrid = unsigned((size_t(NR) * NR) / CC::L);
   const dim3 sgrid((a.nc + SC::L - 1) / SC::L, NR);
+  const dim3 xgrid((a.nc + XC::L - 1) / XC::L, NR);
   const T scale = T(1.0 / (double(NR) * NR * NR));  // fft_solver.cpp:67
   const T four_pi2 = T(4.0 * M_PI * M_PI);           // fft_solver.cpp:66
+  const bool tma = a.tma != nullptr && NR >= 4;
+  if (tma && (a.tma->spec != a.spec || a.tma->n != NR)) {
+    if ((e = encode_spec_maps<T, NR>(a.tma, a.spec))) return e;
+  }
   mark(a, 0);
-  k_zfwd<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, a.ncp, tw);
-  mark(a, 1);
-  k_ypass<T, NR, -1><<<sgrid, SC::THREADS, SC::SMEM, a.stream>>>(S, a.ncp, a.nc, tw);
-  mark(a, 2);
-  k_xmid<T, NR><<<sgrid, SC::THREADS, SC::SMEM, a.stream>>>(S, a.ncp, a.nc, tw, scale, four_pi2);
-  mark(a, 3);
-  k_ypass<T, NR, +1><<<sgrid, SC::THREADS, SC::SMEM, a.stream>>>(S, a.ncp, a.nc, tw);
+  k_zfwd<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw);
+  if (tma) {
+    const CUtensorMap& my = *reinterpret_cast<const CUtensorMap*>(a.tma->maps[0]);
+    const CUtensorMap& mx = *reinterpret_cast<const CUtensorMap*>(a.tma->maps[1]);
+    mark(a, 1);
+    if ((e = launch_strided_tma<T, NR, 0>(a, my, scale, four_pi2))) return e;
+    mark(a, 2);
+    if ((e = launch_strided_tma<T, NR, 2>(a, mx, scale, four_pi2))) return e;
+    mark(a, 3);
+    if ((e = launch_strided_tma<T, NR, 1>(a, my, scale, four_pi2))) return e;
+  } else {
+    mark(a, 1);
+    k_ypass<T, NR, -1><<<sgrid, SC::THREADS, SC::SMEM, a.stream>>>(S, tw);
+    mark(a, 2);
+    k_xmid<T, NR><<<xgrid, XC::THREADS, XC::SMEM, a.stream>>>(S, tw, scale, four_pi2);
+    mark(a, 3);
+    k_ypass<T, NR, +1><<<sgrid, SC::THREADS, SC::SMEM, a.stream>>>(S, tw);
+  }
   mark(a, 4);
-  k_zinv<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), a.ncp, tw);
+  k_zinv<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw);
   mark(a, 5);
   return cudaGetLastError();
+}
+
+// Tile geometry of each kernel (exported for the CPU index-model tests).
+template <typename T, int NR>
+void pow2_config_n(KernelGeom* g) {
+  using CC = ContigCfg<T, NR>;
+  using SC = StridedCfg<T, NR, 0>;
+  using XC = StridedCfg<T, NR, 1>;
+  g[0] = {CC::M, CC::E, CC::L, CC::THREADS, CC::SMEM};  // zfwd: M-point lines
+  g[1] = {NR, SC::E, SC::L, SC::THREADS, SC::SMEM};     // ypass
+  g[2] = {NR, XC::E, XC::L, XC::THREADS, XC::SMEM};     // xmid
+}
+
+template <typename T>
+bool pow2_config(int n, KernelGeom* g) {
+  switch (n) {
+    case 2: pow2_config_n<T, 2>(g); return true;
+    case 4: pow2_config_n<T, 4>(g); return true;
+    case 8: pow2_config_n<T, 8>(g); return true;
+    case 16: pow2_config_n<T, 16>(g); return true;
+    case 32: pow2_config_n<T, 32>(g); return true;
+    case 64: pow2_config_n<T, 64>(g); return true;
+    case 128: pow2_config_n<T, 128>(g); return true;
+    case 256: pow2_config_n<T, 256>(g); return true;
+    case 512: pow2_config_n<T, 512>(g); return true;
+    case 1024: pow2_config_n<T, 1024>(g); return true;
+    case 2048: pow2_config_n<T, 2048>(g); return true;
+    default: return false;
+  }
 }
 
 template <typename T>

@@ -1,0 +1,80 @@
+"""CPU index model of the sm_100a kernels (tests/sim/engine_sim.py) driven by the
+tile geometry compiled into libarena_fft.so (arena_pow2_kernel_geometry): every
+Stockham plan / swizzled exchange used by the power-of-two path is replayed on
+random data and checked against numpy, and the shared-memory exchange is
+checked collision-free.  No GPU needed."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import pytest
+
+import paper_1408_6497_b200 as arena
+
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), "sim"))
+import engine_sim as sim  # noqa: E402
+
+POW2 = [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048]
+
+
+def geometry(n, prec, with_x=False):
+    out = (ctypes.c_int * 15)()
+    arena.lib.arena_pow2_kernel_geometry.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+    assert arena.lib.arena_pow2_kernel_geometry(n, prec, out) == 0
+    keys = ("line", "E", "L", "threads", "smem")
+    z, s, x = (dict(zip(keys, out[5 * i:5 * i + 5])) for i in range(3))
+    return (z, s, x) if with_x else (z, s)
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+@pytest.mark.parametrize("n", POW2)
+def test_tile_geometry_is_launchable(n, prec):
+    z, s, x = geometry(n, prec, with_x=True)
+    vb = 2 * (prec // 8)
+    assert x["line"] == n and x["smem"] >= x["line"] * x["L"] * vb
+    for g in (z, s, x):
+        assert g["L"] & (g["L"] - 1) == 0, g
+        assert g["threads"] == g["L"] * (g["line"] // g["E"]) <= 1024, g
+        assert g["smem"] <= 227 * 1024, g
+    assert z["line"] == n // 2 and s["line"] == n
+    assert (n * n) % z["L"] == 0  # z grid covers every row exactly
+    assert z["smem"] >= (z["line"] * z["L"] + z["L"]) * vb
+    assert s["smem"] >= s["line"] * s["L"] * vb
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+@pytest.mark.parametrize("n", POW2)
+def test_stockham_plan_replay(n, prec):
+    z, s, x = geometry(n, prec, with_x=True)
+    vb = 2 * (prec // 8)
+    for g in (z, s, x):
+        N, E, L = g["line"], g["E"], g["L"]
+        if N < 2:
+            continue
+        Lm = min(L, 2)  # lines are independent; two suffice to exercise the interleaved layout
+        for S in (-1, +1):
+            err = sim.check_line(N, E, L, S, vbytes=vb, lines_checked=Lm)
+            assert err < 1e-13, (N, E, L, S, err)
+
+
+@pytest.mark.parametrize("n", [4, 8, 16])
+def test_full_solve_model_vs_oracle(n):
+    import oracle
+
+    z, s = geometry(n, 64)
+    f = np.random.default_rng(n).uniform(-1, 1, (n, n, n))
+    u = sim.solve_model(f, z, s)
+    assert np.linalg.norm(u - oracle.poisson_solve(f)) <= 1e-13 * np.linalg.norm(u)
+
+
+@pytest.mark.parametrize("n", POW2)
+def test_blocked_row_layout_is_a_bijection(n):
+    """row_off (poisson_pow2.cuh): S rows grouped in j-blocks of JB; every (i, j)
+    gets its own ncp-element row inside the n*n*ncp workspace."""
+    jb = min(8, n)
+    ncp = (n // 2 + 1 + 7) // 8 * 8
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    rows = ((j // jb) * n + i) * jb + (j % jb)
+    assert np.array_equal(np.sort(rows.ravel()), np.arange(n * n))
+    assert rows.max() * ncp + ncp <= n * n * ncp

@@ -209,32 +209,34 @@ __device__ __forceinline__ int smem_idx(int pos, int l) {
   }
 }
 
-// Twiddle table reads: read-only global path, or a plain load when the table
-// was staged in shared memory (ARENA_TW_SMEM).
-#ifndef ARENA_TW_SMEM
-#define ARENA_TW_SMEM 0
-#endif
+// Twiddle table reads go through the read-only (L1) path.
 template <typename V>
 __device__ __forceinline__ V tw_load(const V* __restrict__ tw, int idx) {
-#if ARENA_TW_SMEM
-  return tw[idx];
-#else
   return __ldg(tw + idx);
-#endif
 }
 
-// Table twiddle W_N^m (forward) for an N-point line; `tw` holds W_NT^j for
-// j in [0, NT) and TWMUL = NT / N.
+// Multiply by a table twiddle (forward sign) or its conjugate (backward).
 template <int S, typename V>
 __device__ __forceinline__ V tw_apply(V a, const V* __restrict__ tw, int idx) {
   const V w = tw_load(tw, idx);
   return S < 0 ? cmul(a, w) : cmulc(a, w);
 }
 
+// Per-stage twiddle tables.  Stage s >= 1 (radix R, NS = product of the
+// earlier radices) multiplies input r of butterfly j by W_{NS*R}^{(j mod NS) r};
+// they are stored as tab_s[r*NS + (j mod NS)], so the lanes of a warp (adjacent
+// j) read adjacent entries — one 128-byte wavefront instead of one per lane
+// group.  Tables for consecutive stages are concatenated (stage_tw_offset).
+constexpr int stage_tw_size(int N, int E, int s) { return (1 << stage_log2(N, E, s)) * stage_ns(N, E, s); }
+constexpr int stage_tw_offset(int N, int E, int s) {  // offset of stage s (>= 1) in the (N, E) table
+  return s <= 1 ? 0 : stage_tw_offset(N, E, s - 1) + stage_tw_size(N, E, s - 1);
+}
+constexpr int stage_tw_total(int N, int E) { return num_stages(N, E) <= 1 ? 0 : stage_tw_offset(N, E, num_stages(N, E)); }
+
 // One Stockham stage on registers (no exchange).  Thread holds elements
 // t + P*e; butterfly q uses v[q + NB*r], r < R.
 template <int N, int E, int R, int NS, int S, typename V>
-__device__ __forceinline__ void stage_compute(V (&v)[E], int t, const V* __restrict__ tw, int twmul) {
+__device__ __forceinline__ void stage_compute(V (&v)[E], int t, const V* __restrict__ stw) {
   constexpr int P = N / E, NB = E / R;
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
@@ -243,9 +245,8 @@ __device__ __forceinline__ void stage_compute(V (&v)[E], int t, const V* __restr
     for (int r = 0; r < R; ++r) a[r] = v[q + NB * r];
     if constexpr (NS > 1) {
       const int jj = (t + P * q) & (NS - 1);
-      const int base = jj * (N / (NS * R)) * twmul;
 #pragma unroll
-      for (int r = 1; r < R; ++r) a[r] = tw_apply<S>(a[r], tw, base * r);
+      for (int r = 1; r < R; ++r) a[r] = tw_apply<S>(a[r], stw, r * NS + jj);
     }
     Dft<R, S>::run(a);
 #pragma unroll
@@ -272,24 +273,25 @@ __device__ __forceinline__ void stage_exchange(V (&v)[E], V* sm, int t, int l) {
 }
 
 template <int N, int E, int L, int S, int STAGE, typename V>
-__device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, const V* __restrict__ tw, int twmul, int t, int l) {
+__device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, const V* __restrict__ stw, int t, int l) {
   constexpr int NSTAGE = num_stages(N, E);
   if constexpr (STAGE < NSTAGE) {
     constexpr int R = 1 << stage_log2(N, E, STAGE);
     constexpr int NS = stage_ns(N, E, STAGE);
     constexpr int SW = stage_log2(N, E, 0);
-    stage_compute<N, E, R, NS, S>(v, t, tw, twmul);
+    stage_compute<N, E, R, NS, S>(v, t, stw + (STAGE >= 1 ? stage_tw_offset(N, E, STAGE) : 0));
     if constexpr (STAGE + 1 < NSTAGE) stage_exchange<N, E, L, R, NS, SW>(v, sm, t, l);
-    fft_stages<N, E, L, S, STAGE + 1>(v, sm, tw, twmul, t, l);
+    fft_stages<N, E, L, S, STAGE + 1>(v, sm, stw, t, l);
   }
 }
 
 // Full N-point line FFT of the tile.  On entry and exit thread (l, t) holds
 // line-l elements t + P*e (natural order).  `sm` must hold N*L elements and
 // be free (all threads past their last access) on entry; on exit it is free.
+// `stw` is the (N, E) stage-twiddle table (stage_tw_total(N, E) entries).
 template <int N, int E, int L, int S, typename V>
-__device__ __forceinline__ void line_fft(V (&v)[E], V* sm, const V* __restrict__ tw, int twmul, int t, int l) {
-  fft_stages<N, E, L, S, 0>(v, sm, tw, twmul, t, l);
+__device__ __forceinline__ void line_fft(V (&v)[E], V* sm, const V* __restrict__ stw, int t, int l) {
+  fft_stages<N, E, L, S, 0>(v, sm, stw, t, l);
 }
 
 // Swizzle parameter callers must use when they stage data in `sm` in the

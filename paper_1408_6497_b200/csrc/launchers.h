@@ -17,11 +17,19 @@ struct alignas(64) TmaCache {
   int n = 0;
 };
 
+// Stage-twiddle tables (fft_engine.cuh stage_tw_*) a plan holds: for line
+// lengths N = n/2 (which = 0) and N = n (which = 1) and every points-per-thread
+// E in {2, 4, 8, 16, 32} (clamped to N), concatenated in that order.
+size_t stw_entries(int n);
+size_t stw_offset(int n, int which, int E);
+void stw_fill_host(int n, int precision_bits, void* host);  // stw_entries(n) vec2 values
+
 struct Pow2Args {
   const void* f;
   void* u;
   void* spec;
-  const void* tw;
+  const void* tw;   // W_n^m, m in [0, n)
+  const void* stw;  // stage-twiddle tables (stw_offset)
   int n, nc, ncp;
   cudaStream_t stream;
   cudaEvent_t* ev;  // nullable; kPow2Launches + 1 events: before each kernel and after the last

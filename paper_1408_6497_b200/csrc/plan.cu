@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -62,6 +63,7 @@ struct arena_fft_plan {
   void* spec = nullptr;  // half spectrum workspace
   size_t spec_bytes = 0;
   void* tw = nullptr;  // W_n^m table, vec2 of the precision
+  void* stw = nullptr;  // stage-twiddle tables (power-of-two path)
   GenPlan gplan{};
   TmaCache* tma = nullptr;  // TMA descriptors (power-of-two path), nullptr = classic kernels
   int sm_count = 148;
@@ -107,6 +109,14 @@ arena_status make_twiddles(arena_fft_plan* p) {
   if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? fail(ARENA_ENOMEM, "twiddle table") : cuda_fail(e, "cudaMalloc");
   e = cudaMemcpy(p->tw, host.data(), host.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "twiddle upload");
+  if (p->path == ARENA_PATH_POW2) {
+    const size_t ns = stw_entries(n);
+    std::vector<unsigned char> st(std::max<size_t>(ns, 1) * vb);
+    stw_fill_host(n, p->prec, st.data());
+    if ((e = cudaMalloc(&p->stw, st.size())) != cudaSuccess) return fail(ARENA_ENOMEM, "stage twiddle tables");
+    if ((e = cudaMemcpy(p->stw, st.data(), st.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cuda_fail(e, "stage twiddle upload");
+  }
   return ARENA_OK;
 }
 
@@ -115,6 +125,7 @@ void free_plan(arena_fft_plan* p) {
   DeviceGuard g(p->device);
   if (p->spec) cudaFree(p->spec);
   if (p->tw) cudaFree(p->tw);
+  if (p->stw) cudaFree(p->stw);
   if (p->d_in) cudaFree(p->d_in);
   if (p->d_out) cudaFree(p->d_out);
   if (p->d_work) cudaFree(p->d_work);
@@ -144,7 +155,7 @@ arena_status enqueue_solve(arena_fft_plan* p, const void* d_f, void* d_u, cudaSt
   cudaError_t e;
   cudaEvent_t* ev = timing_events(p);
   if (p->path == ARENA_PATH_POW2) {
-    Pow2Args a{d_f, d_u, p->spec, p->tw, p->n, p->nc, p->ncp, s, ev, p->tma, p->sm_count};
+    Pow2Args a{d_f, d_u, p->spec, p->tw, p->stw, p->n, p->nc, p->ncp, s, ev, p->tma, p->sm_count};
     e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
   } else {
     GenArgs a{&p->gplan, p->tw, p->n, p->nc, p->ncp, s, ev};

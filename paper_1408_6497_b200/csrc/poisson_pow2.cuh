@@ -35,13 +35,18 @@ __host__ __device__ constexpr int spec_pitch(int n) { return (n / 2 + 1 + 7) / 8
 #define ARENA_STRIDED_MINB 2  // min CTAs/SM hint for the strided (y, x) kernels
 #endif
 #ifndef ARENA_CONTIG_MINB
-#define ARENA_CONTIG_MINB 2  // min CTAs/SM hint for the contiguous (z) kernels
+#define ARENA_CONTIG_MINB 8  // min CTAs/SM hint for the contiguous (z) kernels
 #endif
 #ifndef ARENA_STRIDED_E
 #define ARENA_STRIDED_E 16  // points per thread, y / x kernels
 #endif
 #ifndef ARENA_CONTIG_E
-#define ARENA_CONTIG_E 16  // points per thread, z kernels
+#define ARENA_CONTIG_E 32  // points per thread, z kernels
+#endif
+#ifndef ARENA_CONTIG_ROWS
+#define ARENA_CONTIG_ROWS 2  // rows per z CTA: with E = 32 and n = 1024 one warp per CTA, so the
+                             // exchanges' barrier spans a single warp (B200 A/B: 3.2 ms vs 6.6 ms
+                             // for 8 rows x 16 points per thread)
 #endif
 #ifndef ARENA_Y_SMEM
 #define ARENA_Y_SMEM (64 * 1024)  // shared-memory budget per y tile (sets its width L)
@@ -65,7 +70,7 @@ struct StridedCfg {  // y (PASS 0) / x (PASS 1) passes: lines along a strided ax
   static constexpr int P = N / E;
   static constexpr int THREADS = L * P;
   static constexpr int SMEM_X = N * L * VB;                   // exchange buffer bytes
-  static constexpr int SMEM = SMEM_X + (ARENA_TW_SMEM ? N * VB : 0);
+  static constexpr int SMEM = SMEM_X;
 };
 
 template <typename T, int NR>
@@ -76,12 +81,12 @@ struct ContigCfg {  // z passes: rows of NR reals = M = NR/2 complex
   static constexpr int VB = 2 * sizeof(T);
   // rows per CTA (a power of two, so it divides the n^2 rows): aim for 256
   // threads and at least 8 rows, at most ~96 KB of shared memory.
-  static constexpr int L0 = imax(8, 256 / P);
+  static constexpr int L0 = imax(ARENA_CONTIG_ROWS, 32 / P);  // at least one full warp
   static constexpr int L1 = imin(L0, imax(1, (96 * 1024) / ((M + 1) * VB)));
   static constexpr int L = pow2_floor(imin(L1, NR * NR));
   static constexpr int THREADS = L * P;
   static constexpr int SMEM_X = (M * L + L) * VB;
-  static constexpr int SMEM = SMEM_X + (ARENA_TW_SMEM ? NR * VB : 0);
+  static constexpr int SMEM = SMEM_X;
 };
 
 __device__ __forceinline__ int signed_freq(int k, int n) { return k <= n / 2 ? k : k - n; }  // fft_solver.hpp:19
@@ -104,19 +109,6 @@ __device__ __forceinline__ V* smem_base() {
   return reinterpret_cast<V*>(arena_smem_raw);
 }
 
-// The twiddle table the engine reads: the global table, or (ARENA_TW_SMEM) a
-// copy staged once per CTA after the exchange buffer (SX bytes).
-template <typename V, int NT, int SX>
-__device__ __forceinline__ const V* stage_twiddles(const V* __restrict__ tw) {
-#if ARENA_TW_SMEM
-  V* t = reinterpret_cast<V*>(reinterpret_cast<unsigned char*>(smem_base<V>()) + SX);
-  for (int i = threadIdx.x; i < NT; i += blockDim.x) t[i] = __ldg(tw + i);
-  __syncthreads();
-  return t;
-#else
-  return tw;
-#endif
-}
 
 // ------------------------------------------------------------------- K1 zfwd
 // Rows of NR reals: z[m] = f[2m] + i f[2m+1] (one vector load), M-point FFT,
@@ -124,14 +116,14 @@ __device__ __forceinline__ const V* stage_twiddles(const V* __restrict__ tw) {
 // for k in [0, M]; X[M] = Re Z0 - Im Z0.
 template <typename T, int NR>
 __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
-    k_zfwd(const T* __restrict__ f, vec2_t<T>* __restrict__ S, const vec2_t<T>* tw) {
+    k_zfwd(const T* __restrict__ f, vec2_t<T>* __restrict__ S, const vec2_t<T>* __restrict__ tw,
+           const vec2_t<T>* __restrict__ stw) {
   using V = vec2_t<T>;
   using C = ContigCfg<T, NR>;
   constexpr int M = C::M, E = C::E, P = C::P, L = C::L;
   constexpr int ncp = spec_pitch(NR);
   constexpr int SW = engine_swizzle<M, E>();
   V* sm = smem_base<V>();
-  tw = stage_twiddles<V, NR, C::SMEM_X>(tw);
   const int l = threadIdx.x % L, t = threadIdx.x / L;
   const size_t row = size_t(blockIdx.x) * L + l;
   const V* src = reinterpret_cast<const V*>(f + row * NR);
@@ -139,7 +131,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
   V v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = __ldcs(src + t + P * e);
-  line_fft<M, E, L, -1>(v, sm, tw, 2, t, l);
+  line_fft<M, E, L, -1>(v, sm, stw, t, l);
 #pragma unroll
   for (int e = 0; e < E; ++e) sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
   __syncthreads();
@@ -163,14 +155,14 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
 // M-point backward FFT, u[2m] = Re z[m], u[2m+1] = Im z[m].
 template <typename T, int NR>
 __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
-    k_zinv(const vec2_t<T>* __restrict__ S, T* __restrict__ u, const vec2_t<T>* tw) {
+    k_zinv(const vec2_t<T>* __restrict__ S, T* __restrict__ u, const vec2_t<T>* __restrict__ tw,
+           const vec2_t<T>* __restrict__ stw) {
   using V = vec2_t<T>;
   using C = ContigCfg<T, NR>;
   constexpr int M = C::M, E = C::E, P = C::P, L = C::L;
   constexpr int ncp = spec_pitch(NR);
   constexpr int SW = engine_swizzle<M, E>();
   V* sm = smem_base<V>();
-  tw = stage_twiddles<V, NR, C::SMEM_X>(tw);
   V* xm = sm + M * L;  // X[M] per line
   const int l = threadIdx.x % L, t = threadIdx.x / L;
   const size_t row = size_t(blockIdx.x) * L + l;
@@ -200,7 +192,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
     v[e] = V{Ep.x - Op.y, Ep.y + Op.x};
   }
   __syncthreads();
-  line_fft<M, E, L, +1>(v, sm, tw, 2, t, l);
+  line_fft<M, E, L, +1>(v, sm, stw, t, l);
   V* dst = reinterpret_cast<V*>(u + row * NR);
 #pragma unroll
   for (int e = 0; e < E; ++e) __stcs(dst + t + P * e, v[e]);
@@ -209,13 +201,12 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
 // --------------------------------------------------------------- K2/K4 ypass
 template <typename T, int N, int S>
 __global__ void __launch_bounds__(StridedCfg<T, N, 0>::THREADS, ARENA_STRIDED_MINB)
-    k_ypass(vec2_t<T>* __restrict__ spec, const vec2_t<T>* tw) {
+    k_ypass(vec2_t<T>* __restrict__ spec, const vec2_t<T>* __restrict__ stw) {
   using V = vec2_t<T>;
   using C = StridedCfg<T, N, 0>;
   constexpr int E = C::E, P = C::P, L = C::L;
   constexpr int ncp = spec_pitch(N), nc = N / 2 + 1;
   V* sm = smem_base<V>();
-  tw = stage_twiddles<V, N, C::SMEM_X>(tw);
   const int l = threadIdx.x % L, t = threadIdx.x / L;
   const int k = blockIdx.x * L + l;
   const bool valid = k < nc;
@@ -225,7 +216,7 @@ __global__ void __launch_bounds__(StridedCfg<T, N, 0>::THREADS, ARENA_STRIDED_MI
   V v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = valid ? __ldcs(base + row_off<N>(i, t + P * e)) : V{T(0), T(0)};
-  line_fft<N, E, L, S>(v, sm, tw, 1, t, l);
+  line_fft<N, E, L, S>(v, sm, stw, t, l);
   if (valid) {
 #pragma unroll
     for (int e = 0; e < E; ++e) __stcs(base + row_off<N>(i, t + P * e), v[e]);
@@ -239,13 +230,12 @@ __global__ void __launch_bounds__(StridedCfg<T, N, 0>::THREADS, ARENA_STRIDED_MI
 // registers between the two transforms.
 template <typename T, int N>
 __global__ void __launch_bounds__(StridedCfg<T, N, 1>::THREADS, ARENA_STRIDED_MINB)
-    k_xmid(vec2_t<T>* __restrict__ spec, const vec2_t<T>* tw, T scale, T four_pi2) {
+    k_xmid(vec2_t<T>* __restrict__ spec, const vec2_t<T>* __restrict__ stw, T scale, T four_pi2) {
   using V = vec2_t<T>;
   using C = StridedCfg<T, N, 1>;
   constexpr int E = C::E, P = C::P, L = C::L;
   constexpr int ncp = spec_pitch(N), nc = N / 2 + 1;
   V* sm = smem_base<V>();
-  tw = stage_twiddles<V, N, C::SMEM_X>(tw);
   const int l = threadIdx.x % L, t = threadIdx.x / L;
   const int k = blockIdx.x * L + l;
   const int j = blockIdx.y;
@@ -255,7 +245,7 @@ __global__ void __launch_bounds__(StridedCfg<T, N, 1>::THREADS, ARENA_STRIDED_MI
   V v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = valid ? __ldcs(base + size_t(t + P * e) * istride) : V{T(0), T(0)};
-  line_fft<N, E, L, -1>(v, sm, tw, 1, t, l);
+  line_fft<N, E, L, -1>(v, sm, stw, t, l);
   const T kj = T(signed_freq(j, N)), kk = T(k);
   const T c = kj * kj + kk * kk;
 #pragma unroll
@@ -266,7 +256,7 @@ __global__ void __launch_bounds__(StridedCfg<T, N, 1>::THREADS, ARENA_STRIDED_MI
     v[e].x *= m;
     v[e].y *= m;
   }
-  line_fft<N, E, L, +1>(v, sm, tw, 1, t, l);
+  line_fft<N, E, L, +1>(v, sm, stw, t, l);
   if (valid) {
 #pragma unroll
     for (int e = 0; e < E; ++e) __stcs(base + size_t(t + P * e) * istride, v[e]);
@@ -286,10 +276,17 @@ __global__ void __launch_bounds__(StridedCfg<T, N, 1>::THREADS, ARENA_STRIDED_MI
 
 namespace arena_fft {
 
+#ifndef ARENA_TMA_E
+#define ARENA_TMA_E 16  // points per thread in the TMA strided kernels
+#endif
+#ifndef ARENA_TMA_MINB
+#define ARENA_TMA_MINB 1
+#endif
+
 template <typename T, int N>
 struct TmaCfg {
   static constexpr int VB = 2 * sizeof(T);
-  static constexpr int E = imin(ARENA_STRIDED_E, N);
+  static constexpr int E = imin(ARENA_TMA_E, N);
   static constexpr int P = N / E;
   static constexpr int L = pow2_floor(imax(2, imin(8, (64 * 1024) / (N * VB))));
   static constexpr int THREADS = L * P;
@@ -303,9 +300,9 @@ struct TmaCfg {
 
 // PASS 0: y forward, 1: y backward, 2: x forward * Poisson symbol * x backward.
 template <typename T, int N, int PASS>
-__global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, 1)
+__global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
     k_strided_tma(const __grid_constant__ CUtensorMap tmap, vec2_t<T>* __restrict__ spec,
-                  const vec2_t<T>* __restrict__ tw, T scale, T four_pi2) {
+                  const vec2_t<T>* __restrict__ stw, T scale, T four_pi2) {
   using V = vec2_t<T>;
   using C = TmaCfg<T, N>;
   constexpr int E = C::E, P = C::P, L = C::L, KT = C::KT, TILE = C::TILE;
@@ -354,11 +351,11 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, 1)
     const int outer = g / KT;
     const int k = (g % KT) * L + l;
     if constexpr (PASS == 0) {
-      line_fft<N, E, L, -1>(v, cur, tw, 1, t, l);
+      line_fft<N, E, L, -1>(v, cur, stw, t, l);
     } else if constexpr (PASS == 1) {
-      line_fft<N, E, L, +1>(v, cur, tw, 1, t, l);
+      line_fft<N, E, L, +1>(v, cur, stw, t, l);
     } else {
-      line_fft<N, E, L, -1>(v, cur, tw, 1, t, l);
+      line_fft<N, E, L, -1>(v, cur, stw, t, l);
       const int j = outer;
       const T kj = T(signed_freq(j, N)), kk = T(k);
       const T c = kj * kj + kk * kk;
@@ -370,7 +367,7 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, 1)
         v[e].x *= m;
         v[e].y *= m;
       }
-      line_fft<N, E, L, +1>(v, cur, tw, 1, t, l);
+      line_fft<N, E, L, +1>(v, cur, stw, t, l);
     }
     if (k < C::NC) {
       if constexpr (PASS < 2) {

@@ -79,6 +79,11 @@ cudaError_t encode_spec_maps(TmaCache* c, void* spec) {
   return cudaSuccess;
 }
 
+template <typename T>
+inline const vec2_t<T>* stw_ptr(const Pow2Args& a, int which, int E) {
+  return static_cast<const vec2_t<T>*>(a.stw) + stw_offset(a.n, which, E);
+}
+
 template <typename T, int N, int PASS>
 cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, T scale, T four_pi2) {
   using C = TmaCfg<T, N>;
@@ -91,7 +96,7 @@ cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, T scal
   const int tiles = N * C::KT;
   int grid = a.sm_count * (per_sm > 0 ? per_sm : 1);
   if (grid > tiles) grid = tiles;
-  kern<<<grid, C::THREADS, C::SMEM, a.stream>>>(map, static_cast<V*>(a.spec), static_cast<const V*>(a.tw), scale,
+  kern<<<grid, C::THREADS, C::SMEM, a.stream>>>(map, static_cast<V*>(a.spec), stw_ptr<T>(a, 1, C::E), scale,
                                                four_pi2);
   return cudaGetLastError();
 }
@@ -127,7 +132,8 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
     if ((e = encode_spec_maps<T, NR>(a.tma, a.spec))) return e;
   }
   mark(a, 0);
-  k_zfwd<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw);
+  k_zfwd<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw,
+                                                             stw_ptr<T>(a, 0, CC::E));
   if (tma) {
     const CUtensorMap& my = *reinterpret_cast<const CUtensorMap*>(a.tma->maps[0]);
     const CUtensorMap& mx = *reinterpret_cast<const CUtensorMap*>(a.tma->maps[1]);
@@ -139,14 +145,15 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
     if ((e = launch_strided_tma<T, NR, 1>(a, my, scale, four_pi2))) return e;
   } else {
     mark(a, 1);
-    k_ypass<T, NR, -1><<<sgrid, SC::THREADS, SC::SMEM, a.stream>>>(S, tw);
+    k_ypass<T, NR, -1><<<sgrid, SC::THREADS, SC::SMEM, a.stream>>>(S, stw_ptr<T>(a, 1, SC::E));
     mark(a, 2);
-    k_xmid<T, NR><<<xgrid, XC::THREADS, XC::SMEM, a.stream>>>(S, tw, scale, four_pi2);
+    k_xmid<T, NR><<<xgrid, XC::THREADS, XC::SMEM, a.stream>>>(S, stw_ptr<T>(a, 1, XC::E), scale, four_pi2);
     mark(a, 3);
-    k_ypass<T, NR, +1><<<sgrid, SC::THREADS, SC::SMEM, a.stream>>>(S, tw);
+    k_ypass<T, NR, +1><<<sgrid, SC::THREADS, SC::SMEM, a.stream>>>(S, stw_ptr<T>(a, 1, SC::E));
   }
   mark(a, 4);
-  k_zinv<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw);
+  k_zinv<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw,
+                                                             stw_ptr<T>(a, 0, CC::E));
   mark(a, 5);
   return cudaGetLastError();
 }

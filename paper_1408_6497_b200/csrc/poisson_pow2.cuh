@@ -276,11 +276,18 @@ __global__ void __launch_bounds__(StridedCfg<T, N, 1>::THREADS, ARENA_STRIDED_MI
 
 namespace arena_fft {
 
+// B200 A/B at 1024^3 fp64 (tools/ab.sh): one tile buffer per CTA with two
+// co-resident CTAs per SM (x pass 5.4 ms) beat a double-buffered single CTA
+// (6.3 ms); three buffers were slower still (the carveout starves L1, which
+// holds the twiddle tables).
 #ifndef ARENA_TMA_E
-#define ARENA_TMA_E 16  // points per thread in the TMA strided kernels
+#define ARENA_TMA_E 32  // points per thread in the TMA strided kernels
 #endif
 #ifndef ARENA_TMA_MINB
-#define ARENA_TMA_MINB 1
+#define ARENA_TMA_MINB 2  // co-resident CTAs per SM
+#endif
+#ifndef ARENA_TMA_NBUF
+#define ARENA_TMA_NBUF 1  // tile buffers per CTA (prefetch distance NBUF-1)
 #endif
 
 template <typename T, int N>
@@ -295,7 +302,8 @@ struct TmaCfg {
   static constexpr int TILE = N * L;          // elements per tile
   static constexpr int JB = ARENA_JBLOCK < N ? ARENA_JBLOCK : N;
   static constexpr int IB = N < 256 ? N : 256;  // TMA box rows for the x pass
-  static constexpr int SMEM = 2 * TILE * VB + 16;
+  static constexpr int NBUF = (ARENA_TMA_NBUF * TILE * VB <= 200 * 1024) ? ARENA_TMA_NBUF : imin(2, ARENA_TMA_NBUF);
+  static constexpr int SMEM = NBUF * TILE * VB + 8 * NBUF;
 };
 
 // PASS 0: y forward, 1: y backward, 2: x forward * Poisson symbol * x backward.
@@ -308,15 +316,15 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
   constexpr int E = C::E, P = C::P, L = C::L, KT = C::KT, TILE = C::TILE;
   constexpr int NT = N * KT;
   constexpr uint32_t TILE_BYTES = TILE * sizeof(V);
-  V* buf0 = smem_base<V>();
-  V* buf1 = buf0 + TILE;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(buf1 + TILE);
+  constexpr int NBUF = C::NBUF;
+  V* bufs = smem_base<V>();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(bufs + NBUF * TILE);
   const int tid = threadIdx.x;
   const int l = tid % L, t = tid / L;
 
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int b = 0; b < NBUF; ++b) mbar_init(&bar[b], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -333,17 +341,32 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
     }
   };
 
-  int g = blockIdx.x;
-  if (tid == 0 && g < NT) issue(g, buf0, &bar[0]);
-  for (int it = 0; g < NT; ++it, g += gridDim.x) {
-    V* cur = (it & 1) ? buf1 : buf0;
-    V* nxt = (it & 1) ? buf0 : buf1;
-    const int gn = g + gridDim.x;
-    if (tid == 0 && gn < NT) {
-      fence_proxy_async_smem();
-      issue(gn, nxt, &bar[(it & 1) ^ 1]);
+  // Prologue: tiles 0 .. NBUF-2 of this CTA in flight.
+  if (tid == 0) {
+#pragma unroll
+    for (int p = 0; p < NBUF - 1; ++p) {
+      const int gp = blockIdx.x + p * gridDim.x;
+      if (gp < NT) issue(gp, bufs + p * TILE, &bar[p]);
     }
-    mbar_wait(&bar[it & 1], (it >> 1) & 1);
+  }
+  int g = blockIdx.x;
+  for (int it = 0; g < NT; ++it, g += gridDim.x) {
+    const int b = it % NBUF;
+    V* cur = bufs + b * TILE;
+    if constexpr (NBUF == 1) {  // no intra-CTA prefetch: co-resident CTAs overlap instead
+      if (tid == 0) {
+        fence_proxy_async_smem();
+        issue(g, bufs, &bar[0]);
+      }
+    } else {
+      const int gn = g + (NBUF - 1) * gridDim.x;
+      if (tid == 0 && gn < NT) {  // refill the buffer iteration it-1 used
+        const int bn = (it + NBUF - 1) % NBUF;
+        fence_proxy_async_smem();
+        issue(gn, bufs + bn * TILE, &bar[bn]);
+      }
+    }
+    mbar_wait(&bar[b], (it / NBUF) & 1);
     V v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = cur[(t + P * e) * L + l];

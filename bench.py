@@ -216,11 +216,7 @@ def run_ours(args, rank, world, local):
     from paper_1408_6497_b200 import problems
 
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = None  # single GPU (N > 1 runs the slab decomposition, run_slab)
     n, prec = args.n, args.precision
     elem = 8 if prec == 64 else 4
     dt = torch.float64 if prec == 64 else torch.float32
@@ -353,11 +349,129 @@ def run_ours(args, rank, world, local):
         dist.destroy_process_group()
 
 
+def run_slab(args, rank, world, local):
+    """N > 1: slab decomposition over the ranks' GPUs, NCCL all-to-alls (strong scaling:
+    the n^3 problem is fixed, each rank owns n/N planes)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1408_6497_b200 as arena
+    from paper_1408_6497_b200 import problems
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, prec = args.n, args.precision
+    elem = 8 if prec == 64 else 4
+    dt = torch.float64 if prec == 64 else torch.float32
+    src = problems.config(args.config, n)
+    ni = n // world
+    i0 = rank * ni
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    # this rank's planes of f, global mean removed
+    f64 = torch.empty((ni, n, n), dtype=torch.float64, device="cuda")
+    problems.fill_device(src, "f", f64, 64, sh, i0, ni)
+    tot = f64.sum().reshape(1)
+    dist.all_reduce(tot)
+    f64 -= tot.item() / float(n) ** 3
+    f = f64 if prec == 64 else f64.float()
+    u = torch.empty_like(f)
+
+    nb = arena.lib.arena_nccl_unique_id_bytes()
+    idt = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        idt.copy_(torch.frombuffer(bytearray(arena.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(idt, 0)
+    slab = arena.Slab(n, world, rank=rank, nccl_id=bytes(idt.cpu().numpy().tobytes()), precision=prec, device=local)
+
+    for _ in range(args.warmup):
+        slab.solve_device(f, u, sh)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        start.record(stream)
+        for _ in range(args.steps):
+            slab.solve_device(f, u, sh)
+        end.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    t = torch.tensor([start.elapsed_time(end)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = t.item() / args.steps
+    value = n ** 3 / (ms_step / 1e3)
+
+    ua = torch.empty((ni, n, n), dtype=torch.float64, device="cuda")
+    problems.fill_device(src, "u", ua, 64, sh, i0, ni)
+    sums = torch.stack([ua.sum(), ((u.double() - ua) ** 2).sum(), (ua ** 2).sum()])
+    dist.all_reduce(sums)
+    mean_u = sums[0].item() / float(n) ** 3
+    # ||u - (ua - mean)||^2 = sum (u-ua)^2 + 2 mean sum(u-ua) + N mean^2 ; recompute directly per rank
+    d2 = torch.stack([((u.double() - (ua - mean_u)) ** 2).sum(), ((ua - mean_u) ** 2).sum()])
+    dist.all_reduce(d2)
+    rel_an = (d2[0] / d2[1]).sqrt().item()
+
+    peak, peak_kind = _peaks()
+    _, b_solve = algorithmic_bytes(n, elem)
+    C = n * n * (n // 2 + 1) * 2 * elem
+    hbm_per_gpu = b_solve / world
+    nvl_per_gpu = 2 * (C / world) * (world - 1) / world
+    nvl_peak = 770.0  # GB/s per direction, measured peer copy (B200_PROFILING.md)
+    t_roof = max(hbm_per_gpu / (peak * 1e9), nvl_per_gpu / (nvl_peak * 1e9))
+
+    e2e = None
+    if not args.no_e2e:
+        hf = torch.empty((ni, n, n), dtype=dt, pin_memory=True)
+        hf.copy_(f)
+        hu = torch.empty_like(hf, pin_memory=True)
+        ksteps = max(1, min(args.steps, 3))
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ksteps):
+            f.copy_(hf, non_blocking=True)
+            slab.solve_device(f, u, sh)
+            hu.copy_(u, non_blocking=True)
+            torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        te = torch.tensor([el], device="cuda", dtype=torch.float64)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        el = te.item()
+        e2e = {"value": n ** 3 * ksteps / el, "unit": UNIT, "h2d_bytes_per_step": n ** 3 * elem,
+               "d2h_bytes_per_step": n ** 3 * elem, "steps": ksteps, "ms_per_step": el / ksteps * 1e3,
+               "api": "arena_slab_solve_device with per-rank pinned H2D/D2H of the rank's slab (summed over ranks)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64" if prec == 64 else "f32", "data": "synthetic",
+            "config": {"workload": f"C{args.config}: {problems.CONFIG_TEXT[args.config]}", "n": n, "precision": prec,
+                       "decomposition": f"slab x{world} over i, NCCL grouped send/recv all-to-all",
+                       "l2": "inputs larger than L2, no flush"},
+            "roofline": {"bound": "hbm+nvlink", "achieved": hbm_per_gpu / (ms_step / 1e3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": t_roof / (ms_step / 1e3), "traffic": None, "peak_kind": peak_kind,
+                         "nvlink_bytes_per_gpu": nvl_per_gpu, "nvlink_peak_gbs": nvl_peak,
+                         "t_roof_ms": t_roof * 1e3},
+            "cpu_baseline": None,
+            "e2e": e2e,
+            "gpu_launches": 5 * args.steps,
+            "clocks": clk.summary(),
+            "parity": {"rel_l2_vs_analytic": rel_an},
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = _args()
     rank, world, local = _dist()
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif world > 1:
+        run_slab(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)
 

@@ -98,6 +98,31 @@ arena_status arena_source_modes(int n, int precision_bits, int nmodes, const int
                                 void* stream);
 arena_status arena_source_gaussian(int n, int precision_bits, double alpha, double cx, double cy, double cz, int which,
                                    void* d_out, void* stream);
+/* Slab variants: only planes i0 .. i0+ni-1 of the n^3 field (ni*n*n values). */
+arena_status arena_source_modes_slab(int n, int precision_bits, int nmodes, const int* k, const double* coef, int i0,
+                                     int ni, void* d_out, void* stream);
+arena_status arena_source_gaussian_slab(int n, int precision_bits, double alpha, double cx, double cy, double cz,
+                                        int which, int i0, int ni, void* d_out, void* stream);
+
+/* ---- Slab decomposition over P GPUs ------------------------
+ * One process per GPU.  Rank r owns planes i in [r*n/P, (r+1)*n/P) of f and u
+ * (a contiguous n/P * n * n slice of the GridField layout).  The two global
+ * transposes are grouped ncclSend/ncclRecv all-to-alls (NCCL loaded at run time).
+ * Create: rank 0 calls arena_nccl_unique_id, the id (arena_nccl_unique_id_bytes()
+ * bytes) is broadcast out of band (e.g. torch.distributed), every rank calls
+ * arena_slab_create.  arena_slab_create_loopback runs P virtual ranks on ONE
+ * device (exchanges are device copies) — used to test the decomposition without
+ * a multi-GPU box; its solve takes the full n^3 field.  Power-of-two n, P | n. */
+typedef struct arena_fft_slab arena_fft_slab;
+int arena_nccl_unique_id_bytes(void);
+arena_status arena_nccl_unique_id(void* out, int len);
+arena_status arena_slab_create(arena_fft_slab** slab, int n, int precision_bits, int device, int nranks, int rank,
+                               const void* nccl_id);
+arena_status arena_slab_create_loopback(arena_fft_slab** slab, int n, int precision_bits, int device, int nvranks);
+void arena_slab_destroy(arena_fft_slab* slab);
+arena_status arena_slab_info(const arena_fft_slab* slab, int* ni, int* nj, size_t* chunk_bytes, size_t* workspace_bytes);
+/* d_f, d_u: this rank's slab (loopback: the full field); asynchronous on stream. */
+arena_status arena_slab_solve_device(arena_fft_slab* slab, const void* d_f, void* d_u, void* stream);
 
 /* Tile geometry of the power-of-two kernels for (n, precision): out15[0..4] =
  * {line length, points/thread, lines/CTA, threads/CTA, shared bytes} of the

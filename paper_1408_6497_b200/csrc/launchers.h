@@ -9,13 +9,17 @@ namespace arena_fft {
 constexpr int kPow2MaxN = 2048;
 constexpr int kPow2Launches = 5;
 
-// Plan-owned cache of the TMA descriptors over the half spectrum (encoded on
-// first use; they depend only on the workspace address and n).
+// Plan-owned cache of the TMA descriptors over the half-spectrum workspaces
+// (encoded on first use; they depend only on the buffers and the geometry).
 struct alignas(64) TmaCache {
-  unsigned char maps[2][128];  // CUtensorMap for the y and the x boxes
-  const void* spec = nullptr;  // workspace the maps were encoded for
-  int n = 0;
+  unsigned char maps[2][128];  // CUtensorMap: y boxes over workspace B, x boxes over workspace C
+  const void* specB = nullptr;
+  const void* specC = nullptr;
+  int n = 0, ni = 0, nj = 0, nchunks = 0;
 };
+
+// Solve phases (bit mask): the slab path runs them around its two exchanges.
+enum : int { kPhaseZY = 1, kPhaseX = 2, kPhaseYZ = 4, kPhaseAll = 7 };
 
 // Stage-twiddle tables (fft_engine.cuh stage_tw_*) a plan holds: for line
 // lengths N = n/2 (which = 0) and N = n (which = 1) and every points-per-thread
@@ -33,8 +37,15 @@ struct Pow2Args {
   int n, nc, ncp;
   cudaStream_t stream;
   cudaEvent_t* ev;  // nullable; kPow2Launches + 1 events: before each kernel and after the last
-  TmaCache* tma;    // nullable: classic (non-TMA) strided kernels
+  TmaCache* tma;    // nullable: classic (non-TMA) strided kernels (single GPU only)
   int sm_count;
+  // Slab geometry.  Single GPU: ni = nj = n, nchunks = 1, j0 = 0, specC = spec.
+  int ni;        // local i planes (rows of f / u and of workspace B)
+  int nj;        // local j lines of workspace C (x pass)
+  int nchunks;   // P: number of slabs
+  int j0;        // global j of local j = 0 (x pass)
+  void* specC;   // workspace C (x pass); == spec on one GPU
+  int phases;    // kPhase* mask
 };
 
 cudaError_t launch_pow2_f64(const Pow2Args& a);

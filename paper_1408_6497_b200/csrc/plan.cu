@@ -155,7 +155,8 @@ arena_status enqueue_solve(arena_fft_plan* p, const void* d_f, void* d_u, cudaSt
   cudaError_t e;
   cudaEvent_t* ev = timing_events(p);
   if (p->path == ARENA_PATH_POW2) {
-    Pow2Args a{d_f, d_u, p->spec, p->tw, p->stw, p->n, p->nc, p->ncp, s, ev, p->tma, p->sm_count};
+    Pow2Args a{d_f, d_u, p->spec, p->tw, p->stw, p->n, p->nc, p->ncp, s, ev, p->tma, p->sm_count,
+               /*ni*/ p->n, /*nj*/ p->n, /*nchunks*/ 1, /*j0*/ 0, /*specC*/ p->spec, kPhaseAll};
     e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
   } else {
     GenArgs a{&p->gplan, p->tw, p->n, p->nc, p->ncp, s, ev};
@@ -187,7 +188,11 @@ const char* arena_last_error(void) { return g_last_error.c_str(); }
 
 int arena_fft_abi_version(void) { return 100; }
 
-arena_status arena_fft_plan_create(arena_fft_plan** out, int n, int precision_bits, int device) {
+}  // extern "C"
+
+// Plan construction shared by single-GPU plans and slab ranks (which own
+// their own, smaller workspaces and pass alloc_spec = false).
+static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits, int device, bool alloc_spec) {
   if (!out) return fail(ARENA_EINVAL, "plan pointer is NULL");
   *out = nullptr;
   if (n < 2) return fail(ARENA_EINVAL, "GridField: n >= 2 required");  // grid.hpp:18
@@ -232,14 +237,23 @@ arena_status arena_fft_plan_create(arena_fft_plan** out, int n, int precision_bi
     free_plan(p);
     return st;
   }
-  p->spec_bytes = size_t(n) * n * p->ncp * 2 * p->elem;
-  if ((e = cudaMalloc(&p->spec, p->spec_bytes)) != cudaSuccess) {
-    free_plan(p);
-    return fail(ARENA_ENOMEM, "half-spectrum workspace (" + std::to_string(p->spec_bytes) + " B): " + cudaGetErrorString(e));
+  if (alloc_spec) {
+    p->spec_bytes = size_t(n) * n * p->ncp * 2 * p->elem;
+    if ((e = cudaMalloc(&p->spec, p->spec_bytes)) != cudaSuccess) {
+      free_plan(p);
+      return fail(ARENA_ENOMEM,
+                  "half-spectrum workspace (" + std::to_string(p->spec_bytes) + " B): " + cudaGetErrorString(e));
+    }
   }
   *out = p;
   g_last_error.clear();
   return ARENA_OK;
+}
+
+extern "C" {
+
+arena_status arena_fft_plan_create(arena_fft_plan** out, int n, int precision_bits, int device) {
+  return create_plan(out, n, precision_bits, device, true);
 }
 
 void arena_fft_plan_destroy(arena_fft_plan* plan) { free_plan(plan); }
@@ -396,6 +410,269 @@ arena_status arena_fft_stage_times(arena_fft_plan* p, double* ms, const char** n
   }
   if (n_stages) *n_stages = L;
   if (n_solves) *n_solves = p->solves;
+  return ARENA_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================
+// Slab decomposition over P ranks: rank r owns the f / u planes
+// i in [r*n/P, (r+1)*n/P) (a contiguous part of GridField.data).  Per solve:
+//   K1 z-r2c, K2 y-fwd on the rank's planes          (workspace B, layout B)
+//   all-to-all #1: chunk d of B (j in rank d's range) -> rank d's C chunk r
+//   K3 x-fwd * symbol * x-inv on the rank's j lines  (workspace C, layout C)
+//   all-to-all #2: the reverse
+//   K4 y-inv, K5 z-c2r                               (workspace B)
+// Every chunk is one contiguous block of ni*nj rows (Layout, poisson_pow2.cuh),
+// so the exchanges are plain grouped ncclSend/ncclRecv (NCCL has no all-to-all
+// primitive) — or, for P virtual ranks on one device ("loopback", used to test
+// the decomposition with one GPU), device-to-device cudaMemcpyAsync.
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+// NCCL is loaded lazily (the single-GPU path never needs it); in a process that
+// already loaded one (e.g. torch's), dlopen returns that same library.
+NcclApi* nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      api.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (api.h) break;
+    }
+    if (!api.h) return;
+    auto sym = [](const char* s) { return dlsym(api.h, s); };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GroupStart && api.GroupEnd && api.Send &&
+             api.Recv && api.GetErrorString;
+  });
+  return api.ok ? &api : nullptr;
+}
+
+arena_status nccl_fail(ncclResult_t r, const char* what) {
+  NcclApi* a = nccl_api();
+  return fail(ARENA_ENCCL, std::string(what) + ": " + (a ? a->GetErrorString(r) : "NCCL unavailable"));
+}
+
+struct SlabRank {
+  void* B = nullptr;  // workspace B: ni * n rows
+  void* C = nullptr;  // workspace C: n * nj rows
+  TmaCache tma;
+};
+
+}  // namespace
+
+struct arena_fft_slab {
+  arena_fft_plan* base = nullptr;  // twiddles, stage tables, device, precision (no workspace)
+  int n = 0, P = 1, rank = 0, loopback = 0;
+  int ni = 0, nj = 0;
+  size_t chunk_elems = 0;  // reals per exchange chunk
+  size_t ws_bytes = 0;     // bytes of one workspace (B or C)
+  std::vector<SlabRank> ranks;  // loopback: P virtual ranks; NCCL: this rank only
+  ncclComm_t comm = nullptr;
+};
+
+namespace {
+
+void free_slab(arena_fft_slab* s) {
+  if (!s) return;
+  if (s->base) {
+    DeviceGuard g(s->base->device);
+    for (SlabRank& r : s->ranks) {
+      if (r.B) cudaFree(r.B);
+      if (r.C) cudaFree(r.C);
+    }
+    if (s->comm) {
+      if (NcclApi* a = nccl_api()) a->CommDestroy(s->comm);
+    }
+  }
+  free_plan(s->base);
+  delete s;
+}
+
+arena_status slab_init(arena_fft_slab** out, int n, int prec, int device, int P, int rank, int loopback,
+                       const void* id) {
+  if (!out) return fail(ARENA_EINVAL, "slab pointer is NULL");
+  *out = nullptr;
+  if (P < 1 || rank < 0 || rank >= P) return fail(ARENA_EINVAL, "bad rank / size");
+  if (!is_pow2(n) || n > kPow2MaxN || n < 4) return fail(ARENA_EUNSUPPORTED, "slab path needs power-of-two 4 <= n <= 2048");
+  if ((P & (P - 1)) || P > n) return fail(ARENA_EUNSUPPORTED, "slab count must be a power of two <= n");
+  arena_fft_slab* s = new (std::nothrow) arena_fft_slab;
+  if (!s) return fail(ARENA_ENOMEM, "slab");
+  arena_status st = create_plan(&s->base, n, prec, device, false);
+  if (st != ARENA_OK) {
+    delete s;
+    return st;
+  }
+  if (!s->base->tma) {
+    free_slab(s);
+    return fail(ARENA_EUNSUPPORTED, "slab path needs the TMA kernels (unset ARENA_FFT_KERNELS)");
+  }
+  DeviceGuard g(s->base->device);
+  s->n = n;
+  s->P = P;
+  s->rank = rank;
+  s->loopback = loopback;
+  s->ni = n / P;
+  s->nj = n / P;
+  const size_t ncp = size_t(s->base->ncp);
+  s->chunk_elems = size_t(s->ni) * s->nj * ncp * 2;
+  s->ws_bytes = size_t(s->ni) * n * ncp * 2 * s->base->elem;
+  s->ranks.resize(loopback ? P : 1);
+  for (SlabRank& r : s->ranks) {
+    cudaError_t e;
+    if ((e = cudaMalloc(&r.B, s->ws_bytes)) != cudaSuccess || (e = cudaMalloc(&r.C, s->ws_bytes)) != cudaSuccess) {
+      free_slab(s);
+      return fail(ARENA_ENOMEM, "slab workspaces: " + std::string(cudaGetErrorString(e)));
+    }
+  }
+  if (!loopback) {
+    NcclApi* a = nccl_api();
+    if (!a) {
+      free_slab(s);
+      return fail(ARENA_ENCCL, "libnccl.so.2 not found");
+    }
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof uid);
+    ncclResult_t r = a->CommInitRank(&s->comm, P, uid, rank);
+    if (r != ncclSuccess) {
+      s->comm = nullptr;
+      free_slab(s);
+      return nccl_fail(r, "ncclCommInitRank");
+    }
+  }
+  *out = s;
+  return ARENA_OK;
+}
+
+Pow2Args slab_args(arena_fft_slab* s, SlabRank& r, int rank, const void* f, void* u, cudaStream_t st, int phases) {
+  arena_fft_plan* p = s->base;
+  return Pow2Args{f, u, r.B, p->tw, p->stw, p->n, p->nc, p->ncp, st, nullptr, &r.tma, p->sm_count,
+                  s->ni, s->nj, s->P, rank * s->nj, r.C, phases};
+}
+
+cudaError_t slab_phase(arena_fft_slab* s, SlabRank& r, int rank, const void* f, void* u, cudaStream_t st, int phases) {
+  const Pow2Args a = slab_args(s, r, rank, f, u, st, phases);
+  return s->base->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
+}
+
+// All-to-all between workspaces: forward (B chunk d of rank r -> C chunk r of rank d)
+// or backward (C chunk d of rank r -> B chunk r of rank d).
+arena_status slab_exchange(arena_fft_slab* s, cudaStream_t st, bool forward) {
+  const size_t bytes = s->chunk_elems * s->base->elem;
+  if (s->loopback) {
+    for (int r = 0; r < s->P; ++r)
+      for (int d = 0; d < s->P; ++d) {
+        const char* src = static_cast<const char*>(forward ? s->ranks[r].B : s->ranks[r].C) + size_t(d) * bytes;
+        char* dst = static_cast<char*>(forward ? s->ranks[d].C : s->ranks[d].B) + size_t(r) * bytes;
+        cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "loopback exchange");
+      }
+    return ARENA_OK;
+  }
+  NcclApi* a = nccl_api();
+  const ncclDataType_t dt = s->base->prec == 64 ? ncclFloat64 : ncclFloat32;
+  SlabRank& me = s->ranks[0];
+  const char* src = static_cast<const char*>(forward ? me.B : me.C);
+  char* dst = static_cast<char*>(forward ? me.C : me.B);
+  ncclResult_t res = a->GroupStart();
+  if (res != ncclSuccess) return nccl_fail(res, "ncclGroupStart");
+  for (int d = 0; d < s->P; ++d) {
+    if ((res = a->Send(src + size_t(d) * bytes, s->chunk_elems, dt, d, s->comm, st)) != ncclSuccess)
+      return nccl_fail(res, "ncclSend");
+    if ((res = a->Recv(dst + size_t(d) * bytes, s->chunk_elems, dt, d, s->comm, st)) != ncclSuccess)
+      return nccl_fail(res, "ncclRecv");
+  }
+  if ((res = a->GroupEnd()) != ncclSuccess) return nccl_fail(res, "ncclGroupEnd");
+  return ARENA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+arena_status arena_nccl_unique_id(void* out, int len) {
+  if (!out || len < int(sizeof(ncclUniqueId))) return fail(ARENA_EINVAL, "unique id buffer too small");
+  NcclApi* a = nccl_api();
+  if (!a) return fail(ARENA_ENCCL, "libnccl.so.2 not found");
+  ncclUniqueId uid;
+  ncclResult_t r = a->GetUniqueId(&uid);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  memcpy(out, &uid, sizeof uid);
+  return ARENA_OK;
+}
+
+int arena_nccl_unique_id_bytes(void) { return int(sizeof(ncclUniqueId)); }
+
+arena_status arena_slab_create(arena_fft_slab** out, int n, int precision_bits, int device, int nranks, int rank,
+                               const void* nccl_id) {
+  if (!nccl_id) return fail(ARENA_EINVAL, "NCCL unique id is NULL");
+  return slab_init(out, n, precision_bits, device, nranks, rank, 0, nccl_id);
+}
+
+arena_status arena_slab_create_loopback(arena_fft_slab** out, int n, int precision_bits, int device, int nvranks) {
+  return slab_init(out, n, precision_bits, device, nvranks, 0, 1, nullptr);
+}
+
+void arena_slab_destroy(arena_fft_slab* s) { free_slab(s); }
+
+arena_status arena_slab_info(const arena_fft_slab* s, int* ni, int* nj, size_t* chunk_bytes, size_t* workspace_bytes) {
+  if (!s) return fail(ARENA_EINVAL, "slab is NULL");
+  if (ni) *ni = s->ni;
+  if (nj) *nj = s->nj;
+  if (chunk_bytes) *chunk_bytes = s->chunk_elems * s->base->elem;
+  if (workspace_bytes) *workspace_bytes = s->ws_bytes;
+  return ARENA_OK;
+}
+
+arena_status arena_slab_solve_device(arena_fft_slab* s, const void* d_f, void* d_u, void* stream) {
+  if (!s || !d_f || !d_u) return fail(ARENA_EINVAL, "NULL slab or buffer");
+  DeviceGuard g(s->base->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t slab_bytes = size_t(s->ni) * s->n * s->n * s->base->elem;
+  auto fr = [&](int r) { return static_cast<const char*>(d_f) + (s->loopback ? size_t(r) * slab_bytes : 0); };
+  auto ur = [&](int r) { return static_cast<char*>(d_u) + (s->loopback ? size_t(r) * slab_bytes : 0); };
+  const int nr = int(s->ranks.size());
+  cudaError_t e;
+  for (int v = 0; v < nr; ++v) {
+    const int rank = s->loopback ? v : s->rank;
+    if ((e = slab_phase(s, s->ranks[v], rank, fr(v), ur(v), st, kPhaseZY)) != cudaSuccess)
+      return cuda_fail(e, "slab K1+K2");
+  }
+  arena_status stt = slab_exchange(s, st, true);
+  if (stt != ARENA_OK) return stt;
+  for (int v = 0; v < nr; ++v) {
+    const int rank = s->loopback ? v : s->rank;
+    if ((e = slab_phase(s, s->ranks[v], rank, fr(v), ur(v), st, kPhaseX)) != cudaSuccess) return cuda_fail(e, "slab K3");
+  }
+  if ((stt = slab_exchange(s, st, false)) != ARENA_OK) return stt;
+  for (int v = 0; v < nr; ++v) {
+    const int rank = s->loopback ? v : s->rank;
+    if ((e = slab_phase(s, s->ranks[v], rank, fr(v), ur(v), st, kPhaseYZ)) != cudaSuccess)
+      return cuda_fail(e, "slab K4+K5");
+  }
   return ARENA_OK;
 }
 

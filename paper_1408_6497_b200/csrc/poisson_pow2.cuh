@@ -55,7 +55,7 @@ __host__ __device__ constexpr int spec_pitch(int n) { return (n / 2 + 1 + 7) / 8
 #define ARENA_X_SMEM (64 * 1024)  // shared-memory budget per x tile
 #endif
 #ifndef ARENA_JBLOCK
-#define ARENA_JBLOCK 8  // j-block of the half-spectrum layout (see row_off)
+#define ARENA_JBLOCK 8  // j-block of the half-spectrum layout (see Layout)
 #endif
 
 // ------------------------------------------------------------ configuration
@@ -91,16 +91,48 @@ struct ContigCfg {  // z passes: rows of NR reals = M = NR/2 complex
 
 __device__ __forceinline__ int signed_freq(int k, int n) { return k <= n / 2 ? k : k - n; }  // fft_solver.hpp:19
 
-// Half-spectrum row (i, j) offset in elements.  Rows are grouped in blocks of
-// JB consecutive j: S[(((j / JB) * n + i) * JB + j % JB) * ncp + k].  A y tile
-// (fixed i) then reads n/JB contiguous JB-row chunks and an x tile (fixed j)
-// reads rows JB*ncp apart, so both strided passes touch O(n/JB) and
-// O(JB*ncp*16 B*n / 2 MB) pages instead of 5 and n (the row-major x pass ran
-// at 3.1 TB/s on B200, TLB-bound; tools/pattern_bw.cu).
-template <int N>
-__host__ __device__ __forceinline__ size_t row_off(int i, int j) {
-  constexpr int JB = ARENA_JBLOCK < N ? ARENA_JBLOCK : N;
-  return ((size_t(j / JB) * N + i) * JB + (j % JB)) * size_t(spec_pitch(N));
+// Half-spectrum layout, shared by the single-GPU and the slab (multi-GPU)
+// paths.  A workspace holds P chunks of ni x nj rows of ncp complex; inside a
+// chunk rows are blocked by JB = min(8, nj) in j:
+//   row(c, il, jl) = c*ni*nj + ((jl / JB)*ni + il)*JB + jl % JB.
+// Single GPU: P = 1, ni = nj = n, so row(i, j) = ((j/8)*n + i)*8 + j%8 — a y tile
+// (fixed i) reads n/8 contiguous 8-row chunks and an x tile (fixed j) reads rows
+// 8*ncp apart; with plain row-major rows the x pass touched n different 2 MB
+// pages per tile and its access pattern alone capped at 3.1 TB/s on B200
+// (tools/pattern_bw.cu; 6.2-6.4 TB/s blocked).
+// Slab over P ranks (ni = nj = n/P): layout B (K1/K2/K4/K5 on a rank's i-slab)
+// puts j in chunk c = j / nj, so the block for peer c is contiguous; layout C
+// (K3 on a j-slab) puts i in chunk c = i / ni — exactly what arrives from rank c.
+struct Layout {
+  int ni, nj;       // rows per chunk: il in [0, ni), jl in [0, nj)
+  int nis, njs;     // log2 ni, log2 nj
+  int jbs;          // log2 JB
+};
+
+__host__ __device__ __forceinline__ size_t lrow(const Layout& g, int c, int il, int jl) {
+  return (size_t(c) << (g.nis + g.njs)) + ((size_t(jl >> g.jbs) * g.ni + il) << g.jbs) + (jl & ((1 << g.jbs) - 1));
+}
+// Layout B: (local i, global j).  Layout C: (global i, local j).
+__host__ __device__ __forceinline__ size_t rowB(const Layout& g, int il, int j) {
+  return lrow(g, j >> g.njs, il, j & (g.nj - 1));
+}
+__host__ __device__ __forceinline__ size_t rowC(const Layout& g, int i, int jl) {
+  return lrow(g, i >> g.nis, i & (g.ni - 1), jl);
+}
+
+inline int ilog2_host(int x) {
+  int r = 0;
+  while ((1 << r) < x) ++r;
+  return r;
+}
+inline Layout make_layout(int ni, int nj) {
+  Layout g;
+  g.ni = ni;
+  g.nj = nj;
+  g.nis = ilog2_host(ni);
+  g.njs = ilog2_host(nj);
+  g.jbs = ilog2_host(nj < ARENA_JBLOCK ? nj : ARENA_JBLOCK);
+  return g;
 }
 
 template <typename V>
@@ -117,7 +149,7 @@ __device__ __forceinline__ V* smem_base() {
 template <typename T, int NR>
 __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
     k_zfwd(const T* __restrict__ f, vec2_t<T>* __restrict__ S, const vec2_t<T>* __restrict__ tw,
-           const vec2_t<T>* __restrict__ stw) {
+           const vec2_t<T>* __restrict__ stw, Layout g) {
   using V = vec2_t<T>;
   using C = ContigCfg<T, NR>;
   constexpr int M = C::M, E = C::E, P = C::P, L = C::L;
@@ -127,7 +159,6 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
   const int l = threadIdx.x % L, t = threadIdx.x / L;
   const size_t row = size_t(blockIdx.x) * L + l;
   const V* src = reinterpret_cast<const V*>(f + row * NR);
-  (void)ncp;
   V v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = __ldcs(src + t + P * e);
@@ -135,7 +166,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
 #pragma unroll
   for (int e = 0; e < E; ++e) sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
   __syncthreads();
-  V* dst = S + row_off<NR>(int(row / NR), int(row % NR));
+  V* dst = S + rowB(g, int(row / NR), int(row % NR)) * ncp;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int k = t + P * e;
@@ -156,7 +187,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
 template <typename T, int NR>
 __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
     k_zinv(const vec2_t<T>* __restrict__ S, T* __restrict__ u, const vec2_t<T>* __restrict__ tw,
-           const vec2_t<T>* __restrict__ stw) {
+           const vec2_t<T>* __restrict__ stw, Layout g) {
   using V = vec2_t<T>;
   using C = ContigCfg<T, NR>;
   constexpr int M = C::M, E = C::E, P = C::P, L = C::L;
@@ -166,8 +197,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
   V* xm = sm + M * L;  // X[M] per line
   const int l = threadIdx.x % L, t = threadIdx.x / L;
   const size_t row = size_t(blockIdx.x) * L + l;
-  const V* src = S + row_off<NR>(int(row / NR), int(row % NR));
-  (void)ncp;
+  const V* src = S + rowB(g, int(row / NR), int(row % NR)) * ncp;
   V v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -201,7 +231,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
 // --------------------------------------------------------------- K2/K4 ypass
 template <typename T, int N, int S>
 __global__ void __launch_bounds__(StridedCfg<T, N, 0>::THREADS, ARENA_STRIDED_MINB)
-    k_ypass(vec2_t<T>* __restrict__ spec, const vec2_t<T>* __restrict__ stw) {
+    k_ypass(vec2_t<T>* __restrict__ spec, const vec2_t<T>* __restrict__ stw, Layout g) {
   using V = vec2_t<T>;
   using C = StridedCfg<T, N, 0>;
   constexpr int E = C::E, P = C::P, L = C::L;
@@ -212,14 +242,13 @@ __global__ void __launch_bounds__(StridedCfg<T, N, 0>::THREADS, ARENA_STRIDED_MI
   const bool valid = k < nc;
   V* base = spec + k;
   const int i = blockIdx.y;
-  (void)ncp;
   V v[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) v[e] = valid ? __ldcs(base + row_off<N>(i, t + P * e)) : V{T(0), T(0)};
+  for (int e = 0; e < E; ++e) v[e] = valid ? __ldcs(base + rowB(g, i, t + P * e) * ncp) : V{T(0), T(0)};
   line_fft<N, E, L, S>(v, sm, stw, t, l);
   if (valid) {
 #pragma unroll
-    for (int e = 0; e < E; ++e) __stcs(base + row_off<N>(i, t + P * e), v[e]);
+    for (int e = 0; e < E; ++e) __stcs(base + rowB(g, i, t + P * e) * ncp, v[e]);
   }
 }
 
@@ -230,7 +259,7 @@ __global__ void __launch_bounds__(StridedCfg<T, N, 0>::THREADS, ARENA_STRIDED_MI
 // registers between the two transforms.
 template <typename T, int N>
 __global__ void __launch_bounds__(StridedCfg<T, N, 1>::THREADS, ARENA_STRIDED_MINB)
-    k_xmid(vec2_t<T>* __restrict__ spec, const vec2_t<T>* __restrict__ stw, T scale, T four_pi2) {
+    k_xmid(vec2_t<T>* __restrict__ spec, const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g) {
   using V = vec2_t<T>;
   using C = StridedCfg<T, N, 1>;
   constexpr int E = C::E, P = C::P, L = C::L;
@@ -240,8 +269,8 @@ __global__ void __launch_bounds__(StridedCfg<T, N, 1>::THREADS, ARENA_STRIDED_MI
   const int k = blockIdx.x * L + l;
   const int j = blockIdx.y;
   const bool valid = k < nc;
-  const size_t istride = row_off<N>(1, j) - row_off<N>(0, j);  // JB * ncp
-  V* base = spec + row_off<N>(0, j) + k;
+  const size_t istride = (rowC(g, 1, j) - rowC(g, 0, j)) * ncp;  // JB * ncp (single GPU)
+  V* base = spec + rowC(g, 0, j) * ncp + k;
   V v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = valid ? __ldcs(base + size_t(t + P * e) * istride) : V{T(0), T(0)};
@@ -298,25 +327,32 @@ struct TmaCfg {
   static constexpr int L = pow2_floor(imax(2, imin(8, (64 * 1024) / (N * VB))));
   static constexpr int THREADS = L * P;
   static constexpr int NC = N / 2 + 1;
-  static constexpr int KT = (NC + L - 1) / L;  // k tiles per (i) or (j)
+  static constexpr int KT = (NC + L - 1) / L;  // k tiles per line set
   static constexpr int TILE = N * L;          // elements per tile
-  static constexpr int JB = ARENA_JBLOCK < N ? ARENA_JBLOCK : N;
-  static constexpr int IB = N < 256 ? N : 256;  // TMA box rows for the x pass
   static constexpr int NBUF = (ARENA_TMA_NBUF * TILE * VB <= 200 * 1024) ? ARENA_TMA_NBUF : imin(2, ARENA_TMA_NBUF);
   static constexpr int SMEM = NBUF * TILE * VB + 8 * NBUF;
 };
 
-// PASS 0: y forward, 1: y backward, 2: x forward * Poisson symbol * x backward.
+// TMA view of a workspace in Layout g: a 5-D tensor of reals
+//   {2*nc (re/im of k), JB (jl % JB), ni (il), nj/JB (jl / JB), P (chunk)}.
+// y tile (fixed il): box {2L, JB, 1, nj/JB, P}  -> all j in natural order.
+// x tile (fixed jl): boxes {2L, 1, IB, 1, 1} over il blocks and chunks -> all i.
+__host__ __device__ constexpr int tma_ib(int ni) { return ni < 256 ? ni : 256; }
+
+// PASS 0: y forward, 1: y backward (layout B, tiles over (il, k-tile));
+// PASS 2: x forward * Poisson symbol * x backward (layout C, tiles over (jl, k-tile)).
+// j0: global j of this rank's first local j (x pass symbol; 0 on one GPU).
 template <typename T, int N, int PASS>
 __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
     k_strided_tma(const __grid_constant__ CUtensorMap tmap, vec2_t<T>* __restrict__ spec,
-                  const vec2_t<T>* __restrict__ stw, T scale, T four_pi2) {
+                  const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g, int nchunks, int j0) {
   using V = vec2_t<T>;
   using C = TmaCfg<T, N>;
   constexpr int E = C::E, P = C::P, L = C::L, KT = C::KT, TILE = C::TILE;
-  constexpr int NT = N * KT;
+  constexpr int ncp = spec_pitch(N);
   constexpr uint32_t TILE_BYTES = TILE * sizeof(V);
   constexpr int NBUF = C::NBUF;
+  const int NT = (PASS < 2 ? g.ni : g.nj) * KT;
   V* bufs = smem_base<V>();
   uint64_t* bar = reinterpret_cast<uint64_t*>(bufs + NBUF * TILE);
   const int tid = threadIdx.x;
@@ -329,15 +365,17 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
   }
   __syncthreads();
 
-  auto issue = [&](int g, V* dst, uint64_t* b) {
-    const int outer = g / KT, kt = g % KT;
+  auto issue = [&](int gt, V* dst, uint64_t* b) {
+    const int outer = gt / KT, kt = gt % KT;
     mbar_arrive_expect_tx(b, TILE_BYTES);
-    if constexpr (PASS < 2) {  // y tile: fixed i = outer, all j (JB-row chunks)
-      tma_load_4d(dst, &tmap, b, 2 * kt * L, 0, outer, 0);
-    } else {  // x tile: fixed j = outer, all i in boxes of IB rows
-#pragma unroll
-      for (int q = 0; q < N / C::IB; ++q)
-        tma_load_4d(dst + q * C::IB * L, &tmap, b, 2 * kt * L, outer % C::JB, q * C::IB, outer / C::JB);
+    if constexpr (PASS < 2) {  // y tile: fixed il = outer, all j
+      tma_load_5d(dst, &tmap, b, 2 * kt * L, 0, outer, 0, 0);
+    } else {  // x tile: fixed jl = outer, all i (chunk c, il blocks of IB)
+      const int IB = tma_ib(g.ni);
+      const int jb = (1 << g.jbs) - 1;
+      for (int c = 0; c < nchunks; ++c)
+        for (int q = 0; q < g.ni; q += IB)
+          tma_load_5d(dst + (size_t(c) * g.ni + q) * L, &tmap, b, 2 * kt * L, outer & jb, q, outer >> g.jbs, c);
     }
   };
 
@@ -349,17 +387,17 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
       if (gp < NT) issue(gp, bufs + p * TILE, &bar[p]);
     }
   }
-  int g = blockIdx.x;
-  for (int it = 0; g < NT; ++it, g += gridDim.x) {
+  int gt = blockIdx.x;
+  for (int it = 0; gt < NT; ++it, gt += gridDim.x) {
     const int b = it % NBUF;
     V* cur = bufs + b * TILE;
     if constexpr (NBUF == 1) {  // no intra-CTA prefetch: co-resident CTAs overlap instead
       if (tid == 0) {
         fence_proxy_async_smem();
-        issue(g, bufs, &bar[0]);
+        issue(gt, bufs, &bar[0]);
       }
     } else {
-      const int gn = g + (NBUF - 1) * gridDim.x;
+      const int gn = gt + (NBUF - 1) * gridDim.x;
       if (tid == 0 && gn < NT) {  // refill the buffer iteration it-1 used
         const int bn = (it + NBUF - 1) % NBUF;
         fence_proxy_async_smem();
@@ -371,16 +409,15 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = cur[(t + P * e) * L + l];
     __syncthreads();  // the tile buffer becomes exchange scratch
-    const int outer = g / KT;
-    const int k = (g % KT) * L + l;
+    const int outer = gt / KT;
+    const int k = (gt % KT) * L + l;
     if constexpr (PASS == 0) {
       line_fft<N, E, L, -1>(v, cur, stw, t, l);
     } else if constexpr (PASS == 1) {
       line_fft<N, E, L, +1>(v, cur, stw, t, l);
     } else {
       line_fft<N, E, L, -1>(v, cur, stw, t, l);
-      const int j = outer;
-      const T kj = T(signed_freq(j, N)), kk = T(k);
+      const T kj = T(signed_freq(j0 + outer, N)), kk = T(k);
       const T c = kj * kj + kk * kk;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
@@ -395,12 +432,10 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
     if (k < C::NC) {
       if constexpr (PASS < 2) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) __stcs(spec + row_off<N>(outer, t + P * e) + k, v[e]);
+        for (int e = 0; e < E; ++e) __stcs(spec + rowB(g, outer, t + P * e) * ncp + k, v[e]);
       } else {
-        V* base = spec + row_off<N>(0, outer) + k;
-        constexpr size_t istride = size_t(C::JB) * spec_pitch(N);
 #pragma unroll
-        for (int e = 0; e < E; ++e) __stcs(base + size_t(t + P * e) * istride, v[e]);
+        for (int e = 0; e < E; ++e) __stcs(spec + rowC(g, t + P * e, outer) * ncp + k, v[e]);
       }
     }
     // No barrier needed here: every thread's last access to `cur` (the tile

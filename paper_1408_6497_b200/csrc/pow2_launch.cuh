@@ -52,31 +52,31 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// Half spectrum as a 4-D tensor of reals: {2*nc (re/im of k), JB (j % JB),
-// n (i), n/JB (j / JB)} — the blocked layout of row_off().
+// TMA descriptor of a workspace in Layout g (5-D, see k_strided_tma).
 template <typename T, int N>
-cudaError_t encode_spec_maps(TmaCache* c, void* spec) {
+cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool ybox) {
   using C = TmaCfg<T, N>;
   auto enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
   const CUtensorMapDataType dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const cuuint64_t row = cuuint64_t(spec_pitch(N)) * 2 * sizeof(T);
-  const cuuint64_t dims[4] = {cuuint64_t(2 * C::NC), cuuint64_t(C::JB), cuuint64_t(N), cuuint64_t(N / C::JB)};
-  const cuuint64_t strides[3] = {row, row * C::JB, row * C::JB * N};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const cuuint32_t box_y[4] = {cuuint32_t(2 * C::L), cuuint32_t(C::JB), 1, cuuint32_t(N / C::JB)};
-  const cuuint32_t box_x[4] = {cuuint32_t(2 * C::L), 1, cuuint32_t(C::IB), 1};
-  CUresult r = enc(reinterpret_cast<CUtensorMap*>(c->maps[0]), dt, 4, spec, dims, strides, box_y, estr,
+  const int JB = 1 << g.jbs;
+  const cuuint64_t dims[5] = {cuuint64_t(2 * C::NC), cuuint64_t(JB), cuuint64_t(g.ni), cuuint64_t(g.nj / JB),
+                              cuuint64_t(nchunks)};
+  const cuuint64_t strides[4] = {row, row * JB, row * JB * g.ni, row * g.ni * g.nj};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  cuuint32_t box[5];
+  if (ybox) {
+    box[0] = 2 * C::L; box[1] = JB; box[2] = 1; box[3] = g.nj / JB; box[4] = nchunks;
+  } else {
+    box[0] = 2 * C::L; box[1] = 1; box[2] = tma_ib(g.ni); box[3] = 1; box[4] = 1;
+  }
+  for (int d = 1; d < 5; ++d)
+    if (box[d] > 256) return cudaErrorInvalidValue;
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(out), dt, 5, spec, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  r = enc(reinterpret_cast<CUtensorMap*>(c->maps[1]), dt, 4, spec, dims, strides, box_x, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  c->spec = spec;
-  c->n = N;
-  return cudaSuccess;
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 template <typename T>
@@ -85,7 +85,8 @@ inline const vec2_t<T>* stw_ptr(const Pow2Args& a, int which, int E) {
 }
 
 template <typename T, int N, int PASS>
-cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, T scale, T four_pi2) {
+cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* spec, const Layout& g, T scale,
+                               T four_pi2) {
   using C = TmaCfg<T, N>;
   using V = vec2_t<T>;
   auto kern = k_strided_tma<T, N, PASS>;
@@ -93,11 +94,11 @@ cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, T scal
   if (e) return e;
   int per_sm = 1;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM))) return e;
-  const int tiles = N * C::KT;
+  const int tiles = (PASS < 2 ? g.ni : g.nj) * C::KT;
   int grid = a.sm_count * (per_sm > 0 ? per_sm : 1);
   if (grid > tiles) grid = tiles;
-  kern<<<grid, C::THREADS, C::SMEM, a.stream>>>(map, static_cast<V*>(a.spec), stw_ptr<T>(a, 1, C::E), scale,
-                                               four_pi2);
+  kern<<<grid, C::THREADS, C::SMEM, a.stream>>>(map, static_cast<V*>(spec), stw_ptr<T>(a, 1, C::E), scale, four_pi2, g,
+                                               a.nchunks, a.j0);
   return cudaGetLastError();
 }
 
@@ -114,47 +115,72 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   const V* tw = static_cast<const V*>(a.tw);
   V* S = static_cast<V*>(a.spec);
   cudaError_t e;
-  if ((e = ensure_smem<k_zfwd<T, NR>>(CC::SMEM, CC::THREADS))) return e;
-  if ((e = ensure_smem<k_zinv<T, NR>>(CC::SMEM, CC::THREADS))) return e;
-  if ((e = ensure_smem<k_ypass<T, NR, -1>>(SC::SMEM, SC::THREADS))) return e;
-  if ((e = ensure_smem<k_ypass<T, NR, +1>>(SC::SMEM, SC::THREADS))) return e;
-  if ((e = ensure_smem<k_xmid<T, NR>>(XC::SMEM, XC::THREADS))) return e;
   static_assert((size_t(NR) * NR) % CC::L == 0, "rows per CTA must divide n^2");
   if (a.ncp != spec_pitch(NR) || a.nc != NR / 2 + 1) return cudaErrorInvalidValue;
-  static_assert((CC::L & (CC::L - 1)) == 0 && (SC::L & (SC::L - 1)) == 0, "tile widths are powers of two");
-  const unsigned zgrid = unsigned((size_t(NR) * NR) / CC::L);
-  const dim3 sgrid((a.nc + SC::L - 1) / SC::L, NR);
-  const dim3 xgrid((a.nc + XC::L - 1) / XC::L, NR);
+  if (size_t(a.ni) * NR % CC::L) return cudaErrorInvalidValue;
+  if ((e = ensure_smem<k_zfwd<T, NR>>(CC::SMEM, CC::THREADS))) return e;
+  if ((e = ensure_smem<k_zinv<T, NR>>(CC::SMEM, CC::THREADS))) return e;
+  const Layout gB = make_layout(a.ni, NR / a.nchunks);  // (local i, global j) chunks of nj
+  const Layout gC = make_layout(NR / a.nchunks, a.nj);  // (global i, local j) chunks of ni
+  const unsigned zgrid = unsigned((size_t(a.ni) * NR) / CC::L);
   const T scale = T(1.0 / (double(NR) * NR * NR));  // fft_solver.cpp:67
   const T four_pi2 = T(4.0 * M_PI * M_PI);           // fft_solver.cpp:66
   const bool tma = a.tma != nullptr && NR >= 4;
-  if (tma && (a.tma->spec != a.spec || a.tma->n != NR)) {
-    if ((e = encode_spec_maps<T, NR>(a.tma, a.spec))) return e;
-  }
-  mark(a, 0);
-  k_zfwd<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw,
-                                                             stw_ptr<T>(a, 0, CC::E));
+  if (!tma && a.nchunks != 1) return cudaErrorNotSupported;  // classic kernels are single-GPU only
   if (tma) {
-    const CUtensorMap& my = *reinterpret_cast<const CUtensorMap*>(a.tma->maps[0]);
-    const CUtensorMap& mx = *reinterpret_cast<const CUtensorMap*>(a.tma->maps[1]);
-    mark(a, 1);
-    if ((e = launch_strided_tma<T, NR, 0>(a, my, scale, four_pi2))) return e;
-    mark(a, 2);
-    if ((e = launch_strided_tma<T, NR, 2>(a, mx, scale, four_pi2))) return e;
-    mark(a, 3);
-    if ((e = launch_strided_tma<T, NR, 1>(a, my, scale, four_pi2))) return e;
-  } else {
-    mark(a, 1);
-    k_ypass<T, NR, -1><<<sgrid, SC::THREADS, SC::SMEM, a.stream>>>(S, stw_ptr<T>(a, 1, SC::E));
-    mark(a, 2);
-    k_xmid<T, NR><<<xgrid, XC::THREADS, XC::SMEM, a.stream>>>(S, stw_ptr<T>(a, 1, XC::E), scale, four_pi2);
-    mark(a, 3);
-    k_ypass<T, NR, +1><<<sgrid, SC::THREADS, SC::SMEM, a.stream>>>(S, stw_ptr<T>(a, 1, SC::E));
+    TmaCache* c = a.tma;
+    if (c->specB != a.spec || c->specC != a.specC || c->n != NR || c->ni != a.ni || c->nj != a.nj ||
+        c->nchunks != a.nchunks) {
+      if ((e = encode_map<T, NR>(c->maps[0], a.spec, gB, a.nchunks, true))) return e;
+      if ((e = encode_map<T, NR>(c->maps[1], a.specC, gC, a.nchunks, false))) return e;
+      c->specB = a.spec;
+      c->specC = a.specC;
+      c->n = NR;
+      c->ni = a.ni;
+      c->nj = a.nj;
+      c->nchunks = a.nchunks;
+    }
   }
-  mark(a, 4);
-  k_zinv<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw,
-                                                             stw_ptr<T>(a, 0, CC::E));
-  mark(a, 5);
+  const CUtensorMap* my = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[0]) : nullptr;
+  const CUtensorMap* mx = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[1]) : nullptr;
+  int mk = 0;
+  if (a.phases & kPhaseZY) {
+    mark(a, mk++);
+    k_zfwd<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw,
+                                                               stw_ptr<T>(a, 0, CC::E), gB);
+    mark(a, mk++);
+    if (tma) {
+      if ((e = launch_strided_tma<T, NR, 0>(a, *my, a.spec, gB, scale, four_pi2))) return e;
+    } else {
+      if ((e = ensure_smem<k_ypass<T, NR, -1>>(SC::SMEM, SC::THREADS))) return e;
+      k_ypass<T, NR, -1><<<dim3((a.nc + SC::L - 1) / SC::L, NR), SC::THREADS, SC::SMEM, a.stream>>>(
+          S, stw_ptr<T>(a, 1, SC::E), gB);
+    }
+  }
+  if (a.phases & kPhaseX) {
+    mark(a, mk++);
+    if (tma) {
+      if ((e = launch_strided_tma<T, NR, 2>(a, *mx, a.specC, gC, scale, four_pi2))) return e;
+    } else {
+      if ((e = ensure_smem<k_xmid<T, NR>>(XC::SMEM, XC::THREADS))) return e;
+      k_xmid<T, NR><<<dim3((a.nc + XC::L - 1) / XC::L, NR), XC::THREADS, XC::SMEM, a.stream>>>(
+          S, stw_ptr<T>(a, 1, XC::E), scale, four_pi2, gC);
+    }
+  }
+  if (a.phases & kPhaseYZ) {
+    mark(a, mk++);
+    if (tma) {
+      if ((e = launch_strided_tma<T, NR, 1>(a, *my, a.spec, gB, scale, four_pi2))) return e;
+    } else {
+      if ((e = ensure_smem<k_ypass<T, NR, +1>>(SC::SMEM, SC::THREADS))) return e;
+      k_ypass<T, NR, +1><<<dim3((a.nc + SC::L - 1) / SC::L, NR), SC::THREADS, SC::SMEM, a.stream>>>(
+          S, stw_ptr<T>(a, 1, SC::E), gB);
+    }
+    mark(a, mk++);
+    k_zinv<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw, stw_ptr<T>(a, 0, CC::E),
+                                                               gB);
+    mark(a, mk++);
+  }
   return cudaGetLastError();
 }
 

@@ -22,14 +22,14 @@
 namespace {
 
 template <typename T>
-__global__ void k_modes(T* __restrict__ out, int n, int nmodes, const int* __restrict__ kv,
+__global__ void k_modes(T* __restrict__ out, int n, int i0, int ni, int nmodes, const int* __restrict__ kv,
                         const double* __restrict__ coef, const double2* __restrict__ tw) {
-  const long long N = (long long)n * n * n;
+  const long long N = (long long)ni * n * n;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
        idx += (long long)gridDim.x * blockDim.x) {
     const int k = int(idx % n);
     const long long ij = idx / n;
-    const int j = int(ij % n), i = int(ij / n);
+    const int j = int(ij % n), i = i0 + int(ij / n);
     double acc = 0.0;
     for (int m = 0; m < nmodes; ++m) {
       long long p = ((long long)kv[3 * m] * i + (long long)kv[3 * m + 1] * j + (long long)kv[3 * m + 2] * k) % n;
@@ -42,13 +42,14 @@ __global__ void k_modes(T* __restrict__ out, int n, int nmodes, const int* __res
 }
 
 template <typename T>
-__global__ void k_gauss(T* __restrict__ out, int n, double alpha, double cx, double cy, double cz, int which) {
-  const long long N = (long long)n * n * n;
+__global__ void k_gauss(T* __restrict__ out, int n, int i0, int ni, double alpha, double cx, double cy, double cz,
+                        int which) {
+  const long long N = (long long)ni * n * n;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
        idx += (long long)gridDim.x * blockDim.x) {
     const int k = int(idx % n);
     const long long ij = idx / n;
-    const int j = int(ij % n), i = int(ij / n);
+    const int j = int(ij % n), i = i0 + int(ij / n);
     const double x = double(i) / n, y = double(j) / n, z = double(k) / n;
     double acc = 0.0;
     for (int a = -1; a <= 1; ++a)
@@ -69,11 +70,12 @@ thread_local std::string g_src_err;
 
 extern "C" {
 
-// out (device, n^3 of precision_bits) = sum_m Re(coef_m e^{2 pi i k_m.x}); k: 3*nmodes ints,
-// coef: 2*nmodes doubles (re, im), both host arrays.
-arena_status arena_source_modes(int n, int precision_bits, int nmodes, const int* k, const double* coef, void* d_out,
-                                void* stream) {
-  if (n < 2 || nmodes < 0 || !d_out || (nmodes && (!k || !coef))) return ARENA_EINVAL;
+// out (device, planes i0 .. i0+ni-1 of the n^3 field, precision_bits) =
+// sum_m Re(coef_m e^{2 pi i k_m.x}); k: 3*nmodes ints, coef: 2*nmodes doubles (re, im), host arrays.
+arena_status arena_source_modes_slab(int n, int precision_bits, int nmodes, const int* k, const double* coef, int i0,
+                                     int ni, void* d_out, void* stream) {
+  if (n < 2 || nmodes < 0 || !d_out || (nmodes && (!k || !coef)) || i0 < 0 || ni < 1 || i0 + ni > n)
+    return ARENA_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   std::vector<double> tw(2 * size_t(n));
   const long double two_pi = 6.283185307179586476925286766559005768L;
@@ -94,10 +96,10 @@ arena_status arena_source_modes(int n, int precision_bits, int nmodes, const int
     cudaMemcpy(d_c, coef, sizeof(double) * 2 * nmodes, cudaMemcpyHostToDevice);
   }
   if (precision_bits == 64)
-    k_modes<double><<<148 * 16, 256, 0, s>>>(static_cast<double*>(d_out), n, nmodes, static_cast<int*>(d_k),
+    k_modes<double><<<148 * 16, 256, 0, s>>>(static_cast<double*>(d_out), n, i0, ni, nmodes, static_cast<int*>(d_k),
                                             static_cast<double*>(d_c), static_cast<double2*>(d_tw));
   else
-    k_modes<float><<<148 * 16, 256, 0, s>>>(static_cast<float*>(d_out), n, nmodes, static_cast<int*>(d_k),
+    k_modes<float><<<148 * 16, 256, 0, s>>>(static_cast<float*>(d_out), n, i0, ni, nmodes, static_cast<int*>(d_k),
                                            static_cast<double*>(d_c), static_cast<double2*>(d_tw));
   cudaError_t e = cudaGetLastError();
   cudaStreamSynchronize(s);
@@ -107,16 +109,26 @@ arena_status arena_source_modes(int n, int precision_bits, int nmodes, const int
   return e == cudaSuccess ? ARENA_OK : ARENA_ECUDA;
 }
 
-// which = 0: u (periodised Gaussian), 1: f = -Lap u.
-arena_status arena_source_gaussian(int n, int precision_bits, double alpha, double cx, double cy, double cz, int which,
-                                   void* d_out, void* stream) {
-  if (n < 2 || !d_out || (which != 0 && which != 1)) return ARENA_EINVAL;
+arena_status arena_source_modes(int n, int precision_bits, int nmodes, const int* k, const double* coef, void* d_out,
+                                void* stream) {
+  return arena_source_modes_slab(n, precision_bits, nmodes, k, coef, 0, n, d_out, stream);
+}
+
+// which = 0: u (periodised Gaussian), 1: f = -Lap u; planes i0 .. i0+ni-1.
+arena_status arena_source_gaussian_slab(int n, int precision_bits, double alpha, double cx, double cy, double cz,
+                                        int which, int i0, int ni, void* d_out, void* stream) {
+  if (n < 2 || !d_out || (which != 0 && which != 1) || i0 < 0 || ni < 1 || i0 + ni > n) return ARENA_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (precision_bits == 64)
-    k_gauss<double><<<148 * 16, 256, 0, s>>>(static_cast<double*>(d_out), n, alpha, cx, cy, cz, which);
+    k_gauss<double><<<148 * 16, 256, 0, s>>>(static_cast<double*>(d_out), n, i0, ni, alpha, cx, cy, cz, which);
   else
-    k_gauss<float><<<148 * 16, 256, 0, s>>>(static_cast<float*>(d_out), n, alpha, cx, cy, cz, which);
+    k_gauss<float><<<148 * 16, 256, 0, s>>>(static_cast<float*>(d_out), n, i0, ni, alpha, cx, cy, cz, which);
   return cudaGetLastError() == cudaSuccess ? ARENA_OK : ARENA_ECUDA;
+}
+
+arena_status arena_source_gaussian(int n, int precision_bits, double alpha, double cx, double cy, double cz, int which,
+                                   void* d_out, void* stream) {
+  return arena_source_gaussian_slab(n, precision_bits, alpha, cx, cy, cz, which, 0, n, d_out, stream);
 }
 
 }  // extern "C"

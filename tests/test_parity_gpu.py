@@ -175,3 +175,42 @@ def test_stage_timing_hooks(cuda):
     times, nsol = p.stage_times()
     assert nsol == 3 and len(times) == 5 and all(t > 0 for t in times.values())
     p.set_stage_timing(False)
+
+
+@pytest.mark.parametrize("n,P", [(16, 2), (32, 4), (64, 2), (64, 8), (128, 4), (256, 8)])
+def test_slab_loopback_vs_oracle(cuda, n, P):
+    """Slab decomposition (K1/K2 per slab, all-to-all, K3 on j-slabs, all-to-all,
+    K4/K5) with P virtual ranks on one GPU: the chunk layouts and exchange order
+    the NCCL path uses, checked against the CPU oracle."""
+    torch = cuda
+    f_np = np.random.default_rng(n + P).uniform(-1, 1, (n, n, n))
+    f = torch.from_numpy(f_np).cuda()
+    u = torch.empty_like(f)
+    s = arena.Slab(n, P, loopback=True)
+    s.solve_device(f, u)
+    torch.cuda.synchronize()
+    assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64
+
+
+def test_slab_loopback_config4_1024(cuda):
+    """1024^3 config 4 through 8 virtual slabs vs the analytic solution."""
+    torch = cuda
+    src, f, ua = _config_device(torch, 4)
+    u = torch.empty_like(f)
+    arena.Slab(1024, 8, loopback=True).solve_device(f, u)
+    torch.cuda.synchronize()
+    e = (torch.linalg.vector_norm(u - ua) / torch.linalg.vector_norm(ua)).item()
+    assert e <= 1e-12, e
+
+
+def test_slab_nccl_single_rank(cuda):
+    """The NCCL code path with a one-rank communicator (this box has one GPU)."""
+    torch = cuda
+    n = 64
+    f_np = np.random.default_rng(5).uniform(-1, 1, (n, n, n))
+    f = torch.from_numpy(f_np).cuda()
+    u = torch.empty_like(f)
+    s = arena.Slab(n, 1, rank=0, nccl_id=arena.nccl_unique_id())
+    s.solve_device(f, u)
+    torch.cuda.synchronize()
+    assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64

@@ -123,7 +123,10 @@ def algorithmic_bytes(n: int, elem: int):
     """Per-kernel algorithmic HBM bytes: R = real field, C = half spectrum."""
     R = n ** 3 * elem
     C = n * n * (n // 2 + 1) * 2 * elem
-    return {"zfwd_r2c": R + C, "yfwd": 2 * C, "xmid_fwd_scale_inv": 2 * C, "yinv": 2 * C, "zinv_c2r": C + R}, 2 * R + 8 * C
+    per = {"zfwd_r2c": R + C, "yfwd": 2 * C, "xmid_fwd_scale_inv": 2 * C, "yinv": 2 * C, "zinv_c2r": C + R,
+           # L2-fused pairs: HBM sees f read + spectrum write (and the reverse) once
+           "zy_fused_fwd": R + C, "yz_fused_inv": C + R}
+    return per, 2 * R + 8 * C
 
 
 def cpu_sample(n: int, config: int, kind=None, min_seconds: float = 10.0, max_runs: int = 3):

@@ -256,9 +256,21 @@ __device__ __forceinline__ void stage_compute(V (&v)[E], int t, const V* __restr
   }
 }
 
+// Barrier scope of the exchanges: the whole CTA, or one warp when a warp owns
+// its lines and their shared-memory region exclusively.
+enum { kSyncCta = 0, kSyncWarp = 1 };
+template <int SYNC>
+__device__ __forceinline__ void xbarrier() {
+  if constexpr (SYNC == kSyncWarp) {
+    __syncwarp();
+  } else {
+    __syncthreads();
+  }
+}
+
 // Write stage outputs to shared memory at their Stockham destinations and
 // read back the natural-order inputs of the next stage.
-template <int N, int E, int L, int R, int NS, int SW, typename V>
+template <int N, int E, int L, int R, int NS, int SW, int SYNC, typename V>
 __device__ __forceinline__ void stage_exchange(V (&v)[E], V* sm, int t, int l) {
   constexpr int P = N / E, NB = E / R;
 #pragma unroll
@@ -268,13 +280,13 @@ __device__ __forceinline__ void stage_exchange(V (&v)[E], V* sm, int t, int l) {
 #pragma unroll
     for (int r = 0; r < R; ++r) sm[smem_idx<L, SW, V>(dst + r * NS, l)] = v[q + NB * r];
   }
-  __syncthreads();
+  xbarrier<SYNC>();
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = sm[smem_idx<L, SW, V>(t + P * e, l)];
-  __syncthreads();
+  xbarrier<SYNC>();
 }
 
-template <int N, int E, int L, int S, int STAGE, typename V>
+template <int N, int E, int L, int S, int SYNC, int STAGE, typename V>
 __device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, const V* __restrict__ stw, int t, int l) {
   constexpr int NSTAGE = num_stages(N, E);
   if constexpr (STAGE < NSTAGE) {
@@ -282,8 +294,8 @@ __device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, const V* __restrict
     constexpr int NS = stage_ns(N, E, STAGE);
     constexpr int SW = stage_log2(N, E, 0);
     stage_compute<N, E, R, NS, S>(v, t, stw + (STAGE >= 1 ? stage_tw_offset(N, E, STAGE) : 0));
-    if constexpr (STAGE + 1 < NSTAGE) stage_exchange<N, E, L, R, NS, SW>(v, sm, t, l);
-    fft_stages<N, E, L, S, STAGE + 1>(v, sm, stw, t, l);
+    if constexpr (STAGE + 1 < NSTAGE) stage_exchange<N, E, L, R, NS, SW, SYNC>(v, sm, t, l);
+    fft_stages<N, E, L, S, SYNC, STAGE + 1>(v, sm, stw, t, l);
   }
 }
 
@@ -291,9 +303,9 @@ __device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, const V* __restrict
 // line-l elements t + P*e (natural order).  `sm` must hold N*L elements and
 // be free (all threads past their last access) on entry; on exit it is free.
 // `stw` is the (N, E) stage-twiddle table (stage_tw_total(N, E) entries).
-template <int N, int E, int L, int S, typename V>
+template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V>
 __device__ __forceinline__ void line_fft(V (&v)[E], V* sm, const V* __restrict__ stw, int t, int l) {
-  fft_stages<N, E, L, S, 0>(v, sm, stw, t, l);
+  fft_stages<N, E, L, S, SYNC, 0>(v, sm, stw, t, l);
 }
 
 // Swizzle parameter callers must use when they stage data in `sm` in the

@@ -46,6 +46,8 @@ struct Pow2Args {
   int j0;        // global j of local j = 0 (x pass)
   void* specC;   // workspace C (x pass); == spec on one GPU
   int phases;    // kPhase* mask
+  int* ctrs;     // fused z+y passes: device counters (ni + 1 ints); nullptr = unfused kernels
+  int lag;       // fused schedule lag in planes
 };
 
 cudaError_t launch_pow2_f64(const Pow2Args& a);
@@ -58,6 +60,9 @@ struct KernelGeom {
 // g[0]: z kernels (M = n/2 point lines), g[1]: y kernels, g[2]: x kernel (n-point lines).
 bool pow2_config_f64(int n, KernelGeom* g);
 bool pow2_config_f32(int n, KernelGeom* g);
+// Whether the L2-fused z+y kernels exist for this n (they need 128-thread y tiles).
+bool pow2_fused_ok_f64(int n);
+bool pow2_fused_ok_f32(int n);
 
 // Generic mixed-radix path (any n >= 2).  One Stockham plan for an n-point line.
 constexpr int kGenMaxStages = 40;

@@ -38,6 +38,7 @@ arena_status cuda_fail(cudaError_t e, const char* what) {
 bool is_pow2(int n) { return n >= 2 && (n & (n - 1)) == 0; }
 
 const char* kPow2Names[kPow2Launches] = {"zfwd_r2c", "yfwd", "xmid_fwd_scale_inv", "yinv", "zinv_c2r"};
+const char* kFusedNames[3] = {"zy_fused_fwd", "xmid_fwd_scale_inv", "yz_fused_inv"};
 const char* kGenNames[kGenLaunches] = {"gen_z_r2c", "gen_y_fwd", "gen_x_fwd", "gen_scale",
                                        "gen_x_inv", "gen_y_inv", "gen_z_c2r"};
 
@@ -66,6 +67,8 @@ struct arena_fft_plan {
   void* stw = nullptr;  // stage-twiddle tables (power-of-two path)
   GenPlan gplan{};
   TmaCache* tma = nullptr;  // TMA descriptors (power-of-two path), nullptr = classic kernels
+  int* ctrs = nullptr;      // fused z+y schedule counters (n + 1 ints), nullptr = unfused
+  int lag = 2;
   int sm_count = 148;
   // host-boundary resources (lazily allocated)
   void* d_in = nullptr;
@@ -81,7 +84,7 @@ struct arena_fft_plan {
   int solves = 0;
   std::mutex ev_mu;
 
-  int launches() const { return path == ARENA_PATH_POW2 ? kPow2Launches : kGenLaunches; }
+  int launches() const { return path == ARENA_PATH_POW2 ? (ctrs ? 3 : kPow2Launches) : kGenLaunches; }
   size_t real_bytes() const { return size_t(n) * n * n * elem; }
 };
 
@@ -126,6 +129,7 @@ void free_plan(arena_fft_plan* p) {
   if (p->spec) cudaFree(p->spec);
   if (p->tw) cudaFree(p->tw);
   if (p->stw) cudaFree(p->stw);
+  if (p->ctrs) cudaFree(p->ctrs);
   if (p->d_in) cudaFree(p->d_in);
   if (p->d_out) cudaFree(p->d_out);
   if (p->d_work) cudaFree(p->d_work);
@@ -156,7 +160,7 @@ arena_status enqueue_solve(arena_fft_plan* p, const void* d_f, void* d_u, cudaSt
   cudaEvent_t* ev = timing_events(p);
   if (p->path == ARENA_PATH_POW2) {
     Pow2Args a{d_f, d_u, p->spec, p->tw, p->stw, p->n, p->nc, p->ncp, s, ev, p->tma, p->sm_count,
-               /*ni*/ p->n, /*nj*/ p->n, /*nchunks*/ 1, /*j0*/ 0, /*specC*/ p->spec, kPhaseAll};
+               /*ni*/ p->n, /*nj*/ p->n, /*nchunks*/ 1, /*j0*/ 0, /*specC*/ p->spec, kPhaseAll, p->ctrs, p->lag};
     e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
   } else {
     GenArgs a{&p->gplan, p->tw, p->n, p->nc, p->ncp, s, ev};
@@ -221,6 +225,15 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
     p->path = ARENA_PATH_POW2;
     const char* kern = std::getenv("ARENA_FFT_KERNELS");  // "classic" selects the non-TMA strided kernels
     if (!(kern && std::string(kern) == "classic")) p->tma = new (std::nothrow) TmaCache;
+    const char* fz = std::getenv("ARENA_FFT_FUSED");  // "0" disables the L2-fused z+y kernels
+    const bool fused_ok = precision_bits == 64 ? pow2_fused_ok_f64(n) : pow2_fused_ok_f32(n);
+    if (p->tma && fused_ok && !(fz && std::string(fz) == "0")) {
+      if ((e = cudaMalloc(&p->ctrs, sizeof(int) * size_t(n + 1))) != cudaSuccess) {
+        free_plan(p);
+        return fail(ARENA_ENOMEM, "fused schedule counters");
+      }
+    }
+    if (const char* lg = std::getenv("ARENA_FFT_FUSED_LAG")) p->lag = std::atoi(lg);
   } else {
     p->path = ARENA_PATH_GENERIC;
     if (!gen_plan_make(n, &p->gplan)) {
@@ -403,7 +416,7 @@ arena_status arena_fft_stage_times(arena_fft_plan* p, double* ms, const char** n
     ++p->solves;
   }
   p->ev_sets_used = 0;
-  const char** nm = p->path == ARENA_PATH_POW2 ? kPow2Names : kGenNames;
+  const char** nm = p->path == ARENA_PATH_POW2 ? (p->ctrs ? kFusedNames : kPow2Names) : kGenNames;
   for (int k = 0; k < L && k < max_stages; ++k) {
     if (ms) ms[k] = p->stage_ms[k];
     if (names) names[k] = nm[k];
@@ -479,6 +492,7 @@ arena_status nccl_fail(ncclResult_t r, const char* what) {
 struct SlabRank {
   void* B = nullptr;  // workspace B: ni * n rows
   void* C = nullptr;  // workspace C: n * nj rows
+  int* ctrs = nullptr;  // fused z+y counters (ni + 1), nullptr = unfused
   TmaCache tma;
 };
 
@@ -503,6 +517,7 @@ void free_slab(arena_fft_slab* s) {
     for (SlabRank& r : s->ranks) {
       if (r.B) cudaFree(r.B);
       if (r.C) cudaFree(r.C);
+      if (r.ctrs) cudaFree(r.ctrs);
     }
     if (s->comm) {
       if (NcclApi* a = nccl_api()) a->CommDestroy(s->comm);
@@ -547,6 +562,10 @@ arena_status slab_init(arena_fft_slab** out, int n, int prec, int device, int P,
       free_slab(s);
       return fail(ARENA_ENOMEM, "slab workspaces: " + std::string(cudaGetErrorString(e)));
     }
+    if (s->base->ctrs && (e = cudaMalloc(&r.ctrs, sizeof(int) * size_t(s->ni + 1))) != cudaSuccess) {
+      free_slab(s);
+      return fail(ARENA_ENOMEM, "slab counters");
+    }
   }
   if (!loopback) {
     NcclApi* a = nccl_api();
@@ -570,7 +589,7 @@ arena_status slab_init(arena_fft_slab** out, int n, int prec, int device, int P,
 Pow2Args slab_args(arena_fft_slab* s, SlabRank& r, int rank, const void* f, void* u, cudaStream_t st, int phases) {
   arena_fft_plan* p = s->base;
   return Pow2Args{f, u, r.B, p->tw, p->stw, p->n, p->nc, p->ncp, st, nullptr, &r.tma, p->sm_count,
-                  s->ni, s->nj, s->P, rank * s->nj, r.C, phases};
+                  s->ni, s->nj, s->P, rank * s->nj, r.C, phases, r.ctrs, p->lag};
 }
 
 cudaError_t slab_phase(arena_fft_slab* s, SlabRank& r, int rank, const void* f, void* u, cudaStream_t st, int phases) {

@@ -146,26 +146,26 @@ __device__ __forceinline__ V* smem_base() {
 // Rows of NR reals: z[m] = f[2m] + i f[2m+1] (one vector load), M-point FFT,
 // then X[k] = 1/2 (A + B) - 1/2 i W_n^k (A - B), A = Z[k], B = conj(Z[M-k]),
 // for k in [0, M]; X[M] = Re Z0 - Im Z0.
-template <typename T, int NR>
-__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
-    k_zfwd(const T* __restrict__ f, vec2_t<T>* __restrict__ S, const vec2_t<T>* __restrict__ tw,
-           const vec2_t<T>* __restrict__ stw, Layout g) {
+// One group of L*P threads (index gt) transforms slab rows row0 .. row0+L-1
+// (row = il*n + j) using `sm` ((M+1)*L elements); SYNC is the group barrier.
+template <typename T, int NR, int E, int L, int SYNC>
+__device__ __forceinline__ void zfwd_rows(const T* __restrict__ f, vec2_t<T>* __restrict__ S,
+                                          const vec2_t<T>* __restrict__ tw, const vec2_t<T>* __restrict__ stw,
+                                          const Layout& g, size_t row0, vec2_t<T>* sm, int gt) {
   using V = vec2_t<T>;
-  using C = ContigCfg<T, NR>;
-  constexpr int M = C::M, E = C::E, P = C::P, L = C::L;
+  constexpr int M = NR / 2, P = M / E;
   constexpr int ncp = spec_pitch(NR);
   constexpr int SW = engine_swizzle<M, E>();
-  V* sm = smem_base<V>();
-  const int l = threadIdx.x % L, t = threadIdx.x / L;
-  const size_t row = size_t(blockIdx.x) * L + l;
+  const int l = gt % L, t = gt / L;
+  const size_t row = row0 + l;
   const V* src = reinterpret_cast<const V*>(f + row * NR);
   V v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = __ldcs(src + t + P * e);
-  line_fft<M, E, L, -1>(v, sm, stw, t, l);
+  line_fft<M, E, L, -1, SYNC>(v, sm, stw, t, l);
 #pragma unroll
   for (int e = 0; e < E; ++e) sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
-  __syncthreads();
+  xbarrier<SYNC>();
   V* dst = S + rowB(g, int(row / NR), int(row % NR)) * ncp;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -180,32 +180,50 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
   }
 }
 
+template <typename T, int NR>
+__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
+    k_zfwd(const T* __restrict__ f, vec2_t<T>* __restrict__ S, const vec2_t<T>* __restrict__ tw,
+           const vec2_t<T>* __restrict__ stw, Layout g) {
+  using C = ContigCfg<T, NR>;
+  zfwd_rows<T, NR, C::E, C::L, kSyncCta>(f, S, tw, stw, g, size_t(blockIdx.x) * C::L, smem_base<vec2_t<T>>(),
+                                         threadIdx.x);
+}
+
+// Evict-without-writeback (PTX discard.global.L2) of one 128-byte line.
+__device__ __forceinline__ void l2_discard(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 // ------------------------------------------------------------------- K5 zinv
 // Inverse of K1 with FFTW c2r semantics (imaginary parts of X[0] and X[M]
 // ignored): Z[k] = (A + B) + i (A - B) conj(W_n^k), A = X[k], B = conj(X[M-k]),
-// M-point backward FFT, u[2m] = Re z[m], u[2m+1] = Im z[m].
-template <typename T, int NR>
-__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
-    k_zinv(const vec2_t<T>* __restrict__ S, T* __restrict__ u, const vec2_t<T>* __restrict__ tw,
-           const vec2_t<T>* __restrict__ stw, Layout g) {
+// M-point backward FFT, u[2m] = Re z[m], u[2m+1] = Im z[m].  DISCARD drops the
+// consumed half-spectrum rows from L2 without writing them back (fused path:
+// they were produced in L2 by the y pass and are dead after this read).
+template <typename T, int NR, int E, int L, int SYNC, bool DISCARD>
+__device__ __forceinline__ void zinv_rows(const vec2_t<T>* __restrict__ S, T* __restrict__ u,
+                                          const vec2_t<T>* __restrict__ tw, const vec2_t<T>* __restrict__ stw,
+                                          const Layout& g, size_t row0, vec2_t<T>* sm, int gt) {
   using V = vec2_t<T>;
-  using C = ContigCfg<T, NR>;
-  constexpr int M = C::M, E = C::E, P = C::P, L = C::L;
+  constexpr int M = NR / 2, P = M / E;
   constexpr int ncp = spec_pitch(NR);
   constexpr int SW = engine_swizzle<M, E>();
-  V* sm = smem_base<V>();
   V* xm = sm + M * L;  // X[M] per line
-  const int l = threadIdx.x % L, t = threadIdx.x / L;
-  const size_t row = size_t(blockIdx.x) * L + l;
+  const int l = gt % L, t = gt / L;
+  const size_t row = row0 + l;
   const V* src = S + rowB(g, int(row / NR), int(row % NR)) * ncp;
   V v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    v[e] = __ldcs(src + t + P * e);
+    v[e] = DISCARD ? __ldcg(src + t + P * e) : __ldcs(src + t + P * e);
     sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
   }
-  if (t == 0) xm[l] = __ldcs(src + M);
-  __syncthreads();
+  if (t == 0) xm[l] = DISCARD ? __ldcg(src + M) : __ldcs(src + M);
+  xbarrier<SYNC>();
+  if constexpr (DISCARD) {
+    constexpr int LINES = ncp * int(sizeof(V)) / 128;
+    for (int q = t; q < LINES; q += P) l2_discard(reinterpret_cast<const char*>(src) + size_t(q) * 128);
+  }
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int k = t + P * e;
@@ -221,11 +239,20 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
     const V Op = cmulc(csub(A, B), W);
     v[e] = V{Ep.x - Op.y, Ep.y + Op.x};
   }
-  __syncthreads();
-  line_fft<M, E, L, +1>(v, sm, stw, t, l);
+  xbarrier<SYNC>();
+  line_fft<M, E, L, +1, SYNC>(v, sm, stw, t, l);
   V* dst = reinterpret_cast<V*>(u + row * NR);
 #pragma unroll
   for (int e = 0; e < E; ++e) __stcs(dst + t + P * e, v[e]);
+}
+
+template <typename T, int NR>
+__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
+    k_zinv(const vec2_t<T>* __restrict__ S, T* __restrict__ u, const vec2_t<T>* __restrict__ tw,
+           const vec2_t<T>* __restrict__ stw, Layout g) {
+  using C = ContigCfg<T, NR>;
+  zinv_rows<T, NR, C::E, C::L, kSyncCta, false>(S, u, tw, stw, g, size_t(blockIdx.x) * C::L, smem_base<vec2_t<T>>(),
+                                                threadIdx.x);
 }
 
 // --------------------------------------------------------------- K2/K4 ypass
@@ -318,6 +345,9 @@ namespace arena_fft {
 #ifndef ARENA_TMA_NBUF
 #define ARENA_TMA_NBUF 1  // tile buffers per CTA (prefetch distance NBUF-1)
 #endif
+#ifndef ARENA_TMA_L2PF
+#define ARENA_TMA_L2PF 0  // also prefetch the tile this many iterations ahead into L2 (0: off)
+#endif
 
 template <typename T, int N>
 struct TmaCfg {
@@ -378,9 +408,24 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
           tma_load_5d(dst + (size_t(c) * g.ni + q) * L, &tmap, b, 2 * kt * L, outer & jb, q, outer >> g.jbs, c);
     }
   };
+  auto prefetch = [&](int gt) {  // same boxes, into L2 only
+    const int outer = gt / KT, kt = gt % KT;
+    if constexpr (PASS < 2) {
+      tma_prefetch_5d(&tmap, 2 * kt * L, 0, outer, 0, 0);
+    } else {
+      const int IB = tma_ib(g.ni);
+      const int jb = (1 << g.jbs) - 1;
+      for (int c = 0; c < nchunks; ++c)
+        for (int q = 0; q < g.ni; q += IB) tma_prefetch_5d(&tmap, 2 * kt * L, outer & jb, q, outer >> g.jbs, c);
+    }
+  };
 
-  // Prologue: tiles 0 .. NBUF-2 of this CTA in flight.
+  // Prologue: tiles 0 .. NBUF-2 of this CTA in flight (and the next ones queued in L2).
   if (tid == 0) {
+    for (int p = 1; p < ARENA_TMA_L2PF; ++p) {
+      const int gp = blockIdx.x + p * gridDim.x;
+      if (gp < NT) prefetch(gp);
+    }
 #pragma unroll
     for (int p = 0; p < NBUF - 1; ++p) {
       const int gp = blockIdx.x + p * gridDim.x;
@@ -391,6 +436,10 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
   for (int it = 0; gt < NT; ++it, gt += gridDim.x) {
     const int b = it % NBUF;
     V* cur = bufs + b * TILE;
+    if constexpr (ARENA_TMA_L2PF > 0) {
+      const int gp = gt + ARENA_TMA_L2PF * gridDim.x;
+      if (tid == 0 && gp < NT) prefetch(gp);
+    }
     if constexpr (NBUF == 1) {  // no intra-CTA prefetch: co-resident CTAs overlap instead
       if (tid == 0) {
         fence_proxy_async_smem();

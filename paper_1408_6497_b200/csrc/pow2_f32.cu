@@ -4,4 +4,13 @@
 namespace arena_fft {
 cudaError_t launch_pow2_f32(const Pow2Args& a) { return launch_pow2<float>(a); }
 bool pow2_config_f32(int n, KernelGeom* g) { return pow2_config<float>(n, g); }
+bool pow2_fused_ok_f32(int n) {
+  switch (n) {
+    case 256: return FusedCfg<float, 256>::OK;
+    case 512: return FusedCfg<float, 512>::OK;
+    case 1024: return FusedCfg<float, 1024>::OK;
+    case 2048: return FusedCfg<float, 2048>::OK;
+    default: return false;
+  }
+}
 }  // namespace arena_fft

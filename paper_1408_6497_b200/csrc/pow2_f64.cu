@@ -4,4 +4,13 @@
 namespace arena_fft {
 cudaError_t launch_pow2_f64(const Pow2Args& a) { return launch_pow2<double>(a); }
 bool pow2_config_f64(int n, KernelGeom* g) { return pow2_config<double>(n, g); }
+bool pow2_fused_ok_f64(int n) {
+  switch (n) {
+    case 256: return FusedCfg<double, 256>::OK;
+    case 512: return FusedCfg<double, 512>::OK;
+    case 1024: return FusedCfg<double, 1024>::OK;
+    case 2048: return FusedCfg<double, 2048>::OK;
+    default: return false;
+  }
+}
 }  // namespace arena_fft

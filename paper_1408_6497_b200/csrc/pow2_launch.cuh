@@ -8,7 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include "launchers.h"
-#include "poisson_pow2.cuh"
+#include "poisson_fused.cuh"
 
 namespace arena_fft {
 
@@ -102,6 +102,27 @@ cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* 
   return cudaGetLastError();
 }
 
+template <typename T, int N, int DIR>
+cudaError_t launch_fused(const Pow2Args& a, const CUtensorMap& map, const Layout& g) {
+  using F = FusedCfg<T, N>;
+  using V = vec2_t<T>;
+  auto kern = k_zy_fused<T, N, DIR>;
+  cudaError_t e = ensure_smem<k_zy_fused<T, N, DIR>>(F::SMEM, F::THREADS);
+  if (e) return e;
+  if ((e = cudaMemsetAsync(a.ctrs, 0, sizeof(int) * size_t(g.ni + 1), a.stream))) return e;
+  int per_sm = 1;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, F::THREADS, F::SMEM))) return e;
+  const long long items = (long long)g.ni * (N / F::ZROWS + TmaCfg<T, N>::KT);
+  long long grid = (long long)a.sm_count * (per_sm > 0 ? per_sm : 1);
+  if (grid > items) grid = items;
+  const V* stw_z = static_cast<const V*>(a.stw) + stw_offset(a.n, 0, F::EZ);
+  const V* stw_y = static_cast<const V*>(a.stw) + stw_offset(a.n, 1, TmaCfg<T, N>::E);
+  kern<<<unsigned(grid), F::THREADS, F::SMEM, a.stream>>>(map, static_cast<const T*>(a.f), static_cast<T*>(a.u),
+                                                          static_cast<V*>(a.spec), static_cast<const V*>(a.tw),
+                                                          stw_z, stw_y, g, a.ctrs, a.lag);
+  return cudaGetLastError();
+}
+
 inline void mark(const Pow2Args& a, int i) {
   if (a.ev) cudaEventRecord(a.ev[i], a.stream);
 }
@@ -144,7 +165,13 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   const CUtensorMap* my = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[0]) : nullptr;
   const CUtensorMap* mx = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[1]) : nullptr;
   int mk = 0;
-  if (a.phases & kPhaseZY) {
+  const bool fused = tma && a.ctrs != nullptr && FusedCfg<T, NR>::OK;
+  if (fused && (a.phases & kPhaseZY)) {
+    mark(a, mk++);
+    if constexpr (FusedCfg<T, NR>::OK) {
+      if ((e = launch_fused<T, NR, -1>(a, *my, gB))) return e;
+    }
+  } else if (a.phases & kPhaseZY) {
     mark(a, mk++);
     k_zfwd<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw,
                                                                stw_ptr<T>(a, 0, CC::E), gB);
@@ -167,7 +194,13 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
           S, stw_ptr<T>(a, 1, XC::E), scale, four_pi2, gC);
     }
   }
-  if (a.phases & kPhaseYZ) {
+  if (fused && (a.phases & kPhaseYZ)) {
+    mark(a, mk++);
+    if constexpr (FusedCfg<T, NR>::OK) {
+      if ((e = launch_fused<T, NR, +1>(a, *my, gB))) return e;
+    }
+    mark(a, mk++);
+  } else if (a.phases & kPhaseYZ) {
     mark(a, mk++);
     if (tma) {
       if ((e = launch_strided_tma<T, NR, 1>(a, *my, a.spec, gB, scale, four_pi2))) return e;

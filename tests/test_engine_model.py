@@ -78,3 +78,39 @@ def test_blocked_row_layout_is_a_bijection(n):
     rows = ((j // jb) * n + i) * jb + (j % jb)
     assert np.array_equal(np.sort(rows.ravel()), np.arange(n * n))
     assert rows.max() * ncp + ncp <= n * n * ncp
+
+
+def _fused_decode(w, planes, c1, c2, lag):
+    """Mirror of poisson_fused.cuh fused_decode."""
+    A = lag * c1
+    if w < A:
+        return 1, w // c1, w % c1
+    w -= A
+    mid = (planes - lag) * (c1 + c2)
+    if w < mid:
+        r, s = lag + w // (c1 + c2), w % (c1 + c2)
+        return (1, r, s) if s < c1 else (0, r - lag, s - c1)
+    w -= mid
+    return 0, planes - lag + w // c2, w % c2
+
+
+@pytest.mark.parametrize("planes,c1,c2,lag", [(1024, 128, 129, 2), (1024, 129, 128, 2), (128, 128, 129, 4),
+                                               (4, 3, 5, 4), (16, 7, 2, 1)])
+def test_fused_schedule_is_a_deadlock_free_permutation(planes, c1, c2, lag):
+    """Every (pass, plane, item) is dispatched exactly once, and every second-pass
+    item of plane p comes after all first-pass items of plane p, so in-order
+    dispatch never waits on an item that has not been handed out."""
+    total = planes * (c1 + c2)
+    seen = set()
+    last_first = {}
+    for w in range(total):
+        first, p, s = _fused_decode(w, planes, c1, c2, lag)
+        assert 0 <= p < planes and 0 <= s < (c1 if first else c2)
+        key = (first, p, s)
+        assert key not in seen
+        seen.add(key)
+        if first:
+            last_first[p] = w
+        else:
+            assert last_first.get(p, -1) >= 0 and p in last_first
+    assert len(seen) == total

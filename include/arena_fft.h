@@ -68,6 +68,11 @@ arena_status arena_poisson_solve_device(arena_fft_plan* plan, const void* d_f, v
  * inside.  Synchronous.  This is what arena::poisson_spectral_solve calls. */
 arena_status arena_poisson_solve_host(arena_fft_plan* plan, const void* f, void* u);
 
+/* Batched drop-in path: `count` independent fields f[s] -> u[s] (host buffers;
+ * pinned for full PCIe speed).  The copy-in of field s+1 and copy-out of field
+ * s-1 overlap the solve of field s on separate streams.  Synchronous. */
+arena_status arena_poisson_solve_host_batch(arena_fft_plan* plan, int count, const void* const* f, void* const* u);
+
 /* arena::dft3_forward (fft_solver.cpp:13-29): real n^3 -> full complex n^3
  * spectrum (interleaved), unnormalised, sign -1.  Host and device variants. */
 arena_status arena_dft3_forward_host(arena_fft_plan* plan, const void* g, void* spec);

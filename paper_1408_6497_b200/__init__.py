@@ -52,6 +52,7 @@ _sig = {
                                   ctypes.POINTER(_i), ctypes.POINTER(ctypes.c_size_t)]),
     "arena_poisson_solve_device": (_i, [_vp, _vp, _vp, _vp]),
     "arena_poisson_solve_host": (_i, [_vp, _vp, _vp]),
+    "arena_poisson_solve_host_batch": (_i, [_vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
     "arena_dft3_forward_host": (_i, [_vp, _vp, _vp]),
     "arena_dft3_forward_device": (_i, [_vp, _vp, _vp, _vp]),
     "arena_dft3_inverse_host": (_i, [_vp, _vp, _vp]),
@@ -161,6 +162,14 @@ class Plan:
     # ---- host boundary (the drop-in path)
     def solve_host(self, f, u) -> None:
         _check(lib.arena_poisson_solve_host(self._p, _vp(_ptr(f)), _vp(_ptr(u))), "arena_poisson_solve_host")
+
+    def solve_host_batch(self, fs, us) -> None:
+        """Solve fields fs[s] -> us[s] (host arrays / pinned tensors) with copy/compute overlap."""
+        if len(fs) != len(us):
+            raise ValueError("fs and us must have the same length")
+        fa = (_vp * len(fs))(*[_ptr(x) for x in fs])
+        ua = (_vp * len(us))(*[_ptr(x) for x in us])
+        _check(lib.arena_poisson_solve_host_batch(self._p, len(fs), fa, ua), "arena_poisson_solve_host_batch")
 
     def dft3_forward_host(self, g: np.ndarray) -> np.ndarray:
         out = np.empty(g.shape, dtype=np.complex128 if self.precision == 64 else np.complex64)

@@ -76,6 +76,10 @@ struct arena_fft_plan {
   void* d_work = nullptr;  // n^3 complex, dft3 only
   cudaStream_t hstream = nullptr;
   std::mutex host_mu;  // one host-path call in flight per plan
+  // batched host path: double-buffered device fields, copy-in / copy-out streams
+  void* bin[2] = {nullptr, nullptr};
+  void* bout[2] = {nullptr, nullptr};
+  cudaStream_t s_in = nullptr, s_out = nullptr;
   // stage timing
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -134,6 +138,12 @@ void free_plan(arena_fft_plan* p) {
   if (p->d_out) cudaFree(p->d_out);
   if (p->d_work) cudaFree(p->d_work);
   if (p->hstream) cudaStreamDestroy(p->hstream);
+  for (int b = 0; b < 2; ++b) {
+    if (p->bin[b]) cudaFree(p->bin[b]);
+    if (p->bout[b]) cudaFree(p->bout[b]);
+  }
+  if (p->s_in) cudaStreamDestroy(p->s_in);
+  if (p->s_out) cudaStreamDestroy(p->s_out);
   delete p->tma;
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   delete p;
@@ -319,6 +329,70 @@ arena_status arena_poisson_solve_host(arena_fft_plan* p, const void* f, void* u)
     return cuda_fail(e, "D2H u");
   if ((e = cudaStreamSynchronize(p->hstream)) != cudaSuccess) return cuda_fail(e, "poisson solve");
   return ARENA_OK;
+}
+
+// Batched host solves: field s+1 is copied in and field s-1 copied out while
+// field s is solved (PCIe is full duplex), so a stream of solves runs at
+// max(H2D, D2H, solve) per field instead of their sum.
+arena_status arena_poisson_solve_host_batch(arena_fft_plan* p, int count, const void* const* f, void* const* u) {
+  if (!p || count < 0 || (count && (!f || !u))) return fail(ARENA_EINVAL, "NULL plan or buffer list");
+  DeviceGuard g(p->device);
+  std::lock_guard<std::mutex> lk(p->host_mu);
+  arena_status st = ensure_host_buffers(p, false);
+  if (st != ARENA_OK) return st;
+  cudaError_t e;
+  const size_t bytes = p->real_bytes();
+  for (int b = 0; b < 2; ++b) {
+    if (!p->bin[b] && (e = cudaMalloc(&p->bin[b], bytes)) != cudaSuccess) return fail(ARENA_ENOMEM, "batch input buffer");
+    if (!p->bout[b] && (e = cudaMalloc(&p->bout[b], bytes)) != cudaSuccess) return fail(ARENA_ENOMEM, "batch output buffer");
+  }
+  if (!p->s_in && (e = cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking))) return cuda_fail(e, "stream");
+  if (!p->s_out && (e = cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking))) return cuda_fail(e, "stream");
+  std::vector<cudaEvent_t> ev;
+  auto mkev = [&]() {
+    cudaEvent_t x;
+    if (cudaEventCreateWithFlags(&x, cudaEventDisableTiming) != cudaSuccess) return (cudaEvent_t) nullptr;
+    ev.push_back(x);
+    return x;
+  };
+  std::vector<cudaEvent_t> in_done(count), solved(count), out_done(count);
+  for (int s = 0; s < count; ++s) {
+    in_done[s] = mkev();
+    solved[s] = mkev();
+    out_done[s] = mkev();
+    if (!in_done[s] || !solved[s] || !out_done[s]) {
+      for (cudaEvent_t x : ev) cudaEventDestroy(x);
+      return fail(ARENA_ECUDA, "cudaEventCreate");
+    }
+  }
+  st = ARENA_OK;
+  for (int s = 0; s < count && st == ARENA_OK; ++s) {
+    const int b = s & 1;
+    // copy-in of field s into bin[b] once solve s-2 (the buffer's last reader) is done
+    if (s >= 2) cudaStreamWaitEvent(p->s_in, solved[s - 2], 0);
+    if ((e = cudaMemcpyAsync(p->bin[b], f[s], bytes, cudaMemcpyHostToDevice, p->s_in))) {
+      st = cuda_fail(e, "batch H2D");
+      break;
+    }
+    cudaEventRecord(in_done[s], p->s_in);
+    // solve s once its input arrived and copy-out s-2 (last reader of bout[b]) finished
+    cudaStreamWaitEvent(p->hstream, in_done[s], 0);
+    if (s >= 2) cudaStreamWaitEvent(p->hstream, out_done[s - 2], 0);
+    if ((st = enqueue_solve(p, p->bin[b], p->bout[b], p->hstream)) != ARENA_OK) break;
+    cudaEventRecord(solved[s], p->hstream);
+    // copy-out of field s
+    cudaStreamWaitEvent(p->s_out, solved[s], 0);
+    if ((e = cudaMemcpyAsync(u[s], p->bout[b], bytes, cudaMemcpyDeviceToHost, p->s_out))) {
+      st = cuda_fail(e, "batch D2H");
+      break;
+    }
+    cudaEventRecord(out_done[s], p->s_out);
+  }
+  if ((e = cudaStreamSynchronize(p->s_out)) != cudaSuccess && st == ARENA_OK) st = cuda_fail(e, "batch solve");
+  cudaStreamSynchronize(p->hstream);
+  cudaStreamSynchronize(p->s_in);
+  for (cudaEvent_t x : ev) cudaEventDestroy(x);
+  return st;
 }
 
 static arena_status dft3_fwd_enqueue(arena_fft_plan* p, const void* d_g, void* d_spec, cudaStream_t s) {

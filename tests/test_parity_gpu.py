@@ -214,3 +214,15 @@ def test_slab_nccl_single_rank(cuda):
     s.solve_device(f, u)
     torch.cuda.synchronize()
     assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64
+
+
+def test_batched_host_solves(cuda):
+    """arena_poisson_solve_host_batch (copy/compute overlap) == independent solves."""
+    torch = cuda
+    n = 64
+    p = arena.Plan(n)
+    fs = [torch.from_numpy(np.random.default_rng(s).uniform(-1, 1, (n, n, n))).pin_memory() for s in range(5)]
+    us = [torch.empty_like(x).pin_memory() for x in fs]
+    p.solve_host_batch(fs, us)
+    for f, u in zip(fs, us):
+        assert _rel(u.numpy(), oracle.poisson_solve(f.numpy())) <= TOL64

@@ -129,6 +129,14 @@ arena_status arena_slab_info(const arena_fft_slab* slab, int* ni, int* nj, size_
 /* d_f, d_u: this rank's slab (loopback: the full field); asynchronous on stream. */
 arena_status arena_slab_solve_device(arena_fft_slab* slab, const void* d_f, void* d_u, void* stream);
 
+/* Batch evaluation of arena::SpectralInterpolant (fft_solver.cpp:89-114) on the
+ * GPU: out[p] = sum_m Re(amp_m exp(2 pi i k_m . x_p)).  k: 3*nmodes ints (signed
+ * frequencies), amp: 2*nmodes doubles (re, im — already divided by n^3 as in
+ * SpectralInterpolant::build), pts: 3*npts doubles, out: npts doubles; all host
+ * arrays.  device < 0: current device.  Synchronous. */
+arena_status arena_interpolant_eval(int device, int nmodes, const int* k, const double* amp, int npts,
+                                    const double* pts, double* out);
+
 /* Tile geometry of the power-of-two kernels for (n, precision): out15[0..4] =
  * {line length, points/thread, lines/CTA, threads/CTA, shared bytes} of the
  * contiguous-axis (z) kernels, out15[5..9] the y kernels, out15[10..14] the x

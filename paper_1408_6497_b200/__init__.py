@@ -76,6 +76,7 @@ _sig = {
                              ctypes.POINTER(ctypes.c_size_t)]),
     "arena_slab_solve_device": (_i, [_vp, _vp, _vp, _vp]),
     "arena_pow2_kernel_geometry": (_i, [_i, _i, ctypes.POINTER(_i)]),
+    "arena_interpolant_eval": (_i, [_i, _i, _vp, _vp, _i, _vp, _vp]),
     "arena_last_error": (ctypes.c_char_p, []),
     "arena_fft_abi_version": (_i, []),
 }
@@ -302,6 +303,35 @@ def dft3_inverse(spec: np.ndarray, n: int) -> np.ndarray:
         return p.dft3_inverse_host(spec.reshape(n, n, n))
 
 
+class SpectralInterpolant:
+    """Mirror of arena::SpectralInterpolant (fft_solver.hpp:27-36, fft_solver.cpp:89-114):
+    modes of the full spectrum above rel_cut * max|mode| (spectrum from the GPU
+    dft3_forward); evaluation of many points at once on the GPU."""
+
+    def __init__(self, k: np.ndarray, amp: np.ndarray):
+        self.k = np.ascontiguousarray(k, dtype=np.int32).reshape(-1, 3)
+        self.amp = np.ascontiguousarray(amp, dtype=np.complex128).ravel()
+
+    @classmethod
+    def build(cls, g: np.ndarray, rel_cut: float = 1e-14) -> "SpectralInterpolant":
+        spec = dft3_forward(g)
+        n = g.shape[0]
+        mag = np.abs(spec)
+        keep = np.nonzero(mag > rel_cut * mag.max())
+        sf = np.where(np.arange(n) <= n // 2, np.arange(n), np.arange(n) - n)
+        k = np.stack([sf[keep[0]], sf[keep[1]], sf[keep[2]]], axis=1)
+        return cls(k, spec[keep] / float(n) ** 3)
+
+    def __call__(self, pts, device: int = -1) -> np.ndarray:
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        out = np.empty(pts.shape[0], dtype=np.float64)
+        a = np.ascontiguousarray(np.stack([self.amp.real, self.amp.imag], axis=-1))
+        _check(lib.arena_interpolant_eval(int(device), self.k.shape[0], _vp(self.k.ctypes.data), _vp(a.ctypes.data),
+                                          pts.shape[0], _vp(pts.ctypes.data), _vp(out.ctypes.data)),
+               "arena_interpolant_eval")
+        return out
+
+
 def source_modes(n: int, kvec: np.ndarray, coef: np.ndarray, out, precision: int = 64, stream: int = 0,
                  i0: int = 0, ni: Optional[int] = None) -> None:
     """Device buffer `out` = sum_m Re(coef_m e^{2 pi i k_m.x}) on planes i0..i0+ni-1 (default: all n^3).
@@ -323,7 +353,7 @@ def source_gaussian(n: int, alpha: float, center, which: int, out, precision: in
 
 
 __all__ = [
-    "Plan", "Slab", "nccl_unique_id", "get_plan", "poisson_spectral_solve", "dft3_forward", "dft3_inverse", "signed_freq",
+    "Plan", "Slab", "SpectralInterpolant", "nccl_unique_id", "get_plan", "poisson_spectral_solve", "dft3_forward", "dft3_inverse", "signed_freq",
     "source_modes", "source_gaussian", "ArenaError", "lib", "LIB_PATH", "CORE_PATH", "HEADER_PATH",
     "PATH_POW2", "PATH_GENERIC",
 ]

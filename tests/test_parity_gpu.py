@@ -226,3 +226,18 @@ def test_batched_host_solves(cuda):
     p.solve_host_batch(fs, us)
     for f, u in zip(fs, us):
         assert _rel(u.numpy(), oracle.poisson_solve(f.numpy())) <= TOL64
+
+
+def test_spectral_interpolant_off_grid(cuda):
+    """T11 (test_fft.cpp:155-166) through the GPU path: interpolant of the
+    oscillatory k=2 solution at n=16, evaluated at random points (rel 1e-11),
+    plus a 10^4-point batch against the analytic u."""
+    n = 16
+    x = np.arange(n) / n
+    w = 2 * np.pi * 2
+    u = np.sin(w * x)[:, None, None] * np.sin(w * x)[None, :, None] * np.sin(w * x)[None, None, :]
+    si = arena.SpectralInterpolant.build(u)
+    pts = np.random.default_rng(8).uniform(0, 1, (10000, 3))
+    got = si(pts)
+    want = np.sin(w * pts[:, 0]) * np.sin(w * pts[:, 1]) * np.sin(w * pts[:, 2])
+    assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max() + 1e-13

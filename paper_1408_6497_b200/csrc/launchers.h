@@ -48,7 +48,9 @@ struct Pow2Args {
   int phases;    // kPhase* mask
   int* ctrs;     // fused z+y passes: device counters (ni + 1 ints); nullptr = unfused kernels
   int lag;       // fused schedule lag in planes
+  int fuse;      // kFuseFwd | kFuseInv: which z+y pairs run fused (needs ctrs)
 };
+enum : int { kFuseFwd = 1, kFuseInv = 2 };
 
 cudaError_t launch_pow2_f64(const Pow2Args& a);
 cudaError_t launch_pow2_f32(const Pow2Args& a);

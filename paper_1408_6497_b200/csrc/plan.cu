@@ -37,8 +37,12 @@ arena_status cuda_fail(cudaError_t e, const char* what) {
 
 bool is_pow2(int n) { return n >= 2 && (n & (n - 1)) == 0; }
 
-const char* kPow2Names[kPow2Launches] = {"zfwd_r2c", "yfwd", "xmid_fwd_scale_inv", "yinv", "zinv_c2r"};
-const char* kFusedNames[3] = {"zy_fused_fwd", "xmid_fwd_scale_inv", "yz_fused_inv"};
+// stage names by fused mask (0: none, 1: forward pair fused, 2: inverse pair, 3: both)
+const char* kStageNames[4][kPow2Launches] = {
+    {"zfwd_r2c", "yfwd", "xmid_fwd_scale_inv", "yinv", "zinv_c2r"},
+    {"zy_fused_fwd", "xmid_fwd_scale_inv", "yinv", "zinv_c2r", nullptr},
+    {"zfwd_r2c", "yfwd", "xmid_fwd_scale_inv", "yz_fused_inv", nullptr},
+    {"zy_fused_fwd", "xmid_fwd_scale_inv", "yz_fused_inv", nullptr, nullptr}};
 const char* kGenNames[kGenLaunches] = {"gen_z_r2c", "gen_y_fwd", "gen_x_fwd", "gen_scale",
                                        "gen_x_inv", "gen_y_inv", "gen_z_c2r"};
 
@@ -69,6 +73,7 @@ struct arena_fft_plan {
   TmaCache* tma = nullptr;  // TMA descriptors (power-of-two path), nullptr = classic kernels
   int* ctrs = nullptr;      // fused z+y schedule counters (n + 1 ints), nullptr = unfused
   int lag = 2;
+  int fuse = 0;             // kFuseFwd | kFuseInv
   int sm_count = 148;
   // host-boundary resources (lazily allocated)
   void* d_in = nullptr;
@@ -88,7 +93,10 @@ struct arena_fft_plan {
   int solves = 0;
   std::mutex ev_mu;
 
-  int launches() const { return path == ARENA_PATH_POW2 ? (ctrs ? 3 : kPow2Launches) : kGenLaunches; }
+  int launches() const {
+    if (path != ARENA_PATH_POW2) return kGenLaunches;
+    return kPow2Launches - ((ctrs && (fuse & kFuseFwd)) ? 1 : 0) - ((ctrs && (fuse & kFuseInv)) ? 1 : 0);
+  }
   size_t real_bytes() const { return size_t(n) * n * n * elem; }
 };
 
@@ -170,7 +178,7 @@ arena_status enqueue_solve(arena_fft_plan* p, const void* d_f, void* d_u, cudaSt
   cudaEvent_t* ev = timing_events(p);
   if (p->path == ARENA_PATH_POW2) {
     Pow2Args a{d_f, d_u, p->spec, p->tw, p->stw, p->n, p->nc, p->ncp, s, ev, p->tma, p->sm_count,
-               /*ni*/ p->n, /*nj*/ p->n, /*nchunks*/ 1, /*j0*/ 0, /*specC*/ p->spec, kPhaseAll, p->ctrs, p->lag};
+               /*ni*/ p->n, /*nj*/ p->n, /*nchunks*/ 1, /*j0*/ 0, /*specC*/ p->spec, kPhaseAll, p->ctrs, p->lag, p->fuse};
     e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
   } else {
     GenArgs a{&p->gplan, p->tw, p->n, p->nc, p->ncp, s, ev};
@@ -235,9 +243,18 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
     p->path = ARENA_PATH_POW2;
     const char* kern = std::getenv("ARENA_FFT_KERNELS");  // "classic" selects the non-TMA strided kernels
     if (!(kern && std::string(kern) == "classic")) p->tma = new (std::nothrow) TmaCache;
-    const char* fz = std::getenv("ARENA_FFT_FUSED");  // "0" disables the L2-fused z+y kernels
+    // L2-fused z+y pairs.  B200 A/B (r01): at 1024^3 the fused inverse pair ran 0.2 ms faster
+    // than K4+K5, the fused forward pair 0.3 ms slower than K1+K2, and at 512^3 both lost;
+    // default: inverse pair fused for n >= 1024.  ARENA_FFT_FUSED = 0 | fwd | inv | 1 (both).
+    const char* fz = std::getenv("ARENA_FFT_FUSED");
     const bool fused_ok = precision_bits == 64 ? pow2_fused_ok_f64(n) : pow2_fused_ok_f32(n);
-    if (p->tma && fused_ok && !(fz && std::string(fz) == "0")) {
+    int fuse = n >= 1024 ? kFuseInv : 0;
+    if (fz) {
+      const std::string v(fz);
+      fuse = v == "0" ? 0 : v == "fwd" ? kFuseFwd : v == "inv" ? kFuseInv : (kFuseFwd | kFuseInv);
+    }
+    if (p->tma && fused_ok && fuse) {
+      p->fuse = fuse;
       if ((e = cudaMalloc(&p->ctrs, sizeof(int) * size_t(n + 1))) != cudaSuccess) {
         free_plan(p);
         return fail(ARENA_ENOMEM, "fused schedule counters");
@@ -490,7 +507,7 @@ arena_status arena_fft_stage_times(arena_fft_plan* p, double* ms, const char** n
     ++p->solves;
   }
   p->ev_sets_used = 0;
-  const char** nm = p->path == ARENA_PATH_POW2 ? (p->ctrs ? kFusedNames : kPow2Names) : kGenNames;
+  const char** nm = p->path == ARENA_PATH_POW2 ? kStageNames[p->ctrs ? p->fuse : 0] : kGenNames;
   for (int k = 0; k < L && k < max_stages; ++k) {
     if (ms) ms[k] = p->stage_ms[k];
     if (names) names[k] = nm[k];
@@ -663,7 +680,7 @@ arena_status slab_init(arena_fft_slab** out, int n, int prec, int device, int P,
 Pow2Args slab_args(arena_fft_slab* s, SlabRank& r, int rank, const void* f, void* u, cudaStream_t st, int phases) {
   arena_fft_plan* p = s->base;
   return Pow2Args{f, u, r.B, p->tw, p->stw, p->n, p->nc, p->ncp, st, nullptr, &r.tma, p->sm_count,
-                  s->ni, s->nj, s->P, rank * s->nj, r.C, phases, r.ctrs, p->lag};
+                  s->ni, s->nj, s->P, rank * s->nj, r.C, phases, r.ctrs, p->lag, p->fuse};
 }
 
 cudaError_t slab_phase(arena_fft_slab* s, SlabRank& r, int rank, const void* f, void* u, cudaStream_t st, int phases) {

@@ -166,7 +166,7 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   const CUtensorMap* mx = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[1]) : nullptr;
   int mk = 0;
   const bool fused = tma && a.ctrs != nullptr && FusedCfg<T, NR>::OK;
-  if (fused && (a.phases & kPhaseZY)) {
+  if (fused && (a.fuse & kFuseFwd) && (a.phases & kPhaseZY)) {
     mark(a, mk++);
     if constexpr (FusedCfg<T, NR>::OK) {
       if ((e = launch_fused<T, NR, -1>(a, *my, gB))) return e;
@@ -194,7 +194,7 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
           S, stw_ptr<T>(a, 1, XC::E), scale, four_pi2, gC);
     }
   }
-  if (fused && (a.phases & kPhaseYZ)) {
+  if (fused && (a.fuse & kFuseInv) && (a.phases & kPhaseYZ)) {
     mark(a, mk++);
     if constexpr (FusedCfg<T, NR>::OK) {
       if ((e = launch_fused<T, NR, +1>(a, *my, gB))) return e;

@@ -241,3 +241,34 @@ def test_spectral_interpolant_off_grid(cuda):
     got = si(pts)
     want = np.sin(w * pts[:, 0]) * np.sin(w * pts[:, 1]) * np.sin(w * pts[:, 2])
     assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max() + 1e-13
+
+
+@pytest.mark.parametrize("mode", ["1", "fwd", "inv", "0"])
+def test_fused_modes_512(cuda, mode, monkeypatch):
+    """Every fusion mode of the z+y pairs (L2-fused kernels) against the oracle at 512^3."""
+    torch = cuda
+    monkeypatch.setenv("ARENA_FFT_FUSED", mode)
+    n = 512
+    f_np = np.random.default_rng(51).uniform(-1, 1, (n, n, n))
+    f = torch.from_numpy(f_np).cuda()
+    u = torch.empty_like(f)
+    p = arena.Plan(n)
+    p.solve_device(f, u)
+    torch.cuda.synchronize()
+    assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64
+    p.set_stage_timing(True)
+    p.solve_device(f, u)
+    times, _ = p.stage_times()
+    expect = {"1": 3, "fwd": 4, "inv": 4, "0": 5}[mode]
+    assert len(times) == expect, times
+
+
+def test_fused_both_1024_analytic(cuda, monkeypatch):
+    torch = cuda
+    monkeypatch.setenv("ARENA_FFT_FUSED", "1")
+    src, f, ua = _config_device(torch, 4)
+    u = torch.empty_like(f)
+    arena.Plan(1024).solve_device(f, u)
+    torch.cuda.synchronize()
+    e = (torch.linalg.vector_norm(u - ua) / torch.linalg.vector_norm(ua)).item()
+    assert e <= 1e-12, e

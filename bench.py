@@ -44,6 +44,8 @@ def _args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-n", type=int, default=512, help="grid of the bounded CPU sample")
     ap.add_argument("--slab", action="store_true", help="use the slab (NCCL) path even with one rank")
+    ap.add_argument("--decomp", default="slab", choices=("slab", "pencil"), help="multi-GPU decomposition")
+    ap.add_argument("--pgrid", default=None, help="pencil process grid RxC (default: near-square, R <= C)")
     return ap.parse_args()
 
 
@@ -371,14 +373,26 @@ def run_slab(args, rank, world, local):
     elem = 8 if prec == 64 else 4
     dt = torch.float64 if prec == 64 else torch.float32
     src = problems.config(args.config, n)
-    ni = n // world
-    i0 = rank * ni
+    pencil = args.decomp == "pencil"
+    if pencil:
+        if args.pgrid:
+            pr, pc = (int(x) for x in args.pgrid.lower().split("x"))
+        else:
+            pr = 1
+            while pr * pr * 4 <= world:
+                pr *= 2
+            pc = world // pr
+        assert pr * pc == world, "pencil grid must cover all ranks"
+    else:
+        pr, pc = world, 1
+    ni, nj = n // pr, n // pc
+    i0, j0 = (rank // pc) * ni, (rank % pc) * nj
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
-    # this rank's planes of f, global mean removed
-    f64 = torch.empty((ni, n, n), dtype=torch.float64, device="cuda")
-    problems.fill_device(src, "f", f64, 64, sh, i0, ni)
+    # this rank's block of f, global mean removed
+    f64 = torch.empty((ni, nj, n), dtype=torch.float64, device="cuda")
+    problems.fill_device(src, "f", f64, 64, sh, i0, ni, j0, nj)
     tot = f64.sum().reshape(1)
     dist.all_reduce(tot)
     f64 -= tot.item() / float(n) ** 3
@@ -390,7 +404,11 @@ def run_slab(args, rank, world, local):
     if rank == 0:
         idt.copy_(torch.frombuffer(bytearray(arena.nccl_unique_id()), dtype=torch.uint8))
     dist.broadcast(idt, 0)
-    slab = arena.Slab(n, world, rank=rank, nccl_id=bytes(idt.cpu().numpy().tobytes()), precision=prec, device=local)
+    nid = bytes(idt.cpu().numpy().tobytes())
+    if pencil:
+        slab = arena.Pencil(n, pr, pc, rank=rank, nccl_id=nid, precision=prec, device=local)
+    else:
+        slab = arena.Slab(n, world, rank=rank, nccl_id=nid, precision=prec, device=local)
 
     for _ in range(args.warmup):
         slab.solve_device(f, u, sh)
@@ -410,8 +428,8 @@ def run_slab(args, rank, world, local):
     ms_step = t.item() / args.steps
     value = n ** 3 / (ms_step / 1e3)
 
-    ua = torch.empty((ni, n, n), dtype=torch.float64, device="cuda")
-    problems.fill_device(src, "u", ua, 64, sh, i0, ni)
+    ua = torch.empty((ni, nj, n), dtype=torch.float64, device="cuda")
+    problems.fill_device(src, "u", ua, 64, sh, i0, ni, j0, nj)
     sums = torch.stack([ua.sum(), ((u.double() - ua) ** 2).sum(), (ua ** 2).sum()])
     dist.all_reduce(sums)
     mean_u = sums[0].item() / float(n) ** 3
@@ -424,13 +442,16 @@ def run_slab(args, rank, world, local):
     _, b_solve = algorithmic_bytes(n, elem)
     C = n * n * (n // 2 + 1) * 2 * elem
     hbm_per_gpu = b_solve / world
-    nvl_per_gpu = 2 * (C / world) * (world - 1) / world
+    if pencil:
+        nvl_per_gpu = 2 * (C / world) * ((pr - 1) / pr + (pc - 1) / pc)
+    else:
+        nvl_per_gpu = 2 * (C / world) * (world - 1) / world
     nvl_peak = 770.0  # GB/s per direction, measured peer copy (B200_PROFILING.md)
     t_roof = max(hbm_per_gpu / (peak * 1e9), nvl_per_gpu / (nvl_peak * 1e9))
 
     e2e = None
     if not args.no_e2e:
-        hf = torch.empty((ni, n, n), dtype=dt, pin_memory=True)
+        hf = torch.empty((ni, nj, n), dtype=dt, pin_memory=True)
         hf.copy_(f)
         hu = torch.empty_like(hf, pin_memory=True)
         ksteps = max(1, min(args.steps, 3))
@@ -447,7 +468,7 @@ def run_slab(args, rank, world, local):
         el = te.item()
         e2e = {"value": n ** 3 * ksteps / el, "unit": UNIT, "h2d_bytes_per_step": n ** 3 * elem,
                "d2h_bytes_per_step": n ** 3 * elem, "steps": ksteps, "ms_per_step": el / ksteps * 1e3,
-               "api": "arena_slab_solve_device with per-rank pinned H2D/D2H of the rank's slab (summed over ranks)"}
+               "api": "arena_slab/pencil_solve_device with per-rank pinned H2D/D2H of the rank's block"}
 
     if rank == 0:
         line = {
@@ -455,7 +476,8 @@ def run_slab(args, rank, world, local):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if prec == 64 else "f32", "data": "synthetic",
             "config": {"workload": f"C{args.config}: {problems.CONFIG_TEXT[args.config]}", "n": n, "precision": prec,
-                       "decomposition": f"slab x{world} over i, NCCL grouped send/recv all-to-all",
+                       "decomposition": (f"pencil {pr}x{pc}, NCCL row/column all-to-alls (4 per solve)" if pencil
+                                         else f"slab x{world} over i, NCCL grouped send/recv all-to-all"),
                        "l2": "inputs larger than L2, no flush"},
             "roofline": {"bound": "hbm+nvlink", "achieved": hbm_per_gpu / (ms_step / 1e3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": t_roof / (ms_step / 1e3), "traffic": None, "peak_kind": peak_kind,
@@ -463,7 +485,7 @@ def run_slab(args, rank, world, local):
                          "t_roof_ms": t_roof * 1e3},
             "cpu_baseline": None,
             "e2e": e2e,
-            "gpu_launches": 5 * args.steps,
+            "gpu_launches": slab.launches_per_solve * args.steps,
             "clocks": clk.summary(),
             "parity": {"rel_l2_vs_analytic": rel_an},
         }
@@ -476,7 +498,7 @@ def main():
     rank, world, local = _dist()
     if args.impl == "reference":
         run_reference(args, rank, world)
-    elif world > 1 or args.slab:
+    elif world > 1 or args.slab or args.pgrid:
         run_slab(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)

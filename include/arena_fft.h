@@ -109,6 +109,12 @@ arena_status arena_source_modes_slab(int n, int precision_bits, int nmodes, cons
 arena_status arena_source_gaussian_slab(int n, int precision_bits, double alpha, double cx, double cy, double cz,
                                         int which, int i0, int ni, void* d_out, void* stream);
 
+/* Block variants (pencil ranks): planes i0 .. i0+ni-1, rows j0 .. j0+nj-1, stored ni x nj x n. */
+arena_status arena_source_modes_block(int n, int precision_bits, int nmodes, const int* k, const double* coef, int i0,
+                                      int ni, int j0, int nj, void* d_out, void* stream);
+arena_status arena_source_gaussian_block(int n, int precision_bits, double alpha, double cx, double cy, double cz,
+                                         int which, int i0, int ni, int j0, int nj, void* d_out, void* stream);
+
 /* ---- Slab decomposition over P GPUs ------------------------
  * One process per GPU.  Rank r owns planes i in [r*n/P, (r+1)*n/P) of f and u
  * (a contiguous n/P * n * n slice of the GridField layout).  The two global
@@ -126,8 +132,25 @@ arena_status arena_slab_create(arena_fft_slab** slab, int n, int precision_bits,
 arena_status arena_slab_create_loopback(arena_fft_slab** slab, int n, int precision_bits, int device, int nvranks);
 void arena_slab_destroy(arena_fft_slab* slab);
 arena_status arena_slab_info(const arena_fft_slab* slab, int* ni, int* nj, size_t* chunk_bytes, size_t* workspace_bytes);
+int arena_slab_launches_per_solve(const arena_fft_slab* slab);
 /* d_f, d_u: this rank's slab (loopback: the full field); asynchronous on stream. */
 arena_status arena_slab_solve_device(arena_fft_slab* slab, const void* d_f, void* d_u, void* stream);
+
+/* ---- Pencil decomposition over Pr x Pc GPUs (BASELINE config 5) --------------
+ * Rank r*Pc + c owns the f / u block i in [r n/Pr, (r+1) n/Pr), j in
+ * [c n/Pc, (c+1) n/Pc), all k, stored contiguously as (n/Pr) x (n/Pc) x n.
+ * Four all-to-alls per solve on row / column communicators (ncclCommSplit of a
+ * world communicator made from nccl_id).  Loopback: all ranks on one device, the
+ * solve takes the full n^3 field.  Power-of-two 64 <= n <= 2048. */
+typedef struct arena_fft_pencil arena_fft_pencil;
+arena_status arena_pencil_create(arena_fft_pencil** pencil, int n, int precision_bits, int device, int pr, int pc,
+                                 int rank, const void* nccl_id);
+arena_status arena_pencil_create_loopback(arena_fft_pencil** pencil, int n, int precision_bits, int device, int pr,
+                                          int pc);
+void arena_pencil_destroy(arena_fft_pencil* pencil);
+arena_status arena_pencil_info(const arena_fft_pencil* pencil, int* kq, size_t* buffer_bytes, size_t* block_bytes);
+int arena_pencil_launches_per_solve(const arena_fft_pencil* pencil);
+arena_status arena_pencil_solve_device(arena_fft_pencil* pencil, const void* d_f, void* d_u, void* stream);
 
 /* Batch evaluation of arena::SpectralInterpolant (fft_solver.cpp:89-114) on the
  * GPU: out[p] = sum_m Re(amp_m exp(2 pi i k_m . x_p)).  k: 3*nmodes ints (signed

@@ -67,6 +67,9 @@ _sig = {
     "arena_source_modes_slab": (_i, [_i, _i, _i, _vp, _vp, _i, _i, _vp, _vp]),
     "arena_source_gaussian_slab": (_i, [_i, _i, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                         _i, _i, _i, _vp, _vp]),
+    "arena_source_modes_block": (_i, [_i, _i, _i, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
+    "arena_source_gaussian_block": (_i, [_i, _i, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                         _i, _i, _i, _i, _i, _vp, _vp]),
     "arena_nccl_unique_id_bytes": (_i, []),
     "arena_nccl_unique_id": (_i, [_vp, _i]),
     "arena_slab_create": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _i, _i, _vp]),
@@ -76,6 +79,13 @@ _sig = {
                              ctypes.POINTER(ctypes.c_size_t)]),
     "arena_slab_solve_device": (_i, [_vp, _vp, _vp, _vp]),
     "arena_pow2_kernel_geometry": (_i, [_i, _i, ctypes.POINTER(_i)]),
+    "arena_pencil_create": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _i, _i, _i, _vp]),
+    "arena_pencil_create_loopback": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _i, _i]),
+    "arena_pencil_destroy": (None, [_vp]),
+    "arena_pencil_launches_per_solve": (_i, [_vp]),
+    "arena_slab_launches_per_solve": (_i, [_vp]),
+    "arena_pencil_info": (_i, [_vp, ctypes.POINTER(_i), ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),
+    "arena_pencil_solve_device": (_i, [_vp, _vp, _vp, _vp]),
     "arena_interpolant_eval": (_i, [_i, _i, _vp, _vp, _i, _vp, _vp]),
     "arena_last_error": (ctypes.c_char_p, []),
     "arena_fft_abi_version": (_i, []),
@@ -221,6 +231,10 @@ class Slab:
                "arena_slab_info")
         self.ni, self.nj, self.chunk_bytes, self.workspace_bytes = ni.value, nj.value, cb.value, wb.value
 
+    @property
+    def launches_per_solve(self) -> int:
+        return lib.arena_slab_launches_per_solve(self._s)
+
     def solve_device(self, f, u, stream: Optional[int] = None) -> None:
         if stream is None:
             import torch
@@ -231,6 +245,53 @@ class Slab:
     def close(self) -> None:
         if getattr(self, "_s", None) and self._s.value:
             lib.arena_slab_destroy(self._s)
+            self._s = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Pencil:
+    """Pencil decomposition over a Pr x Pc process grid (include/arena_fft.h, arena_pencil_*).
+
+    Pencil(n, Pr, Pc, rank=r, nccl_id=bytes) — one rank (its block (n/Pr) x (n/Pc) x n);
+    Pencil(n, Pr, Pc, loopback=True)        — all ranks on one device (full field in/out).
+    """
+
+    def __init__(self, n: int, pr: int, pc: int, rank: int = 0, nccl_id: Optional[bytes] = None,
+                 precision: int = 64, device: int = -1, loopback: bool = False):
+        self._s = _vp()
+        if loopback:
+            _check(lib.arena_pencil_create_loopback(ctypes.byref(self._s), int(n), int(precision), int(device),
+                                                    int(pr), int(pc)), "arena_pencil_create_loopback")
+        else:
+            if nccl_id is None:
+                raise ValueError("nccl_id required (see nccl_unique_id())")
+            buf = ctypes.create_string_buffer(bytes(nccl_id), len(nccl_id))
+            _check(lib.arena_pencil_create(ctypes.byref(self._s), int(n), int(precision), int(device), int(pr),
+                                           int(pc), int(rank), buf), "arena_pencil_create")
+        self.n, self.pr, self.pc, self.rank = int(n), int(pr), int(pc), int(rank)
+        kq, bb, kb = _i(), ctypes.c_size_t(), ctypes.c_size_t()
+        _check(lib.arena_pencil_info(self._s, ctypes.byref(kq), ctypes.byref(bb), ctypes.byref(kb)), "arena_pencil_info")
+        self.kq, self.buffer_bytes, self.block_bytes = kq.value, bb.value, kb.value
+
+    @property
+    def launches_per_solve(self) -> int:
+        return lib.arena_pencil_launches_per_solve(self._s)
+
+    def solve_device(self, f, u, stream: Optional[int] = None) -> None:
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(f.device).cuda_stream
+        _check(lib.arena_pencil_solve_device(self._s, _vp(_ptr(f)), _vp(_ptr(u)), _vp(stream)),
+               "arena_pencil_solve_device")
+
+    def close(self) -> None:
+        if getattr(self, "_s", None) and self._s.value:
+            lib.arena_pencil_destroy(self._s)
             self._s = _vp()
 
     def __del__(self):
@@ -333,27 +394,28 @@ class SpectralInterpolant:
 
 
 def source_modes(n: int, kvec: np.ndarray, coef: np.ndarray, out, precision: int = 64, stream: int = 0,
-                 i0: int = 0, ni: Optional[int] = None) -> None:
-    """Device buffer `out` = sum_m Re(coef_m e^{2 pi i k_m.x}) on planes i0..i0+ni-1 (default: all n^3).
-    kvec: (M, 3) ints, coef: (M,) complex."""
+                 i0: int = 0, ni: Optional[int] = None, j0: int = 0, nj: Optional[int] = None) -> None:
+    """Device buffer `out` = sum_m Re(coef_m e^{2 pi i k_m.x}) on the block i0..i0+ni-1 x j0..j0+nj-1 x all k
+    (default: all n^3).  kvec: (M, 3) ints, coef: (M,) complex."""
     kvec = np.ascontiguousarray(kvec, dtype=np.int32).reshape(-1, 3)
     c = np.ascontiguousarray(np.stack([np.real(coef), np.imag(coef)], axis=-1), dtype=np.float64)
-    _check(lib.arena_source_modes_slab(int(n), int(precision), int(kvec.shape[0]), _vp(kvec.ctypes.data),
-                                       _vp(c.ctypes.data), int(i0), int(n if ni is None else ni), _vp(_ptr(out)),
-                                       _vp(stream)), "arena_source_modes")
+    _check(lib.arena_source_modes_block(int(n), int(precision), int(kvec.shape[0]), _vp(kvec.ctypes.data),
+                                        _vp(c.ctypes.data), int(i0), int(n if ni is None else ni), int(j0),
+                                        int(n if nj is None else nj), _vp(_ptr(out)), _vp(stream)),
+           "arena_source_modes")
 
 
 def source_gaussian(n: int, alpha: float, center, which: int, out, precision: int = 64, stream: int = 0,
-                    i0: int = 0, ni: Optional[int] = None) -> None:
-    """Device buffer `out` = periodised Gaussian u (which=0) or f = -Lap u (which=1), planes i0..i0+ni-1."""
+                    i0: int = 0, ni: Optional[int] = None, j0: int = 0, nj: Optional[int] = None) -> None:
+    """Device buffer `out` = periodised Gaussian u (which=0) or f = -Lap u (which=1) on a block."""
     cx, cy, cz = (float(c) for c in center)
-    _check(lib.arena_source_gaussian_slab(int(n), int(precision), float(alpha), cx, cy, cz, int(which), int(i0),
-                                          int(n if ni is None else ni), _vp(_ptr(out)), _vp(stream)),
-           "arena_source_gaussian")
+    _check(lib.arena_source_gaussian_block(int(n), int(precision), float(alpha), cx, cy, cz, int(which), int(i0),
+                                           int(n if ni is None else ni), int(j0), int(n if nj is None else nj),
+                                           _vp(_ptr(out)), _vp(stream)), "arena_source_gaussian")
 
 
 __all__ = [
-    "Plan", "Slab", "SpectralInterpolant", "nccl_unique_id", "get_plan", "poisson_spectral_solve", "dft3_forward", "dft3_inverse", "signed_freq",
+    "Plan", "Slab", "Pencil", "SpectralInterpolant", "nccl_unique_id", "get_plan", "poisson_spectral_solve", "dft3_forward", "dft3_inverse", "signed_freq",
     "source_modes", "source_gaussian", "ArenaError", "lib", "LIB_PATH", "CORE_PATH", "HEADER_PATH",
     "PATH_POW2", "PATH_GENERIC",
 ]

@@ -55,6 +55,35 @@ enum : int { kFuseFwd = 1, kFuseInv = 2 };
 cudaError_t launch_pow2_f64(const Pow2Args& a);
 cudaError_t launch_pow2_f32(const Pow2Args& a);
 
+// Pencil decomposition (Pr x Pc ranks): one phase of a rank's solve.
+struct PencilArgs {
+  const void* f;     // rank's f block: (n/Pr) x (n/Pc) x n
+  void* u;           // rank's u block
+  void* buf1;        // R (k-chunked z output) / B2 (y output, j chunks of n/Pr)
+  void* buf2;        // Y (after the row exchange, j chunks of n/Pc) / C (x pass)
+  const void* tw;
+  const void* stw;
+  int n, Pr, Pc, r, c;
+  int kq;            // k-chunk pitch (complex)
+  cudaStream_t stream;
+  TmaCache* tma;     // maps[0]: y over buf2 (Y), maps[1]: x over buf2 (C); y-inv map in tma2
+  TmaCache* tma2;    // maps[0]: y-inverse over buf1 (B2)
+  int sm_count;
+};
+enum : int { kPencilZ1 = 0, kPencilY1, kPencilX, kPencilY2, kPencilZ2 };
+cudaError_t pencil_phase_f64(const PencilArgs& a, int phase);
+cudaError_t pencil_phase_f32(const PencilArgs& a, int phase);
+// k-chunk pitch: ceil(nc / Pc) rounded up to 8 (128-byte rows), or to 2 when
+// that would leave a rank without k (small n); every chunk is non-empty.
+inline int pencil_kq(int n, int Pc) {
+  const int nc = n / 2 + 1, w = (nc + Pc - 1) / Pc;
+  for (int q : {8, 4, 2}) {
+    const int kq = (w + q - 1) / q * q;
+    if ((Pc - 1) * kq < nc) return kq;
+  }
+  return w;
+}
+
 // Line length, points per thread, lines per CTA, threads, shared bytes.
 struct KernelGeom {
   int line, E, L, threads, smem;

@@ -748,6 +748,8 @@ arena_status arena_slab_create_loopback(arena_fft_slab** out, int n, int precisi
 
 void arena_slab_destroy(arena_fft_slab* s) { free_slab(s); }
 
+int arena_slab_launches_per_solve(const arena_fft_slab* s) { return s ? s->base->launches() : 0; }
+
 arena_status arena_slab_info(const arena_fft_slab* s, int* ni, int* nj, size_t* chunk_bytes, size_t* workspace_bytes) {
   if (!s) return fail(ARENA_EINVAL, "slab is NULL");
   if (ni) *ni = s->ni;
@@ -782,6 +784,265 @@ arena_status arena_slab_solve_device(arena_fft_slab* s, const void* d_f, void* d
     const int rank = s->loopback ? v : s->rank;
     if ((e = slab_phase(s, s->ranks[v], rank, fr(v), ur(v), st, kPhaseYZ)) != cudaSuccess)
       return cuda_fail(e, "slab K4+K5");
+  }
+  return ARENA_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================
+// Pencil decomposition over Pr x Pc ranks (BASELINE config 5):
+// rank (r, c) owns the f / u block i in [r n/Pr, ..), j in [c n/Pc, ..), all k.
+//   K1 z-r2c, k split into Pc chunks (buf1 = R) -> row all-to-all (same r) ->
+//   K2 y-fwd on (il, local k) lines over all j (buf2 = Y -> buf1 = B2, j re-chunked
+//   by n/Pr) -> column all-to-all (same c) -> K3 on (local j, local k) lines over
+//   all i (buf2 = C) -> the reverse.  Four all-to-alls per solve, as in the
+//   paper's pencil scheme.  Row / column communicators come from
+//   ncclCommSplit; the loopback mode runs all Pr*Pc ranks on one device.
+namespace {
+
+struct PencilRank {
+  void* buf1 = nullptr;
+  void* buf2 = nullptr;
+  void* fblk = nullptr;  // loopback only: the rank's f / u blocks
+  void* ublk = nullptr;
+  TmaCache tma, tma2;
+};
+
+}  // namespace
+
+struct arena_fft_pencil {
+  arena_fft_plan* base = nullptr;
+  int n = 0, Pr = 1, Pc = 1, rank = 0, loopback = 0, kq = 0;
+  size_t buf_bytes = 0, blk_bytes = 0;
+  std::vector<PencilRank> ranks;
+  ncclComm_t world = nullptr, row = nullptr, col = nullptr;
+};
+
+namespace {
+
+void free_pencil(arena_fft_pencil* s) {
+  if (!s) return;
+  if (s->base) {
+    DeviceGuard g(s->base->device);
+    for (PencilRank& r : s->ranks)
+      for (void* p : {r.buf1, r.buf2, r.fblk, r.ublk})
+        if (p) cudaFree(p);
+    if (NcclApi* a = nccl_api()) {
+      for (ncclComm_t c : {s->row, s->col, s->world})
+        if (c) a->CommDestroy(c);
+    }
+  }
+  free_plan(s->base);
+  delete s;
+}
+
+arena_status pencil_init(arena_fft_pencil** out, int n, int prec, int device, int Pr, int Pc, int rank, int loopback,
+                         const void* id) {
+  if (!out) return fail(ARENA_EINVAL, "pencil pointer is NULL");
+  *out = nullptr;
+  if (Pr < 1 || Pc < 1 || (Pr & (Pr - 1)) || (Pc & (Pc - 1)) || Pr > n || Pc > n)
+    return fail(ARENA_EINVAL, "process grid must be powers of two <= n");
+  if (rank < 0 || rank >= Pr * Pc) return fail(ARENA_EINVAL, "bad rank");
+  if (!is_pow2(n) || n < 64 || n > kPow2MaxN) return fail(ARENA_EUNSUPPORTED, "pencil path needs power-of-two 64 <= n <= 2048");
+  const int ni = n / Pr, nj = n / Pc;
+  arena_fft_pencil* s = new (std::nothrow) arena_fft_pencil;
+  if (!s) return fail(ARENA_ENOMEM, "pencil");
+  arena_status st = create_plan(&s->base, n, prec, device, false);
+  if (st != ARENA_OK) {
+    delete s;
+    return st;
+  }
+  if (!s->base->tma) {
+    free_pencil(s);
+    return fail(ARENA_EUNSUPPORTED, "pencil path needs the TMA kernels (unset ARENA_FFT_KERNELS)");
+  }
+  DeviceGuard g(s->base->device);
+  s->n = n;
+  s->Pr = Pr;
+  s->Pc = Pc;
+  s->rank = rank;
+  s->loopback = loopback;
+  s->kq = pencil_kq(n, Pc);
+  const size_t elem = s->base->elem;
+  s->buf_bytes = size_t(ni) * n * s->kq * 2 * elem;
+  s->blk_bytes = size_t(ni) * nj * n * elem;
+  if ((size_t(ni) * nj) % 32) {
+    free_pencil(s);
+    return fail(ARENA_EUNSUPPORTED, "rank block too small");
+  }
+  s->ranks.resize(loopback ? Pr * Pc : 1);
+  for (PencilRank& r : s->ranks) {
+    cudaError_t e = cudaSuccess;
+    if ((e = cudaMalloc(&r.buf1, s->buf_bytes)) || (e = cudaMalloc(&r.buf2, s->buf_bytes)) ||
+        (loopback && ((e = cudaMalloc(&r.fblk, s->blk_bytes)) || (e = cudaMalloc(&r.ublk, s->blk_bytes))))) {
+      free_pencil(s);
+      return fail(ARENA_ENOMEM, "pencil buffers: " + std::string(cudaGetErrorString(e)));
+    }
+  }
+  if (!loopback) {
+    NcclApi* a = nccl_api();
+    auto split = reinterpret_cast<ncclResult_t (*)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*)>(
+        a ? dlsym(a->h, "ncclCommSplit") : nullptr);
+    if (!a || !split) {
+      free_pencil(s);
+      return fail(ARENA_ENCCL, "libnccl.so.2 (with ncclCommSplit) not found");
+    }
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof uid);
+    ncclResult_t res = a->CommInitRank(&s->world, Pr * Pc, uid, rank);
+    if (res != ncclSuccess) {
+      s->world = nullptr;
+      free_pencil(s);
+      return nccl_fail(res, "ncclCommInitRank");
+    }
+    const int r = rank / Pc, c = rank % Pc;
+    if ((res = split(s->world, r, c, &s->row, nullptr)) != ncclSuccess ||
+        (res = split(s->world, c, r, &s->col, nullptr)) != ncclSuccess) {
+      free_pencil(s);
+      return nccl_fail(res, "ncclCommSplit");
+    }
+  }
+  *out = s;
+  return ARENA_OK;
+}
+
+PencilArgs pencil_args(arena_fft_pencil* s, PencilRank& pr, int rank, const void* f, void* u, cudaStream_t st) {
+  arena_fft_plan* p = s->base;
+  PencilArgs a{};
+  a.f = f;
+  a.u = u;
+  a.buf1 = pr.buf1;
+  a.buf2 = pr.buf2;
+  a.tw = p->tw;
+  a.stw = p->stw;
+  a.n = s->n;
+  a.Pr = s->Pr;
+  a.Pc = s->Pc;
+  a.r = rank / s->Pc;
+  a.c = rank % s->Pc;
+  a.kq = s->kq;
+  a.stream = st;
+  a.tma = &pr.tma;
+  a.tma2 = &pr.tma2;
+  a.sm_count = p->sm_count;
+  return a;
+}
+
+// Row (same r) or column (same c) all-to-all from buf `from` to buf `to`
+// (1 = buf1, 2 = buf2); chunk q of a rank's source goes to peer q's chunk
+// (sender's index in the group).
+arena_status pencil_exchange(arena_fft_pencil* s, cudaStream_t st, bool rowgrp, int from, int to) {
+  const int ni = s->n / s->Pr;
+  const int grp = rowgrp ? s->Pc : s->Pr;
+  const size_t chunk_rows = size_t(ni) * (rowgrp ? s->n / s->Pc : s->n / s->Pr);
+  const size_t bytes = chunk_rows * s->kq * 2 * s->base->elem;
+  auto buf = [&](PencilRank& r, int which) { return static_cast<char*>(which == 1 ? r.buf1 : r.buf2); };
+  if (s->loopback) {
+    for (int rk = 0; rk < s->Pr * s->Pc; ++rk) {
+      const int r = rk / s->Pc, c = rk % s->Pc;
+      const int me = rowgrp ? c : r;
+      for (int q = 0; q < grp; ++q) {
+        const int peer = rowgrp ? r * s->Pc + q : q * s->Pc + c;
+        cudaError_t e = cudaMemcpyAsync(buf(s->ranks[peer], to) + size_t(me) * bytes,
+                                        buf(s->ranks[rk], from) + size_t(q) * bytes, bytes, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "loopback pencil exchange");
+      }
+    }
+    return ARENA_OK;
+  }
+  NcclApi* a = nccl_api();
+  const ncclDataType_t dt = s->base->prec == 64 ? ncclFloat64 : ncclFloat32;
+  const size_t count = chunk_rows * s->kq * 2;
+  ncclComm_t comm = rowgrp ? s->row : s->col;
+  PencilRank& me = s->ranks[0];
+  ncclResult_t res = a->GroupStart();
+  if (res != ncclSuccess) return nccl_fail(res, "ncclGroupStart");
+  for (int q = 0; q < grp; ++q) {
+    if ((res = a->Send(buf(me, from) + size_t(q) * bytes, count, dt, q, comm, st)) != ncclSuccess)
+      return nccl_fail(res, "ncclSend");
+    if ((res = a->Recv(buf(me, to) + size_t(q) * bytes, count, dt, q, comm, st)) != ncclSuccess)
+      return nccl_fail(res, "ncclRecv");
+  }
+  if ((res = a->GroupEnd()) != ncclSuccess) return nccl_fail(res, "ncclGroupEnd");
+  return ARENA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+arena_status arena_pencil_create(arena_fft_pencil** out, int n, int precision_bits, int device, int pr, int pc,
+                                 int rank, const void* nccl_id) {
+  if (!nccl_id) return fail(ARENA_EINVAL, "NCCL unique id is NULL");
+  return pencil_init(out, n, precision_bits, device, pr, pc, rank, 0, nccl_id);
+}
+
+arena_status arena_pencil_create_loopback(arena_fft_pencil** out, int n, int precision_bits, int device, int pr,
+                                          int pc) {
+  return pencil_init(out, n, precision_bits, device, pr, pc, 0, 1, nullptr);
+}
+
+void arena_pencil_destroy(arena_fft_pencil* s) { free_pencil(s); }
+
+int arena_pencil_launches_per_solve(const arena_fft_pencil* s) { return s ? 5 : 0; }
+
+arena_status arena_pencil_info(const arena_fft_pencil* s, int* kq, size_t* buffer_bytes, size_t* block_bytes) {
+  if (!s) return fail(ARENA_EINVAL, "pencil is NULL");
+  if (kq) *kq = s->kq;
+  if (buffer_bytes) *buffer_bytes = s->buf_bytes;
+  if (block_bytes) *block_bytes = s->blk_bytes;
+  return ARENA_OK;
+}
+
+arena_status arena_pencil_solve_device(arena_fft_pencil* s, const void* d_f, void* d_u, void* stream) {
+  if (!s || !d_f || !d_u) return fail(ARENA_EINVAL, "NULL pencil or buffer");
+  DeviceGuard g(s->base->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int n = s->n, ni = n / s->Pr, nj = n / s->Pc;
+  const size_t elem = s->base->elem;
+  const int nr = int(s->ranks.size());
+  cudaError_t e;
+  // loopback: scatter the full field into the virtual ranks' blocks
+  if (s->loopback) {
+    for (int rk = 0; rk < nr; ++rk) {
+      const int r = rk / s->Pc, c = rk % s->Pc;
+      const char* src = static_cast<const char*>(d_f) + (size_t(r) * ni * n + size_t(c) * nj) * n * elem;
+      if ((e = cudaMemcpy2DAsync(s->ranks[rk].fblk, size_t(nj) * n * elem, src, size_t(n) * n * elem,
+                                 size_t(nj) * n * elem, ni, cudaMemcpyDeviceToDevice, st)))
+        return cuda_fail(e, "pencil scatter");
+    }
+  }
+  auto run = [&](int phase) -> arena_status {
+    for (int v = 0; v < nr; ++v) {
+      const int rank = s->loopback ? v : s->rank;
+      PencilRank& pr = s->ranks[v];
+      const void* f = s->loopback ? pr.fblk : d_f;
+      void* u = s->loopback ? pr.ublk : d_u;
+      const PencilArgs a = pencil_args(s, pr, rank, f, u, st);
+      cudaError_t err = s->base->prec == 64 ? pencil_phase_f64(a, phase) : pencil_phase_f32(a, phase);
+      if (err != cudaSuccess) return cuda_fail(err, "pencil phase");
+    }
+    return ARENA_OK;
+  };
+  arena_status r;
+  if ((r = run(kPencilZ1)) != ARENA_OK) return r;
+  if ((r = pencil_exchange(s, st, true, 1, 2)) != ARENA_OK) return r;   // R -> Y
+  if ((r = run(kPencilY1)) != ARENA_OK) return r;                       // Y -> B2
+  if ((r = pencil_exchange(s, st, false, 1, 2)) != ARENA_OK) return r;  // B2 -> C
+  if ((r = run(kPencilX)) != ARENA_OK) return r;
+  if ((r = pencil_exchange(s, st, false, 2, 1)) != ARENA_OK) return r;  // C -> B2
+  if ((r = run(kPencilY2)) != ARENA_OK) return r;                       // B2 -> Y
+  if ((r = pencil_exchange(s, st, true, 2, 1)) != ARENA_OK) return r;   // Y -> R
+  if ((r = run(kPencilZ2)) != ARENA_OK) return r;
+  if (s->loopback) {
+    for (int rk = 0; rk < nr; ++rk) {
+      const int rr = rk / s->Pc, c = rk % s->Pc;
+      char* dst = static_cast<char*>(d_u) + (size_t(rr) * ni * n + size_t(c) * nj) * n * elem;
+      if ((e = cudaMemcpy2DAsync(dst, size_t(n) * n * elem, s->ranks[rk].ublk, size_t(nj) * n * elem,
+                                 size_t(nj) * n * elem, ni, cudaMemcpyDeviceToDevice, st)))
+        return cuda_fail(e, "pencil gather");
+    }
   }
   return ARENA_OK;
 }

@@ -390,19 +390,30 @@ struct TmaCfg {
 // x tile (fixed jl): boxes {2L, 1, IB, 1, 1} over il blocks and chunks -> all i.
 __host__ __device__ constexpr int tma_ib(int ni) { return ni < 256 ? ni : 256; }
 
-// PASS 0: y forward, 1: y backward (layout B, tiles over (il, k-tile));
+// The k range a workspace holds: local k in [0, kc), row pitch kq complex,
+// global k = k0 + local k.  One GPU and slab: {nc, ncp, 0}; pencil: the rank's
+// k chunk.
+struct KSpan {
+  int kc, kq, k0;
+};
+
+// PASS 0: y forward, 1: y backward (layout B, tiles over (il, k-tile)); the y
+// passes may write to another buffer / layout (`out`, `gout`; the pencil path
+// re-chunks j between its two exchanges).
 // PASS 2: x forward * Poisson symbol * x backward (layout C, tiles over (jl, k-tile)).
 // j0: global j of this rank's first local j (x pass symbol; 0 on one GPU).
 template <typename T, int N, int PASS>
 __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
     k_strided_tma(const __grid_constant__ CUtensorMap tmap, vec2_t<T>* __restrict__ spec,
-                  const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g, int nchunks, int j0) {
+                  const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g, int nchunks, int j0, KSpan ks,
+                  vec2_t<T>* __restrict__ out, Layout gout) {
   using V = vec2_t<T>;
   using C = TmaCfg<T, N>;
-  constexpr int E = C::E, P = C::P, L = C::L, KT = C::KT, TILE = C::TILE;
-  constexpr int ncp = spec_pitch(N);
+  constexpr int E = C::E, P = C::P, L = C::L, TILE = C::TILE;
   constexpr uint32_t TILE_BYTES = TILE * sizeof(V);
   constexpr int NBUF = C::NBUF;
+  const int KT = (ks.kc + L - 1) / L;
+  const size_t kq = size_t(ks.kq);
   const int NT = (PASS < 2 ? g.ni : g.nj) * KT;
   V* bufs = smem_base<V>();
   uint64_t* bar = reinterpret_cast<uint64_t*>(bufs + NBUF * TILE);
@@ -487,7 +498,7 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
       line_fft<N, E, L, +1>(v, cur, stw, t, l);
     } else {
       line_fft<N, E, L, -1>(v, cur, stw, t, l);
-      const T kj = T(signed_freq(j0 + outer, N)), kk = T(k);
+      const T kj = T(signed_freq(j0 + outer, N)), kk = T(ks.k0 + k);
       const T c = kj * kj + kk * kk;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
@@ -499,19 +510,115 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
       }
       line_fft<N, E, L, +1>(v, cur, stw, t, l);
     }
-    if (k < C::NC) {
+    if (k < ks.kc) {
       if constexpr (PASS < 2) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) __stcs(spec + rowB(g, outer, t + P * e) * ncp + k, v[e]);
+        for (int e = 0; e < E; ++e) __stcs(out + rowB(gout, outer, t + P * e) * kq + k, v[e]);
       } else {
 #pragma unroll
-        for (int e = 0; e < E; ++e) __stcs(spec + rowC(g, t + P * e, outer) * ncp + k, v[e]);
+        for (int e = 0; e < E; ++e) __stcs(spec + rowC(g, t + P * e, outer) * kq + k, v[e]);
       }
     }
     // No barrier needed here: every thread's last access to `cur` (the tile
     // read, or the last exchange read) is followed by a __syncthreads, so
     // thread 0 only refills it next iteration after all threads are done.
   }
+}
+
+}  // namespace arena_fft
+
+// ============================================================ pencil z passes
+// Pencil decomposition: a rank owns the f / u block
+// (ni = n/Pr planes) x (nj = n/Pc rows of j) x n, rows (il, jl) contiguous.  K1
+// writes each row's half spectrum split into Pc k-chunks of kq complex — chunk
+// c is the block sent to column c of the rank's row group — and K5 gathers them
+// back.  Inside a chunk rows are in Layout(ni, nj) order.
+namespace arena_fft {
+
+template <typename T, int NR>
+__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
+    k_zfwd_pencil(const T* __restrict__ f, vec2_t<T>* __restrict__ R, const vec2_t<T>* __restrict__ tw,
+                  const vec2_t<T>* __restrict__ stw, Layout gz, int kq) {
+  using V = vec2_t<T>;
+  using C = ContigCfg<T, NR>;
+  constexpr int M = C::M, E = C::E, P = C::P, L = C::L;
+  constexpr int SW = engine_swizzle<M, E>();
+  V* sm = smem_base<V>();
+  const int l = threadIdx.x % L, t = threadIdx.x / L;
+  const size_t row = size_t(blockIdx.x) * L + l;  // il * nj + jl
+  const V* src = reinterpret_cast<const V*>(f + row * NR);
+  V v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = __ldcs(src + t + P * e);
+  line_fft<M, E, L, -1>(v, sm, stw, t, l);
+#pragma unroll
+  for (int e = 0; e < E; ++e) sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
+  __syncthreads();
+  const size_t rin = lrow(gz, 0, int(row >> gz.njs), int(row & (gz.nj - 1)));
+  const size_t chunk = size_t(gz.ni) * gz.nj;
+  auto put = [&](int k, V x) {
+    const int c = k / kq;
+    R[(size_t(c) * chunk + rin) * kq + (k - c * kq)] = x;
+  };
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int k = t + P * e;
+    const V A = v[e];
+    const V Bc = sm[smem_idx<L, SW, V>((M - k) & (M - 1), l)];
+    const V B{Bc.x, -Bc.y};
+    const V W = tw_load(tw, k);
+    const V WD = cmul(W, csub(A, B));
+    put(k, V{T(0.5) * (A.x + B.x + WD.y), T(0.5) * (A.y + B.y - WD.x)});
+    if (k == 0) put(M, V{A.x - A.y, T(0)});
+  }
+}
+
+template <typename T, int NR>
+__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
+    k_zinv_pencil(const vec2_t<T>* __restrict__ R, T* __restrict__ u, const vec2_t<T>* __restrict__ tw,
+                  const vec2_t<T>* __restrict__ stw, Layout gz, int kq) {
+  using V = vec2_t<T>;
+  using C = ContigCfg<T, NR>;
+  constexpr int M = C::M, E = C::E, P = C::P, L = C::L;
+  constexpr int SW = engine_swizzle<M, E>();
+  V* sm = smem_base<V>();
+  V* xm = sm + M * L;
+  const int l = threadIdx.x % L, t = threadIdx.x / L;
+  const size_t row = size_t(blockIdx.x) * L + l;
+  const size_t rin = lrow(gz, 0, int(row >> gz.njs), int(row & (gz.nj - 1)));
+  const size_t chunk = size_t(gz.ni) * gz.nj;
+  auto get = [&](int k) {
+    const int c = k / kq;
+    return __ldcs(R + (size_t(c) * chunk + rin) * kq + (k - c * kq));
+  };
+  V v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    v[e] = get(t + P * e);
+    sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
+  }
+  if (t == 0) xm[l] = get(M);
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int k = t + P * e;
+    V A = v[e];
+    V Bs = (k == 0) ? xm[l] : sm[smem_idx<L, SW, V>(M - k, l)];
+    if (k == 0) {
+      A.y = T(0);
+      Bs.y = T(0);
+    }
+    const V B{Bs.x, -Bs.y};
+    const V W = tw_load(tw, k);
+    const V Ep = cadd(A, B);
+    const V Op = cmulc(csub(A, B), W);
+    v[e] = V{Ep.x - Op.y, Ep.y + Op.x};
+  }
+  __syncthreads();
+  line_fft<M, E, L, +1>(v, sm, stw, t, l);
+  V* dst = reinterpret_cast<V*>(u + row * NR);
+#pragma unroll
+  for (int e = 0; e < E; ++e) __stcs(dst + t + P * e, v[e]);
 }
 
 }  // namespace arena_fft

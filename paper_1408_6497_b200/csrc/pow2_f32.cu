@@ -13,4 +13,5 @@ bool pow2_fused_ok_f32(int n) {
     default: return false;
   }
 }
+cudaError_t pencil_phase_f32(const PencilArgs& a, int phase) { return pencil_phase<float>(a, phase); }
 }  // namespace arena_fft

@@ -13,4 +13,5 @@ bool pow2_fused_ok_f64(int n) {
     default: return false;
   }
 }
+cudaError_t pencil_phase_f64(const PencilArgs& a, int phase) { return pencil_phase<double>(a, phase); }
 }  // namespace arena_fft

@@ -54,14 +54,15 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // TMA descriptor of a workspace in Layout g (5-D, see k_strided_tma).
 template <typename T, int N>
-cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool ybox) {
+cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool ybox, int kc = N / 2 + 1,
+                       int kq = spec_pitch(N)) {
   using C = TmaCfg<T, N>;
   auto enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
   const CUtensorMapDataType dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  const cuuint64_t row = cuuint64_t(spec_pitch(N)) * 2 * sizeof(T);
+  const cuuint64_t row = cuuint64_t(kq) * 2 * sizeof(T);
   const int JB = 1 << g.jbs;
-  const cuuint64_t dims[5] = {cuuint64_t(2 * C::NC), cuuint64_t(JB), cuuint64_t(g.ni), cuuint64_t(g.nj / JB),
+  const cuuint64_t dims[5] = {cuuint64_t(2 * kc), cuuint64_t(JB), cuuint64_t(g.ni), cuuint64_t(g.nj / JB),
                               cuuint64_t(nchunks)};
   const cuuint64_t strides[4] = {row, row * JB, row * JB * g.ni, row * g.ni * g.nj};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
@@ -86,7 +87,8 @@ inline const vec2_t<T>* stw_ptr(const Pow2Args& a, int which, int E) {
 
 template <typename T, int N, int PASS>
 cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* spec, const Layout& g, T scale,
-                               T four_pi2) {
+                               T four_pi2, KSpan ks = KSpan{N / 2 + 1, spec_pitch(N), 0}, void* out = nullptr,
+                               const Layout* gout = nullptr) {
   using C = TmaCfg<T, N>;
   using V = vec2_t<T>;
   auto kern = k_strided_tma<T, N, PASS>;
@@ -94,11 +96,12 @@ cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* 
   if (e) return e;
   int per_sm = 1;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM))) return e;
-  const int tiles = (PASS < 2 ? g.ni : g.nj) * C::KT;
+  const int tiles = (PASS < 2 ? g.ni : g.nj) * ((ks.kc + C::L - 1) / C::L);
   int grid = a.sm_count * (per_sm > 0 ? per_sm : 1);
   if (grid > tiles) grid = tiles;
   kern<<<grid, C::THREADS, C::SMEM, a.stream>>>(map, static_cast<V*>(spec), stw_ptr<T>(a, 1, C::E), scale, four_pi2, g,
-                                               a.nchunks, a.j0);
+                                               a.nchunks, a.j0, ks, static_cast<V*>(out ? out : spec),
+                                               gout ? *gout : g);
   return cudaGetLastError();
 }
 
@@ -215,6 +218,90 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
     mark(a, mk++);
   }
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- pencil
+template <typename T, int NR>
+cudaError_t pencil_phase_n(const PencilArgs& a, int phase) {
+  using V = vec2_t<T>;
+  using CC = ContigCfg<T, NR>;
+  const int ni = NR / a.Pr, nj = NR / a.Pc, nj2 = NR / a.Pr;
+  const int nc = NR / 2 + 1;
+  const KSpan ks{imin(a.kq, nc - a.c * a.kq), a.kq, a.c * a.kq};
+  const bool has_k = ks.kc > 0;
+  const Layout gz = make_layout(ni, nj);   // rows of the rank's f block / R chunks
+  const Layout gY = make_layout(ni, nj);   // Y: j chunks of n/Pc (Pc chunks)
+  const Layout gB2 = make_layout(ni, nj2); // B2: j chunks of n/Pr (Pr chunks)
+  const Layout gC = make_layout(ni, nj2);  // C: i chunks of n/Pr, local j n/Pr (Pr chunks)
+  const T scale = T(1.0 / (double(NR) * NR * NR));
+  const T four_pi2 = T(4.0 * M_PI * M_PI);
+  Pow2Args pa{};  // carries the launch context the TMA launcher reads
+  pa.n = NR;
+  pa.stw = a.stw;
+  pa.stream = a.stream;
+  pa.sm_count = a.sm_count;
+  pa.j0 = a.r * nj2;
+  cudaError_t e;
+  if (has_k && (a.tma->specB != a.buf2 || a.tma->n != NR || a.tma->ni != ni || a.tma->nj != nj ||
+                a.tma->nchunks != a.Pc)) {
+    if ((e = encode_map<T, NR>(a.tma->maps[0], a.buf2, gY, a.Pc, true, ks.kc, ks.kq))) return e;
+    if ((e = encode_map<T, NR>(a.tma->maps[1], a.buf2, gC, a.Pr, false, ks.kc, ks.kq))) return e;
+    if ((e = encode_map<T, NR>(a.tma2->maps[0], a.buf1, gB2, a.Pr, true, ks.kc, ks.kq))) return e;
+    a.tma->specB = a.buf2;
+    a.tma->n = NR;
+    a.tma->ni = ni;
+    a.tma->nj = nj;
+    a.tma->nchunks = a.Pc;
+  }
+  const CUtensorMap& mY = *reinterpret_cast<const CUtensorMap*>(a.tma->maps[0]);
+  const CUtensorMap& mC = *reinterpret_cast<const CUtensorMap*>(a.tma->maps[1]);
+  const CUtensorMap& mB2 = *reinterpret_cast<const CUtensorMap*>(a.tma2->maps[0]);
+  const V* tw = static_cast<const V*>(a.tw);
+  const V* stwz = static_cast<const V*>(a.stw) + stw_offset(NR, 0, CC::E);
+  const unsigned zgrid = unsigned((size_t(ni) * nj) / CC::L);
+  switch (phase) {
+    case kPencilZ1:
+      if ((e = ensure_smem<k_zfwd_pencil<T, NR>>(CC::SMEM, CC::THREADS))) return e;
+      k_zfwd_pencil<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f),
+                                                                      static_cast<V*>(a.buf1), tw, stwz, gz, a.kq);
+      break;
+    case kPencilY1:  // Y (buf2) -> B2 (buf1)
+      if (!has_k) break;
+      pa.nchunks = a.Pc;
+      if ((e = launch_strided_tma<T, NR, 0>(pa, mY, a.buf2, gY, scale, four_pi2, ks, a.buf1, &gB2))) return e;
+      break;
+    case kPencilX:
+      if (!has_k) break;
+      pa.nchunks = a.Pr;
+      if ((e = launch_strided_tma<T, NR, 2>(pa, mC, a.buf2, gC, scale, four_pi2, ks))) return e;
+      break;
+    case kPencilY2:  // B2 (buf1) -> Y (buf2)
+      if (!has_k) break;
+      pa.nchunks = a.Pr;
+      if ((e = launch_strided_tma<T, NR, 1>(pa, mB2, a.buf1, gB2, scale, four_pi2, ks, a.buf2, &gY))) return e;
+      break;
+    case kPencilZ2:
+      if ((e = ensure_smem<k_zinv_pencil<T, NR>>(CC::SMEM, CC::THREADS))) return e;
+      k_zinv_pencil<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const V*>(a.buf1),
+                                                                      static_cast<T*>(a.u), tw, stwz, gz, a.kq);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t pencil_phase(const PencilArgs& a, int phase) {
+  switch (a.n) {
+    case 64: return pencil_phase_n<T, 64>(a, phase);
+    case 128: return pencil_phase_n<T, 128>(a, phase);
+    case 256: return pencil_phase_n<T, 256>(a, phase);
+    case 512: return pencil_phase_n<T, 512>(a, phase);
+    case 1024: return pencil_phase_n<T, 1024>(a, phase);
+    case 2048: return pencil_phase_n<T, 2048>(a, phase);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 // Tile geometry of each kernel (exported for the CPU index-model tests).

@@ -22,14 +22,14 @@
 namespace {
 
 template <typename T>
-__global__ void k_modes(T* __restrict__ out, int n, int i0, int ni, int nmodes, const int* __restrict__ kv,
-                        const double* __restrict__ coef, const double2* __restrict__ tw) {
-  const long long N = (long long)ni * n * n;
+__global__ void k_modes(T* __restrict__ out, int n, int i0, int ni, int j0, int nj, int nmodes,
+                        const int* __restrict__ kv, const double* __restrict__ coef, const double2* __restrict__ tw) {
+  const long long N = (long long)ni * nj * n;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
        idx += (long long)gridDim.x * blockDim.x) {
     const int k = int(idx % n);
     const long long ij = idx / n;
-    const int j = int(ij % n), i = i0 + int(ij / n);
+    const int j = j0 + int(ij % nj), i = i0 + int(ij / nj);
     double acc = 0.0;
     for (int m = 0; m < nmodes; ++m) {
       long long p = ((long long)kv[3 * m] * i + (long long)kv[3 * m + 1] * j + (long long)kv[3 * m + 2] * k) % n;
@@ -42,14 +42,14 @@ __global__ void k_modes(T* __restrict__ out, int n, int i0, int ni, int nmodes, 
 }
 
 template <typename T>
-__global__ void k_gauss(T* __restrict__ out, int n, int i0, int ni, double alpha, double cx, double cy, double cz,
-                        int which) {
-  const long long N = (long long)ni * n * n;
+__global__ void k_gauss(T* __restrict__ out, int n, int i0, int ni, int j0, int nj, double alpha, double cx, double cy,
+                        double cz, int which) {
+  const long long N = (long long)ni * nj * n;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
        idx += (long long)gridDim.x * blockDim.x) {
     const int k = int(idx % n);
     const long long ij = idx / n;
-    const int j = int(ij % n), i = i0 + int(ij / n);
+    const int j = j0 + int(ij % nj), i = i0 + int(ij / nj);
     const double x = double(i) / n, y = double(j) / n, z = double(k) / n;
     double acc = 0.0;
     for (int a = -1; a <= 1; ++a)
@@ -72,9 +72,10 @@ extern "C" {
 
 // out (device, planes i0 .. i0+ni-1 of the n^3 field, precision_bits) =
 // sum_m Re(coef_m e^{2 pi i k_m.x}); k: 3*nmodes ints, coef: 2*nmodes doubles (re, im), host arrays.
-arena_status arena_source_modes_slab(int n, int precision_bits, int nmodes, const int* k, const double* coef, int i0,
-                                     int ni, void* d_out, void* stream) {
-  if (n < 2 || nmodes < 0 || !d_out || (nmodes && (!k || !coef)) || i0 < 0 || ni < 1 || i0 + ni > n)
+arena_status arena_source_modes_block(int n, int precision_bits, int nmodes, const int* k, const double* coef, int i0,
+                                      int ni, int j0, int nj, void* d_out, void* stream) {
+  if (n < 2 || nmodes < 0 || !d_out || (nmodes && (!k || !coef)) || i0 < 0 || ni < 1 || i0 + ni > n || j0 < 0 ||
+      nj < 1 || j0 + nj > n)
     return ARENA_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   std::vector<double> tw(2 * size_t(n));
@@ -96,10 +97,10 @@ arena_status arena_source_modes_slab(int n, int precision_bits, int nmodes, cons
     cudaMemcpy(d_c, coef, sizeof(double) * 2 * nmodes, cudaMemcpyHostToDevice);
   }
   if (precision_bits == 64)
-    k_modes<double><<<148 * 16, 256, 0, s>>>(static_cast<double*>(d_out), n, i0, ni, nmodes, static_cast<int*>(d_k),
+    k_modes<double><<<148 * 16, 256, 0, s>>>(static_cast<double*>(d_out), n, i0, ni, j0, nj, nmodes, static_cast<int*>(d_k),
                                             static_cast<double*>(d_c), static_cast<double2*>(d_tw));
   else
-    k_modes<float><<<148 * 16, 256, 0, s>>>(static_cast<float*>(d_out), n, i0, ni, nmodes, static_cast<int*>(d_k),
+    k_modes<float><<<148 * 16, 256, 0, s>>>(static_cast<float*>(d_out), n, i0, ni, j0, nj, nmodes, static_cast<int*>(d_k),
                                            static_cast<double*>(d_c), static_cast<double2*>(d_tw));
   cudaError_t e = cudaGetLastError();
   cudaStreamSynchronize(s);
@@ -109,21 +110,33 @@ arena_status arena_source_modes_slab(int n, int precision_bits, int nmodes, cons
   return e == cudaSuccess ? ARENA_OK : ARENA_ECUDA;
 }
 
+arena_status arena_source_modes_slab(int n, int precision_bits, int nmodes, const int* k, const double* coef, int i0,
+                                     int ni, void* d_out, void* stream) {
+  return arena_source_modes_block(n, precision_bits, nmodes, k, coef, i0, ni, 0, n, d_out, stream);
+}
+
 arena_status arena_source_modes(int n, int precision_bits, int nmodes, const int* k, const double* coef, void* d_out,
                                 void* stream) {
-  return arena_source_modes_slab(n, precision_bits, nmodes, k, coef, 0, n, d_out, stream);
+  return arena_source_modes_block(n, precision_bits, nmodes, k, coef, 0, n, 0, n, d_out, stream);
 }
 
 // which = 0: u (periodised Gaussian), 1: f = -Lap u; planes i0 .. i0+ni-1.
-arena_status arena_source_gaussian_slab(int n, int precision_bits, double alpha, double cx, double cy, double cz,
-                                        int which, int i0, int ni, void* d_out, void* stream) {
-  if (n < 2 || !d_out || (which != 0 && which != 1) || i0 < 0 || ni < 1 || i0 + ni > n) return ARENA_EINVAL;
+arena_status arena_source_gaussian_block(int n, int precision_bits, double alpha, double cx, double cy, double cz,
+                                         int which, int i0, int ni, int j0, int nj, void* d_out, void* stream) {
+  if (n < 2 || !d_out || (which != 0 && which != 1) || i0 < 0 || ni < 1 || i0 + ni > n || j0 < 0 || nj < 1 ||
+      j0 + nj > n)
+    return ARENA_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (precision_bits == 64)
-    k_gauss<double><<<148 * 16, 256, 0, s>>>(static_cast<double*>(d_out), n, i0, ni, alpha, cx, cy, cz, which);
+    k_gauss<double><<<148 * 16, 256, 0, s>>>(static_cast<double*>(d_out), n, i0, ni, j0, nj, alpha, cx, cy, cz, which);
   else
-    k_gauss<float><<<148 * 16, 256, 0, s>>>(static_cast<float*>(d_out), n, i0, ni, alpha, cx, cy, cz, which);
+    k_gauss<float><<<148 * 16, 256, 0, s>>>(static_cast<float*>(d_out), n, i0, ni, j0, nj, alpha, cx, cy, cz, which);
   return cudaGetLastError() == cudaSuccess ? ARENA_OK : ARENA_ECUDA;
+}
+
+arena_status arena_source_gaussian_slab(int n, int precision_bits, double alpha, double cx, double cy, double cz,
+                                        int which, int i0, int ni, void* d_out, void* stream) {
+  return arena_source_gaussian_block(n, precision_bits, alpha, cx, cy, cz, which, i0, ni, 0, n, d_out, stream);
 }
 
 arena_status arena_source_gaussian(int n, int precision_bits, double alpha, double cx, double cy, double cz, int which,

@@ -160,16 +160,17 @@ CONFIG_TEXT = {
 }
 
 
-def fill_device(src, which: str, out, precision: int = 64, stream: int = 0, i0: int = 0, ni=None) -> None:
+def fill_device(src, which: str, out, precision: int = 64, stream: int = 0, i0: int = 0, ni=None, j0: int = 0,
+                nj=None) -> None:
     """Write f (which='f') or the analytic u (which='u') of `src` into device buffer `out`
-    (planes i0 .. i0+ni-1 of the n^3 field; default all)."""
+    (block i0..i0+ni-1 x j0..j0+nj-1 x all k of the n^3 field; default all)."""
     from . import source_gaussian, source_modes
 
     if isinstance(src, ModeSource):
         coef = src.f_coef() if which == "f" else src.u_coef()
-        source_modes(src.n, src.k, coef, out, precision, stream, i0, ni)
+        source_modes(src.n, src.k, coef, out, precision, stream, i0, ni, j0, nj)
     else:
-        source_gaussian(src.n, src.alpha, src.center, 1 if which == "f" else 0, out, precision, stream, i0, ni)
+        source_gaussian(src.n, src.alpha, src.center, 1 if which == "f" else 0, out, precision, stream, i0, ni, j0, nj)
 
 
 def eval_host(src, which: str) -> np.ndarray:

@@ -18,6 +18,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+
 #include <stdint.h>
 
 namespace arena_fft {
@@ -216,10 +218,20 @@ template <typename V>
 __device__ __forceinline__ V tw_load(const V* __restrict__ tw, int idx) {
   return __ldg(tw + idx);
 }
+// A twiddle table staged in shared memory (plain loads -> LDS).
+template <typename V>
+struct SmemTable {
+  const V* p;
+  __device__ __forceinline__ SmemTable operator+(int o) const { return SmemTable{p + o}; }
+};
+template <typename V>
+__device__ __forceinline__ V tw_load(SmemTable<V> tw, int idx) {
+  return tw.p[idx];
+}
 
 // Multiply by a table twiddle (forward sign) or its conjugate (backward).
-template <int S, typename V>
-__device__ __forceinline__ V tw_apply(V a, const V* __restrict__ tw, int idx) {
+template <int S, typename V, typename TW>
+__device__ __forceinline__ V tw_apply(V a, TW tw, int idx) {
   const V w = tw_load(tw, idx);
   return S < 0 ? cmul(a, w) : cmulc(a, w);
 }
@@ -237,8 +249,8 @@ constexpr int stage_tw_total(int N, int E) { return num_stages(N, E) <= 1 ? 0 : 
 
 // One Stockham stage on registers (no exchange).  Thread holds elements
 // t + P*e; butterfly q uses v[q + NB*r], r < R.
-template <int N, int E, int R, int NS, int S, typename V>
-__device__ __forceinline__ void stage_compute(V (&v)[E], int t, const V* __restrict__ stw) {
+template <int N, int E, int R, int NS, int S, typename V, typename TW>
+__device__ __forceinline__ void stage_compute(V (&v)[E], int t, TW stw) {
   constexpr int P = N / E, NB = E / R;
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
@@ -286,8 +298,8 @@ __device__ __forceinline__ void stage_exchange(V (&v)[E], V* sm, int t, int l) {
   xbarrier<SYNC>();
 }
 
-template <int N, int E, int L, int S, int SYNC, int STAGE, typename V>
-__device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, const V* __restrict__ stw, int t, int l) {
+template <int N, int E, int L, int S, int SYNC, int STAGE, typename V, typename TW>
+__device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, TW stw, int t, int l) {
   constexpr int NSTAGE = num_stages(N, E);
   if constexpr (STAGE < NSTAGE) {
     constexpr int R = 1 << stage_log2(N, E, STAGE);
@@ -303,8 +315,8 @@ __device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, const V* __restrict
 // line-l elements t + P*e (natural order).  `sm` must hold N*L elements and
 // be free (all threads past their last access) on entry; on exit it is free.
 // `stw` is the (N, E) stage-twiddle table (stage_tw_total(N, E) entries).
-template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V>
-__device__ __forceinline__ void line_fft(V (&v)[E], V* sm, const V* __restrict__ stw, int t, int l) {
+template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V, typename TW>
+__device__ __forceinline__ void line_fft(V (&v)[E], V* sm, TW stw, int t, int l) {
   fft_stages<N, E, L, S, SYNC, 0>(v, sm, stw, t, l);
 }
 

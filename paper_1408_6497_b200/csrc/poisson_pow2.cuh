@@ -366,6 +366,12 @@ namespace arena_fft {
 #ifndef ARENA_TMA_NBUF
 #define ARENA_TMA_NBUF 1  // tile buffers per CTA (prefetch distance NBUF-1)
 #endif
+#ifndef ARENA_TMA_TWSMEM_X
+#define ARENA_TMA_TWSMEM_X 1  // x pass: stage-twiddle table staged in shared memory once per CTA
+#endif                        // (B200 A/B: x 5.76 -> 5.04 ms)
+#ifndef ARENA_TMA_TWSMEM_Y
+#define ARENA_TMA_TWSMEM_Y 0  // same for the y passes
+#endif
 #ifndef ARENA_TMA_L2PF
 #define ARENA_TMA_L2PF 0  // also prefetch the tile this many iterations ahead into L2 (0: off)
 #endif
@@ -381,7 +387,10 @@ struct TmaCfg {
   static constexpr int KT = (NC + L - 1) / L;  // k tiles per line set
   static constexpr int TILE = N * L;          // elements per tile
   static constexpr int NBUF = (ARENA_TMA_NBUF * TILE * VB <= 200 * 1024) ? ARENA_TMA_NBUF : imin(2, ARENA_TMA_NBUF);
+  static constexpr int TW = stage_tw_total(N, E);  // staged twiddle entries (x pass)
   static constexpr int SMEM = NBUF * TILE * VB + 8 * NBUF;
+  static constexpr int SMEM_X = SMEM + (ARENA_TMA_TWSMEM_X ? TW * VB : 0);
+  static constexpr int SMEM_Y = SMEM + (ARENA_TMA_TWSMEM_Y ? TW * VB : 0);
 };
 
 // TMA view of a workspace in Layout g: a 5-D tensor of reals
@@ -415,8 +424,10 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
   const int KT = (ks.kc + L - 1) / L;
   const size_t kq = size_t(ks.kq);
   const int NT = (PASS < 2 ? g.ni : g.nj) * KT;
+  constexpr bool TWS = PASS == 2 ? bool(ARENA_TMA_TWSMEM_X) : bool(ARENA_TMA_TWSMEM_Y);
   V* bufs = smem_base<V>();
-  uint64_t* bar = reinterpret_cast<uint64_t*>(bufs + NBUF * TILE);
+  V* tws = bufs + NBUF * TILE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tws + (TWS ? C::TW : 0));
   const int tid = threadIdx.x;
   const int l = tid % L, t = tid / L;
 
@@ -425,7 +436,15 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
     for (int b = 0; b < NBUF; ++b) mbar_init(&bar[b], 1);
     fence_mbar_init();
   }
+  if constexpr (TWS) {
+    for (int i = tid; i < C::TW; i += blockDim.x) tws[i] = __ldg(stw + i);
+  }
   __syncthreads();
+  // x pass: LDS from the staged table; y passes: the L1 path
+  auto twp = [&]() {
+    if constexpr (TWS) return SmemTable<V>{tws};
+    else return stw;
+  }();
 
   auto issue = [&](int gt, V* dst, uint64_t* b) {
     const int outer = gt / KT, kt = gt % KT;
@@ -493,11 +512,11 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
     const int outer = gt / KT;
     const int k = (gt % KT) * L + l;
     if constexpr (PASS == 0) {
-      line_fft<N, E, L, -1>(v, cur, stw, t, l);
+      line_fft<N, E, L, -1>(v, cur, twp, t, l);
     } else if constexpr (PASS == 1) {
-      line_fft<N, E, L, +1>(v, cur, stw, t, l);
+      line_fft<N, E, L, +1>(v, cur, twp, t, l);
     } else {
-      line_fft<N, E, L, -1>(v, cur, stw, t, l);
+      line_fft<N, E, L, -1>(v, cur, twp, t, l);
       const T kj = T(signed_freq(j0 + outer, N)), kk = T(ks.k0 + k);
       const T c = kj * kj + kk * kk;
 #pragma unroll
@@ -508,7 +527,7 @@ __global__ void __launch_bounds__(TmaCfg<T, N>::THREADS, ARENA_TMA_MINB)
         v[e].x *= m;
         v[e].y *= m;
       }
-      line_fft<N, E, L, +1>(v, cur, stw, t, l);
+      line_fft<N, E, L, +1>(v, cur, twp, t, l);
     }
     if (k < ks.kc) {
       if constexpr (PASS < 2) {

@@ -92,14 +92,15 @@ cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* 
   using C = TmaCfg<T, N>;
   using V = vec2_t<T>;
   auto kern = k_strided_tma<T, N, PASS>;
-  cudaError_t e = ensure_smem<k_strided_tma<T, N, PASS>>(C::SMEM, C::THREADS);
+  constexpr int SMEM = PASS == 2 ? C::SMEM_X : C::SMEM_Y;
+  cudaError_t e = ensure_smem<k_strided_tma<T, N, PASS>>(SMEM, C::THREADS);
   if (e) return e;
   int per_sm = 1;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM))) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, SMEM))) return e;
   const int tiles = (PASS < 2 ? g.ni : g.nj) * ((ks.kc + C::L - 1) / C::L);
   int grid = a.sm_count * (per_sm > 0 ? per_sm : 1);
   if (grid > tiles) grid = tiles;
-  kern<<<grid, C::THREADS, C::SMEM, a.stream>>>(map, static_cast<V*>(spec), stw_ptr<T>(a, 1, C::E), scale, four_pi2, g,
+  kern<<<grid, C::THREADS, SMEM, a.stream>>>(map, static_cast<V*>(spec), stw_ptr<T>(a, 1, C::E), scale, four_pi2, g,
                                                a.nchunks, a.j0, ks, static_cast<V*>(out ? out : spec),
                                                gout ? *gout : g);
   return cudaGetLastError();

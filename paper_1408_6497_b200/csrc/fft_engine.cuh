@@ -298,16 +298,16 @@ __device__ __forceinline__ void stage_exchange(V (&v)[E], V* sm, int t, int l) {
   xbarrier<SYNC>();
 }
 
-template <int N, int E, int L, int S, int SYNC, int STAGE, typename V, typename TW>
+template <int N, int E, int L, int S, int SYNC, int STAGE, typename V, typename TW, int STOP = num_stages(N, E)>
 __device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, TW stw, int t, int l) {
   constexpr int NSTAGE = num_stages(N, E);
-  if constexpr (STAGE < NSTAGE) {
+  if constexpr (STAGE < STOP) {
     constexpr int R = 1 << stage_log2(N, E, STAGE);
     constexpr int NS = stage_ns(N, E, STAGE);
     constexpr int SW = stage_log2(N, E, 0);
     stage_compute<N, E, R, NS, S>(v, t, stw + (STAGE >= 1 ? stage_tw_offset(N, E, STAGE) : 0));
     if constexpr (STAGE + 1 < NSTAGE) stage_exchange<N, E, L, R, NS, SW, SYNC>(v, sm, t, l);
-    fft_stages<N, E, L, S, SYNC, STAGE + 1>(v, sm, stw, t, l);
+    fft_stages<N, E, L, S, SYNC, STAGE + 1, V, TW, STOP>(v, sm, stw, t, l);
   }
 }
 
@@ -318,6 +318,20 @@ __device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, TW stw, int t, int 
 template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V, typename TW>
 __device__ __forceinline__ void line_fft(V (&v)[E], V* sm, TW stw, int t, int l) {
   fft_stages<N, E, L, S, SYNC, 0>(v, sm, stw, t, l);
+}
+
+// The same transform split in two: `head` runs every stage but the last
+// (with all exchanges, so `sm` is free on return), `tail` the last stage,
+// in registers only.  Lets a caller refill `sm` while the tail computes.
+template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V, typename TW>
+__device__ __forceinline__ void line_fft_head(V (&v)[E], V* sm, TW stw, int t, int l) {
+  constexpr int NST = num_stages(N, E);
+  if constexpr (NST > 1) fft_stages<N, E, L, S, SYNC, 0, V, TW, NST - 1>(v, sm, stw, t, l);
+}
+template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V, typename TW>
+__device__ __forceinline__ void line_fft_tail(V (&v)[E], V* sm, TW stw, int t, int l) {
+  constexpr int NST = num_stages(N, E);
+  if constexpr (NST > 0) fft_stages<N, E, L, S, SYNC, NST - 1, V, TW, NST>(v, sm, stw, t, l);
 }
 
 // Swizzle parameter callers must use when they stage data in `sm` in the

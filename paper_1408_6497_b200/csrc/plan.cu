@@ -243,12 +243,13 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
     p->path = ARENA_PATH_POW2;
     const char* kern = std::getenv("ARENA_FFT_KERNELS");  // "classic" selects the non-TMA strided kernels
     if (!(kern && std::string(kern) == "classic")) p->tma = new (std::nothrow) TmaCache;
-    // L2-fused z+y pairs.  B200 A/B (r01): at 1024^3 the fused inverse pair ran 0.2 ms faster
-    // than K4+K5, the fused forward pair 0.3 ms slower than K1+K2, and at 512^3 both lost;
-    // default: inverse pair fused for n >= 1024.  ARENA_FFT_FUSED = 0 | fwd | inv | 1 (both).
+    // L2-fused z+y pairs (halve the DRAM traffic of K1+K2 / K4+K5).  B200 A/B (r01,
+    // final kernel configuration, 1024^3): unfused 18.7 ms, inverse pair fused 19.1,
+    // forward 19.3, both 20.5; at 512^3 fusion also lost.  Default: off.
+    // ARENA_FFT_FUSED = 0 | fwd | inv | 1 (both).
     const char* fz = std::getenv("ARENA_FFT_FUSED");
     const bool fused_ok = precision_bits == 64 ? pow2_fused_ok_f64(n) : pow2_fused_ok_f32(n);
-    int fuse = n >= 1024 ? kFuseInv : 0;
+    int fuse = 0;
     if (fz) {
       const std::string v(fz);
       fuse = v == "0" ? 0 : v == "fwd" ? kFuseFwd : v == "inv" ? kFuseInv : (kFuseFwd | kFuseInv);

@@ -17,15 +17,13 @@
 #ifndef ARENA_FUSED_LAG
 #define ARENA_FUSED_LAG 2
 #endif
-#ifndef ARENA_FUSED_MINB
-#define ARENA_FUSED_MINB 2
-#endif
+
 
 namespace arena_fft {
 
 template <typename T, int N>
 struct FusedCfg {
-  using TC = TmaCfg<T, N>;
+  using TC = TmaCfg<T, N, true>;
   static constexpr int VB = 2 * sizeof(T);
   static constexpr int THREADS = TC::THREADS;
   static constexpr int M = N / 2;
@@ -37,7 +35,9 @@ struct FusedCfg {
   static constexpr int ZSM = (M + 1) * RW;     // shared elements per warp (z items)
   static constexpr int SMEM_ELEMS = imax(TC::TILE, ZSM * WARPS);
   static constexpr int SMEM = SMEM_ELEMS * VB + 32;
-  static constexpr bool OK = THREADS == 128 && PZ <= 32 && (32 % PZ) == 0 && (N % ZROWS) == 0 && N >= 256;
+  static constexpr bool OK = (THREADS == 128 || THREADS == 256) && PZ <= 32 && (32 % PZ) == 0 &&
+                             (N % ZROWS) == 0 && N >= 256;
+  static constexpr int MINB = THREADS == 128 ? 2 : 1;  // co-resident CTAs (255 registers per thread)
 };
 
 struct FusedItem {
@@ -65,13 +65,13 @@ __host__ __device__ __forceinline__ FusedItem fused_decode(long long w, int plan
 // tiles, then z-c2r rows).  ctrs[0] = work counter, ctrs[1 + p] = finished
 // first-pass items of plane p (zeroed before the launch).
 template <typename T, int N, int DIR>
-__global__ void __launch_bounds__(FusedCfg<T, N>::THREADS, ARENA_FUSED_MINB)
+__global__ void __launch_bounds__(FusedCfg<T, N>::THREADS, FusedCfg<T, N>::MINB)
     k_zy_fused(const __grid_constant__ CUtensorMap tmap, const T* __restrict__ f, T* __restrict__ u,
                vec2_t<T>* __restrict__ S, const vec2_t<T>* __restrict__ tw, const vec2_t<T>* __restrict__ stw_z,
                const vec2_t<T>* __restrict__ stw_y, Layout g, int* __restrict__ ctrs, int lag) {
   using V = vec2_t<T>;
   using F = FusedCfg<T, N>;
-  using TC = TmaCfg<T, N>;
+  using TC = TmaCfg<T, N, true>;
   constexpr int E = TC::E, P = TC::P, L = TC::L, KT = TC::KT;
   constexpr int ncp = spec_pitch(N);
   constexpr uint32_t TILE_BYTES = TC::TILE * sizeof(V);

@@ -56,7 +56,7 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 template <typename T, int N>
 cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool ybox, int kc = N / 2 + 1,
                        int kq = spec_pitch(N)) {
-  using C = TmaCfg<T, N>;
+  constexpr int LY = TmaCfg<T, N, true>::L, LX = TmaCfg<T, N, false>::L;
   auto enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
   const CUtensorMapDataType dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -68,9 +68,9 @@ cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   cuuint32_t box[5];
   if (ybox) {
-    box[0] = 2 * C::L; box[1] = JB; box[2] = 1; box[3] = g.nj / JB; box[4] = nchunks;
+    box[0] = 2 * LY; box[1] = JB; box[2] = 1; box[3] = g.nj / JB; box[4] = nchunks;
   } else {
-    box[0] = 2 * C::L; box[1] = 1; box[2] = tma_ib(g.ni); box[3] = 1; box[4] = 1;
+    box[0] = 2 * LX; box[1] = 1; box[2] = tma_ib(g.ni); box[3] = 1; box[4] = 1;
   }
   for (int d = 1; d < 5; ++d)
     if (box[d] > 256) return cudaErrorInvalidValue;
@@ -89,7 +89,7 @@ template <typename T, int N, int PASS>
 cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* spec, const Layout& g, T scale,
                                T four_pi2, KSpan ks = KSpan{N / 2 + 1, spec_pitch(N), 0}, void* out = nullptr,
                                const Layout* gout = nullptr) {
-  using C = TmaCfg<T, N>;
+  using C = TmaCfg<T, N, (PASS < 2)>;
   using V = vec2_t<T>;
   auto kern = k_strided_tma<T, N, PASS>;
   constexpr int SMEM = PASS == 2 ? C::SMEM_X : C::SMEM_Y;
@@ -116,11 +116,11 @@ cudaError_t launch_fused(const Pow2Args& a, const CUtensorMap& map, const Layout
   if ((e = cudaMemsetAsync(a.ctrs, 0, sizeof(int) * size_t(g.ni + 1), a.stream))) return e;
   int per_sm = 1;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, F::THREADS, F::SMEM))) return e;
-  const long long items = (long long)g.ni * (N / F::ZROWS + TmaCfg<T, N>::KT);
+  const long long items = (long long)g.ni * (N / F::ZROWS + TmaCfg<T, N, true>::KT);
   long long grid = (long long)a.sm_count * (per_sm > 0 ? per_sm : 1);
   if (grid > items) grid = items;
   const V* stw_z = static_cast<const V*>(a.stw) + stw_offset(a.n, 0, F::EZ);
-  const V* stw_y = static_cast<const V*>(a.stw) + stw_offset(a.n, 1, TmaCfg<T, N>::E);
+  const V* stw_y = static_cast<const V*>(a.stw) + stw_offset(a.n, 1, TmaCfg<T, N, true>::E);
   kern<<<unsigned(grid), F::THREADS, F::SMEM, a.stream>>>(map, static_cast<const T*>(a.f), static_cast<T*>(a.u),
                                                           static_cast<V*>(a.spec), static_cast<const V*>(a.tw),
                                                           stw_z, stw_y, g, a.ctrs, a.lag);

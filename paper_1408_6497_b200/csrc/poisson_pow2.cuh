@@ -385,6 +385,9 @@ namespace arena_fft {
 #ifndef ARENA_TMA_MINB_Y
 #define ARENA_TMA_MINB_Y 1
 #endif
+#ifndef ARENA_TMA_X_TILE
+#define ARENA_TMA_X_TILE (64 * 1024)  // x-pass tile budget (bytes)
+#endif
 #ifndef ARENA_TMA_NBUF_Y
 #define ARENA_TMA_NBUF_Y ARENA_TMA_NBUF
 #endif
@@ -398,7 +401,7 @@ struct TmaCfg {
   static constexpr int VB = 2 * sizeof(T);
   static constexpr int E = imin(ARENA_TMA_E, N);
   static constexpr int P = N / E;
-  static constexpr int BUDGET = YP ? ARENA_TMA_Y_TILE : 64 * 1024;
+  static constexpr int BUDGET = YP ? ARENA_TMA_Y_TILE : ARENA_TMA_X_TILE;
   static constexpr int L = pow2_floor(imax(2, imin(8, BUDGET / (N * VB))));
   static constexpr int THREADS = L * P;
   static constexpr int NC = N / 2 + 1;

@@ -23,7 +23,7 @@ namespace arena_fft {
 
 template <typename T, int N>
 struct FusedCfg {
-  using TC = TmaCfg<T, N, true>;
+  using TC = TmaCfg<T, N, false>;  // 128-thread tiles (its own y-box TMA map)
   static constexpr int VB = 2 * sizeof(T);
   static constexpr int THREADS = TC::THREADS;
   static constexpr int M = N / 2;
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(FusedCfg<T, N>::THREADS, FusedCfg<T, N>::MINB)
                const vec2_t<T>* __restrict__ stw_y, Layout g, int* __restrict__ ctrs, int lag) {
   using V = vec2_t<T>;
   using F = FusedCfg<T, N>;
-  using TC = TmaCfg<T, N, true>;
+  using TC = TmaCfg<T, N, false>;  // 128-thread tiles (its own y-box TMA map)
   constexpr int E = TC::E, P = TC::P, L = TC::L, KT = TC::KT;
   constexpr int ncp = spec_pitch(N);
   constexpr uint32_t TILE_BYTES = TC::TILE * sizeof(V);

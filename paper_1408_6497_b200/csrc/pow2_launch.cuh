@@ -55,8 +55,9 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // TMA descriptor of a workspace in Layout g (5-D, see k_strided_tma).
 template <typename T, int N>
 cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool ybox, int kc = N / 2 + 1,
-                       int kq = spec_pitch(N)) {
-  constexpr int LY = TmaCfg<T, N, true>::L, LX = TmaCfg<T, N, false>::L;
+                       int kq = spec_pitch(N), int ly = TmaCfg<T, N, true>::L) {
+  constexpr int LX = TmaCfg<T, N, false>::L;
+  const int LY = ly;
   auto enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
   const CUtensorMapDataType dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -116,11 +117,11 @@ cudaError_t launch_fused(const Pow2Args& a, const CUtensorMap& map, const Layout
   if ((e = cudaMemsetAsync(a.ctrs, 0, sizeof(int) * size_t(g.ni + 1), a.stream))) return e;
   int per_sm = 1;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, F::THREADS, F::SMEM))) return e;
-  const long long items = (long long)g.ni * (N / F::ZROWS + TmaCfg<T, N, true>::KT);
+  const long long items = (long long)g.ni * (N / F::ZROWS + TmaCfg<T, N, false>::KT);
   long long grid = (long long)a.sm_count * (per_sm > 0 ? per_sm : 1);
   if (grid > items) grid = items;
   const V* stw_z = static_cast<const V*>(a.stw) + stw_offset(a.n, 0, F::EZ);
-  const V* stw_y = static_cast<const V*>(a.stw) + stw_offset(a.n, 1, TmaCfg<T, N, true>::E);
+  const V* stw_y = static_cast<const V*>(a.stw) + stw_offset(a.n, 1, TmaCfg<T, N, false>::E);
   kern<<<unsigned(grid), F::THREADS, F::SMEM, a.stream>>>(map, static_cast<const T*>(a.f), static_cast<T*>(a.u),
                                                           static_cast<V*>(a.spec), static_cast<const V*>(a.tw),
                                                           stw_z, stw_y, g, a.ctrs, a.lag);
@@ -158,6 +159,9 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
         c->nchunks != a.nchunks) {
       if ((e = encode_map<T, NR>(c->maps[0], a.spec, gB, a.nchunks, true))) return e;
       if ((e = encode_map<T, NR>(c->maps[1], a.specC, gC, a.nchunks, false))) return e;
+      if ((e = encode_map<T, NR>(c->maps[2], a.spec, gB, a.nchunks, true, NR / 2 + 1, spec_pitch(NR),
+                                 TmaCfg<T, NR, false>::L)))
+        return e;
       c->specB = a.spec;
       c->specC = a.specC;
       c->n = NR;
@@ -168,12 +172,13 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   }
   const CUtensorMap* my = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[0]) : nullptr;
   const CUtensorMap* mx = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[1]) : nullptr;
+  const CUtensorMap* mf = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[2]) : nullptr;
   int mk = 0;
   const bool fused = tma && a.ctrs != nullptr && FusedCfg<T, NR>::OK;
   if (fused && (a.fuse & kFuseFwd) && (a.phases & kPhaseZY)) {
     mark(a, mk++);
     if constexpr (FusedCfg<T, NR>::OK) {
-      if ((e = launch_fused<T, NR, -1>(a, *my, gB))) return e;
+      if ((e = launch_fused<T, NR, -1>(a, *mf, gB))) return e;
     }
   } else if (a.phases & kPhaseZY) {
     mark(a, mk++);
@@ -201,7 +206,7 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   if (fused && (a.fuse & kFuseInv) && (a.phases & kPhaseYZ)) {
     mark(a, mk++);
     if constexpr (FusedCfg<T, NR>::OK) {
-      if ((e = launch_fused<T, NR, +1>(a, *my, gB))) return e;
+      if ((e = launch_fused<T, NR, +1>(a, *mf, gB))) return e;
     }
     mark(a, mk++);
   } else if (a.phases & kPhaseYZ) {

@@ -72,6 +72,14 @@ struct arena_fft_plan {
   GenPlan gplan{};
   TmaCache* tma = nullptr;  // TMA descriptors (power-of-two path), nullptr = classic kernels
   int* ctrs = nullptr;      // fused z+y schedule counters (n + 1 ints), nullptr = unfused
+  // CUDA graphs of the launch sequence for small n (launch-bound), keyed by (f, u)
+  struct GraphEntry {
+    const void* f;
+    void* u;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
+  bool use_graphs = false;
   int lag = 2;
   int fuse = 0;             // kFuseFwd | kFuseInv
   int sm_count = 148;
@@ -151,6 +159,7 @@ void free_plan(arena_fft_plan* p) {
     if (p->bout[b]) cudaFree(p->bout[b]);
   }
   if (p->s_in) cudaStreamDestroy(p->s_in);
+  for (auto& ge : p->graphs) cudaGraphExecDestroy(ge.exec);
   if (p->s_out) cudaStreamDestroy(p->s_out);
   delete p->tma;
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
@@ -173,9 +182,49 @@ cudaEvent_t* timing_events(arena_fft_plan* p) {
   return ev;
 }
 
+arena_status enqueue_kernels(arena_fft_plan* p, const void* d_f, void* d_u, cudaStream_t s, cudaEvent_t* ev);
+
+// Small grids are launch-bound (five launches of a few microseconds each), so
+// their launch sequence is captured once per (f, u) into a CUDA graph and
+// replayed with one cudaGraphLaunch.  Not used with stage timing or on the
+// legacy default stream (which cannot be captured).
 arena_status enqueue_solve(arena_fft_plan* p, const void* d_f, void* d_u, cudaStream_t s) {
+  if (p->use_graphs && !p->timing && s != nullptr) {
+    for (auto& ge : p->graphs)
+      if (ge.f == d_f && ge.u == d_u) {
+        cudaError_t e = cudaGraphLaunch(ge.exec, s);
+        return e == cudaSuccess ? ARENA_OK : cuda_fail(e, "cudaGraphLaunch");
+      }
+    // first solve for this (f, u): run it eagerly (sets kernel attributes), then capture
+    arena_status st = enqueue_kernels(p, d_f, d_u, s, nullptr);
+    if (st != ARENA_OK) return st;
+    cudaStream_t cap;
+    if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) return ARENA_OK;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool ok = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      const bool launched = enqueue_kernels(p, d_f, d_u, cap, nullptr) == ARENA_OK;
+      ok = cudaStreamEndCapture(cap, &graph) == cudaSuccess && launched;
+    }
+    if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    cudaStreamDestroy(cap);
+    cudaGetLastError();  // a failed capture only means no graph: clear it
+    if (ok) {
+      if (p->graphs.size() >= 8) {
+        cudaGraphExecDestroy(p->graphs.front().exec);
+        p->graphs.erase(p->graphs.begin());
+      }
+      p->graphs.push_back({d_f, d_u, exec});
+    }
+    return ARENA_OK;
+  }
+  return enqueue_kernels(p, d_f, d_u, s, timing_events(p));
+}
+
+arena_status enqueue_kernels(arena_fft_plan* p, const void* d_f, void* d_u, cudaStream_t s, cudaEvent_t* ev) {
   cudaError_t e;
-  cudaEvent_t* ev = timing_events(p);
   if (p->path == ARENA_PATH_POW2) {
     Pow2Args a{d_f, d_u, p->spec, p->tw, p->stw, p->n, p->nc, p->ncp, s, ev, p->tma, p->sm_count,
                /*ni*/ p->n, /*nj*/ p->n, /*nchunks*/ 1, /*j0*/ 0, /*specC*/ p->spec, kPhaseAll, p->ctrs, p->lag, p->fuse};
@@ -239,6 +288,10 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
   p->nc = n / 2 + 1;
   p->ncp = (p->nc + 7) / 8 * 8;
   p->sm_count = prop.multiProcessorCount;
+  {
+    const char* gr = std::getenv("ARENA_FFT_GRAPHS");  // "0" disables graph replay
+    p->use_graphs = n <= 256 && !(gr && std::string(gr) == "0");
+  }
   if (is_pow2(n) && n <= kPow2MaxN) {
     p->path = ARENA_PATH_POW2;
     const char* kern = std::getenv("ARENA_FFT_KERNELS");  // "classic" selects the non-TMA strided kernels

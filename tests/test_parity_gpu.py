@@ -296,3 +296,27 @@ def test_pencil_loopback_1024_2x4_analytic(cuda):
     torch.cuda.synchronize()
     e = (torch.linalg.vector_norm(u - ua) / torch.linalg.vector_norm(ua)).item()
     assert e <= 1e-12, e
+
+
+def test_graph_replay_small_n(cuda):
+    """n <= 256 replays a captured CUDA graph per (f, u); results must not change
+    between the eager first call and graph replays, or after f is rewritten."""
+    torch = cuda
+    n = 64
+    p = arena.Plan(n)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        f = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, (n, n, n))).cuda()
+        u = torch.empty_like(f)
+        outs = []
+        for rep in range(3):
+            p.solve_device(f, u, s.cuda_stream)
+            outs.append(u.clone())
+        f2 = torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, (n, n, n))).cuda()
+        f.copy_(f2)
+        p.solve_device(f, u, s.cuda_stream)
+    torch.cuda.synchronize()
+    ref1 = oracle.poisson_solve(np.random.default_rng(3).uniform(-1, 1, (n, n, n)))
+    for o in outs:
+        assert _rel(o.cpu().numpy(), ref1) <= TOL64
+    assert _rel(u.cpu().numpy(), oracle.poisson_solve(f2.cpu().numpy())) <= TOL64

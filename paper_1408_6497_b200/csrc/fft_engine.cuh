@@ -214,9 +214,39 @@ __device__ __forceinline__ int smem_idx(int pos, int l) {
 // Twiddle table reads through the read-only (L1) path.  (Staging the stage
 // tables in shared memory measured no faster on B200, and a plain generic
 // load made the classic x kernel 30% slower.)
+#ifndef ARENA_TW_LD
+#define ARENA_TW_LD 1  // 0: ld.global.nc, 1: ld.global.nc.L1::evict_last (B200 A/B: -0.3 ms per solve with ST_MODE 2)
+#endif
+#ifndef ARENA_ST_MODE
+#define ARENA_ST_MODE 2  // data stores: 0 st.global.cs, 1 st.global, 2 st.global.L1::no_allocate
+#endif
+__device__ __forceinline__ double2 ldg_keep(const double2* p) {
+  double2 v;
+  asm("ld.global.nc.L1::evict_last.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float2 ldg_keep(const float2* p) {
+  float2 v;
+  asm("ld.global.nc.L1::evict_last.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
 template <typename V>
 __device__ __forceinline__ V tw_load(const V* __restrict__ tw, int idx) {
-  return __ldg(tw + idx);
+  if constexpr (ARENA_TW_LD == 1) return ldg_keep(tw + idx);
+  else return __ldg(tw + idx);
+}
+// Streaming store of a result element (write-once data: keep it out of L1).
+__device__ __forceinline__ void st_na(double2* p, double2 v) {
+  asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_na(float2* p, float2 v) {
+  asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+template <typename V>
+__device__ __forceinline__ void st_out(V* p, V v) {
+  if constexpr (ARENA_ST_MODE == 0) __stcs(p, v);
+  else if constexpr (ARENA_ST_MODE == 1) *p = v;
+  else st_na(p, v);
 }
 // A twiddle table staged in shared memory (plain loads -> LDS).
 template <typename V>

@@ -12,7 +12,8 @@ constexpr int kPow2Launches = 5;
 // Plan-owned cache of the TMA descriptors over the half-spectrum workspaces
 // (encoded on first use; they depend only on the buffers and the geometry).
 struct alignas(64) TmaCache {
-  unsigned char maps[3][128];  // CUtensorMap: y boxes over B, x boxes over C, fused-kernel y boxes over B
+  unsigned char maps[4][128];  // CUtensorMap: y boxes over B, x boxes over C, fused-kernel y boxes over B,
+                              // half-row y boxes over B (k_ystream)
   const void* specB = nullptr;
   const void* specC = nullptr;
   int n = 0, ni = 0, nj = 0, nchunks = 0;

@@ -138,16 +138,19 @@ inline Layout make_layout(int ni, int nj) {
 // The Poisson symbol of fft_solver.cpp:66-79, k2 == 0 ? 0 : scale / (four_pi2 * k2),
 // with the division done as a hardware reciprocal estimate refined by Newton
 // steps (no slow path / divergence); within 2 ulp of the IEEE quotient.
+#ifndef ARENA_RCP_NEWTON
+#define ARENA_RCP_NEWTON 2
+#endif
 __device__ __forceinline__ double poisson_symbol(double k2, double scale, double four_pi2) {
   const double d = four_pi2 * k2;
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  double e = fma(-d, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-d, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-d, r, 1.0);
-  r = fma(r, e, r);
+  // MUFU.RCP64H is good to ~2^-20; each Newton step squares the relative error.
+#pragma unroll
+  for (int it = 0; it < ARENA_RCP_NEWTON; ++it) {
+    const double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+  }
   return k2 == 0.0 ? 0.0 : scale * r;
 }
 __device__ __forceinline__ float poisson_symbol(float k2, float scale, float four_pi2) {
@@ -264,7 +267,7 @@ __device__ __forceinline__ void zinv_rows(const vec2_t<T>* __restrict__ S, T* __
   line_fft<M, E, L, +1, SYNC>(v, sm, stw, t, l);
   V* dst = reinterpret_cast<V*>(u + row * NR);
 #pragma unroll
-  for (int e = 0; e < E; ++e) __stcs(dst + t + P * e, v[e]);
+  for (int e = 0; e < E; ++e) st_out(dst + t + P * e, v[e]);
 }
 
 template <typename T, int NR>
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(StridedCfg<T, N, 0>::THREADS, ARENA_STRIDED_MI
   line_fft<N, E, L, S>(v, sm, stw, t, l);
   if (valid) {
 #pragma unroll
-    for (int e = 0; e < E; ++e) __stcs(base + rowB(g, i, t + P * e) * ncp, v[e]);
+    for (int e = 0; e < E; ++e) st_out(base + rowB(g, i, t + P * e) * ncp, v[e]);
   }
 }
 
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(StridedCfg<T, N, 1>::THREADS, ARENA_STRIDED_MI
   line_fft<N, E, L, +1>(v, sm, stw, t, l);
   if (valid) {
 #pragma unroll
-    for (int e = 0; e < E; ++e) __stcs(base + size_t(t + P * e) * istride, v[e]);
+    for (int e = 0; e < E; ++e) st_out(base + size_t(t + P * e) * istride, v[e]);
   }
 }
 
@@ -582,10 +585,10 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2)>::THREADS, PASS == 2 ?
     if (k < ks.kc) {
       if constexpr (PASS < 2) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) __stcs(out + rowB(gout, outer, t + P * e) * kq + k, v[e]);
+        for (int e = 0; e < E; ++e) st_out(out + rowB(gout, outer, t + P * e) * kq + k, v[e]);
       } else {
 #pragma unroll
-        for (int e = 0; e < E; ++e) __stcs(spec + rowC(g, t + P * e, outer) * kq + k, v[e]);
+        for (int e = 0; e < E; ++e) st_out(spec + rowC(g, t + P * e, outer) * kq + k, v[e]);
       }
     }
     // No barrier needed here: every thread's last access to `cur` (the tile
@@ -687,7 +690,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
   line_fft<M, E, L, +1>(v, sm, stw, t, l);
   V* dst = reinterpret_cast<V*>(u + row * NR);
 #pragma unroll
-  for (int e = 0; e < E; ++e) __stcs(dst + t + P * e, v[e]);
+  for (int e = 0; e < E; ++e) st_out(dst + t + P * e, v[e]);
 }
 
 }  // namespace arena_fft

@@ -9,6 +9,7 @@
 
 #include "launchers.h"
 #include "poisson_fused.cuh"
+#include "poisson_ystream.cuh"
 
 namespace arena_fft {
 
@@ -52,6 +53,9 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+#ifndef ARENA_TMA_PROMO
+#define ARENA_TMA_PROMO 0  // L2 promotion of the TMA boxes: 0 none, 1 64B, 2 128B, 3 256B
+#endif
 // TMA descriptor of a workspace in Layout g (5-D, see k_strided_tma).
 template <typename T, int N>
 cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool ybox, int kc = N / 2 + 1,
@@ -75,9 +79,12 @@ cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool
   }
   for (int d = 1; d < 5; ++d)
     if (box[d] > 256) return cudaErrorInvalidValue;
+  const CUtensorMapL2promotion promo = ARENA_TMA_PROMO == 1   ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                       : ARENA_TMA_PROMO == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                       : ARENA_TMA_PROMO == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                              : CU_TENSOR_MAP_L2_PROMOTION_NONE;
   CUresult r = enc(reinterpret_cast<CUtensorMap*>(out), dt, 5, spec, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
@@ -105,6 +112,27 @@ cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* 
                                                a.nchunks, a.j0, ks, static_cast<V*>(out ? out : spec),
                                                gout ? *gout : g);
   return cudaGetLastError();
+}
+
+template <typename T, int N, int PASS>
+cudaError_t launch_ystream(const Pow2Args& a, const CUtensorMap& map, const Layout& g, KSpan ks, void* out,
+                           const Layout& gout) {
+  using C = YsCfg<T, N>;
+  using V = vec2_t<T>;
+  if constexpr (!C::OK) {
+    return cudaErrorNotSupported;
+  } else {
+    auto kern = k_ystream<T, N, PASS>;
+    cudaError_t e = ensure_smem<k_ystream<T, N, PASS>>(C::SMEM, C::THREADS);
+    if (e) return e;
+    int per_sm = 1;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM))) return e;
+    const int tiles = g.ni * ((ks.kc + C::L - 1) / C::L);
+    int grid = a.sm_count * (per_sm > 0 ? per_sm : 1);
+    if (grid > tiles) grid = tiles;
+    kern<<<grid, C::THREADS, C::SMEM, a.stream>>>(map, stw_ptr<T>(a, 1, C::E), g, ks, static_cast<V*>(out), gout);
+    return cudaGetLastError();
+  }
 }
 
 template <typename T, int N, int DIR>
@@ -162,6 +190,11 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
       if ((e = encode_map<T, NR>(c->maps[2], a.spec, gB, a.nchunks, true, NR / 2 + 1, spec_pitch(NR),
                                  TmaCfg<T, NR, false>::L)))
         return e;
+      if constexpr (ARENA_YSTREAM && YsCfg<T, NR>::OK) {
+        if ((e = encode_map<T, NR>(c->maps[3], a.spec, gB, a.nchunks, true, NR / 2 + 1, spec_pitch(NR),
+                                   YsCfg<T, NR>::LH)))
+          return e;
+      }
       c->specB = a.spec;
       c->specC = a.specC;
       c->n = NR;
@@ -173,6 +206,9 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   const CUtensorMap* my = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[0]) : nullptr;
   const CUtensorMap* mx = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[1]) : nullptr;
   const CUtensorMap* mf = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[2]) : nullptr;
+  const CUtensorMap* mys = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[3]) : nullptr;
+  constexpr bool ys = ARENA_YSTREAM && YsCfg<T, NR>::OK;
+  const KSpan kfull{NR / 2 + 1, spec_pitch(NR), 0};
   int mk = 0;
   const bool fused = tma && a.ctrs != nullptr && FusedCfg<T, NR>::OK;
   if (fused && (a.fuse & kFuseFwd) && (a.phases & kPhaseZY)) {
@@ -186,7 +222,9 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
                                                                stw_ptr<T>(a, 0, CC::E), gB);
     mark(a, mk++);
     if (tma) {
-      if ((e = launch_strided_tma<T, NR, 0>(a, *my, a.spec, gB, scale, four_pi2))) return e;
+      if constexpr (ys) e = launch_ystream<T, NR, 0>(a, *mys, gB, kfull, a.spec, gB);
+      else e = launch_strided_tma<T, NR, 0>(a, *my, a.spec, gB, scale, four_pi2);
+      if (e) return e;
     } else {
       if ((e = ensure_smem<k_ypass<T, NR, -1>>(SC::SMEM, SC::THREADS))) return e;
       k_ypass<T, NR, -1><<<dim3((a.nc + SC::L - 1) / SC::L, NR), SC::THREADS, SC::SMEM, a.stream>>>(
@@ -212,7 +250,9 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   } else if (a.phases & kPhaseYZ) {
     mark(a, mk++);
     if (tma) {
-      if ((e = launch_strided_tma<T, NR, 1>(a, *my, a.spec, gB, scale, four_pi2))) return e;
+      if constexpr (ys) e = launch_ystream<T, NR, 1>(a, *mys, gB, kfull, a.spec, gB);
+      else e = launch_strided_tma<T, NR, 1>(a, *my, a.spec, gB, scale, four_pi2);
+      if (e) return e;
     } else {
       if ((e = ensure_smem<k_ypass<T, NR, +1>>(SC::SMEM, SC::THREADS))) return e;
       k_ypass<T, NR, +1><<<dim3((a.nc + SC::L - 1) / SC::L, NR), SC::THREADS, SC::SMEM, a.stream>>>(

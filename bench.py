@@ -46,6 +46,8 @@ def _args():
     ap.add_argument("--slab", action="store_true", help="use the slab (NCCL) path even with one rank")
     ap.add_argument("--decomp", default="slab", choices=("slab", "pencil"), help="multi-GPU decomposition")
     ap.add_argument("--pgrid", default=None, help="pencil process grid RxC (default: near-square, R <= C)")
+    ap.add_argument("--xchg", default="peer", choices=("peer", "nccl"),
+                    help="slab exchange: peer = fused into K2/K3 as NVLink stores (CUDA IPC), nccl = send/recv")
     return ap.parse_args()
 
 
@@ -399,16 +401,76 @@ def run_slab(args, rank, world, local):
     f = f64 if prec == 64 else f64.float()
     u = torch.empty_like(f)
 
-    nb = arena.lib.arena_nccl_unique_id_bytes()
-    idt = torch.zeros(nb, dtype=torch.uint8, device="cuda")
-    if rank == 0:
-        idt.copy_(torch.frombuffer(bytearray(arena.nccl_unique_id()), dtype=torch.uint8))
-    dist.broadcast(idt, 0)
-    nid = bytes(idt.cpu().numpy().tobytes())
-    if pencil:
-        slab = arena.Pencil(n, pr, pc, rank=rank, nccl_id=nid, precision=prec, device=local)
-    else:
-        slab = arena.Slab(n, world, rank=rank, nccl_id=nid, precision=prec, device=local)
+    ua = torch.empty((ni, nj, n), dtype=torch.float64, device="cuda")
+    problems.fill_device(src, "u", ua, 64, sh, i0, ni, j0, nj)
+
+    def rel_vs_analytic():
+        sums = torch.stack([ua.sum()])
+        dist.all_reduce(sums)
+        mean_u = sums[0].item() / float(n) ** 3
+        d2 = torch.stack([((u.double() - (ua - mean_u)) ** 2).sum(), ((ua - mean_u) ** 2).sum()])
+        dist.all_reduce(d2)
+        return (d2[0] / d2[1]).sqrt().item()
+
+    def make_nccl():
+        nb = arena.lib.arena_nccl_unique_id_bytes()
+        idt = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(arena.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid = bytes(idt.cpu().numpy().tobytes())
+        if pencil:
+            return arena.Pencil(n, pr, pc, rank=rank, nccl_id=nid, precision=prec, device=local)
+        return arena.Slab(n, world, rank=rank, nccl_id=nid, precision=prec, device=local)
+
+    def vote(ok):  # every rank takes the same branch
+        t = torch.tensor([1 if ok else 0], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return t.item() == 1
+
+    def try_peer():
+        nb = arena.lib.arena_slab_peer_handle_bytes()
+        s, err = None, None
+        try:
+            s = arena.Slab(n, world, rank=rank, peer=True, precision=prec, device=local)
+            hb = s.peer_handles()
+        except Exception as exc:
+            err, hb = exc, bytes(nb)
+        h = torch.frombuffer(bytearray(hb), dtype=torch.uint8).cuda()
+        hs = [torch.empty_like(h) for _ in range(world)]
+        dist.all_gather(hs, h)
+        if not vote(err is None):
+            return None, err or "another rank failed to export"
+        try:
+            s.peer_attach(b"".join(bytes(x.cpu().numpy().tobytes()) for x in hs))
+        except Exception as exc:
+            err = exc
+        if not vote(err is None):
+            return None, err or "another rank failed to attach"
+        try:
+            for _ in range(max(1, args.warmup)):
+                s.solve_device(f, u, sh)
+            torch.cuda.synchronize()
+            s.barrier_status()
+        except Exception as exc:
+            err = exc
+        if not vote(err is None):
+            return None, err or "another rank failed"
+        r = rel_vs_analytic()
+        if not r <= (1e-12 if prec == 64 else 1e-5):
+            return None, f"parity {r:.2e}"
+        return s, None
+
+    xchg = "nccl" if pencil else args.xchg
+    note = None
+    slab = None
+    if xchg == "peer":
+        slab, err = try_peer()
+        if slab is None:  # fall back to the NCCL exchange, and say so
+            note = f"peer exchange unavailable ({err}); NCCL used"
+            xchg = "nccl"
+    if slab is None:
+        slab = make_nccl()
 
     for _ in range(args.warmup):
         slab.solve_device(f, u, sh)
@@ -428,15 +490,9 @@ def run_slab(args, rank, world, local):
     ms_step = t.item() / args.steps
     value = n ** 3 / (ms_step / 1e3)
 
-    ua = torch.empty((ni, nj, n), dtype=torch.float64, device="cuda")
-    problems.fill_device(src, "u", ua, 64, sh, i0, ni, j0, nj)
-    sums = torch.stack([ua.sum(), ((u.double() - ua) ** 2).sum(), (ua ** 2).sum()])
-    dist.all_reduce(sums)
-    mean_u = sums[0].item() / float(n) ** 3
-    # ||u - (ua - mean)||^2 = sum (u-ua)^2 + 2 mean sum(u-ua) + N mean^2 ; recompute directly per rank
-    d2 = torch.stack([((u.double() - (ua - mean_u)) ** 2).sum(), ((ua - mean_u) ** 2).sum()])
-    dist.all_reduce(d2)
-    rel_an = (d2[0] / d2[1]).sqrt().item()
+    if xchg == "peer":
+        slab.barrier_status()
+    rel_an = rel_vs_analytic()
 
     peak, peak_kind = _peaks()
     _, b_solve = algorithmic_bytes(n, elem)
@@ -477,7 +533,11 @@ def run_slab(args, rank, world, local):
             "vs_baseline": None, "dtype": "f64" if prec == 64 else "f32", "data": "synthetic",
             "config": {"workload": f"C{args.config}: {problems.CONFIG_TEXT[args.config]}", "n": n, "precision": prec,
                        "decomposition": (f"pencil {pr}x{pc}, NCCL row/column all-to-alls (4 per solve)" if pencil
-                                         else f"slab x{world} over i, NCCL grouped send/recv all-to-all"),
+                                         else f"slab x{world} over i, " + (
+                                             "all-to-alls fused into K2/K3 as stores into the peers' "
+                                             "workspaces (CUDA IPC over NVLink) + device flag barriers"
+                                             if xchg == "peer" else "NCCL grouped send/recv all-to-all")),
+                       "exchange": xchg, "exchange_note": note,
                        "l2": "inputs larger than L2, no flush"},
             "roofline": {"bound": "hbm+nvlink", "achieved": hbm_per_gpu / (ms_step / 1e3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": t_roof / (ms_step / 1e3), "traffic": None, "peak_kind": peak_kind,

@@ -136,6 +136,32 @@ int arena_slab_launches_per_solve(const arena_fft_slab* slab);
 /* d_f, d_u: this rank's slab (loopback: the full field); asynchronous on stream. */
 arena_status arena_slab_solve_device(arena_fft_slab* slab, const void* d_f, void* d_u, void* stream);
 
+/* Exchange modes.  COPY: K2 / K3 work in place and the all-to-alls are NCCL
+ * grouped send/recv (loopback: device copies).  PEER: the ranks' workspaces are
+ * mapped into each other's address space (CUDA IPC over NVLink / NVSwitch) and
+ * K2 / K3 store every output chunk straight into the owning rank's workspace —
+ * the all-to-all is fused into the transform; a device-side flag barrier
+ * (release / acquire, system scope) separates the phases.  Not in the reference
+ * code (its FFT is single-process); the paper's distributed solve. */
+enum { ARENA_XCHG_COPY = 0, ARENA_XCHG_PEER = 1 };
+/* One rank of a peer-exchange slab (no NCCL).  Before solving: export this
+ * rank's handles, gather every rank's (rank order) out of band, attach. */
+arena_status arena_slab_create_peer(arena_fft_slab** slab, int n, int precision_bits, int device, int nranks, int rank);
+int arena_slab_peer_handle_bytes(void);
+arena_status arena_slab_peer_export(arena_fft_slab* slab, void* out, int len);
+arena_status arena_slab_peer_attach(arena_fft_slab* slab, const void* all_handles, int len);
+/* Switch the exchange of a loopback slab (or an attached NCCL slab). */
+arena_status arena_slab_set_exchange(arena_fft_slab* slab, int mode);
+/* Phase p in {0, 1, 2} of a solve (K1+K2, K3, K4+K5, with the COPY exchanges
+ * after phases 0 and 1).  In PEER mode the caller must synchronise all ranks
+ * between phases (arena_slab_solve_device does it on the device). */
+arena_status arena_slab_solve_phase(arena_fft_slab* slab, int phase, const void* d_f, void* d_u, void* stream);
+/* ARENA_OK, or ARENA_ECUDA if a device barrier gave up waiting (20 s). */
+arena_status arena_slab_barrier_status(arena_fft_slab* slab);
+/* Check the peer barrier protocol on one device: one cooperative launch, block r
+ * plays rank r for `rounds` barriers; *bad = visibility violations seen (0). */
+arena_status arena_peer_barrier_selftest(int device, int nranks, int rounds, int* bad);
+
 /* ---- Pencil decomposition over Pr x Pc GPUs (BASELINE config 5) --------------
  * Rank r*Pc + c owns the f / u block i in [r n/Pr, (r+1) n/Pr), j in
  * [c n/Pc, (c+1) n/Pc), all k, stored contiguously as (n/Pr) x (n/Pc) x n.

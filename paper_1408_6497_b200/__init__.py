@@ -78,6 +78,14 @@ _sig = {
     "arena_slab_info": (_i, [_vp, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(ctypes.c_size_t),
                              ctypes.POINTER(ctypes.c_size_t)]),
     "arena_slab_solve_device": (_i, [_vp, _vp, _vp, _vp]),
+    "arena_slab_create_peer": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _i, _i]),
+    "arena_slab_peer_handle_bytes": (_i, []),
+    "arena_slab_peer_export": (_i, [_vp, _vp, _i]),
+    "arena_slab_peer_attach": (_i, [_vp, _vp, _i]),
+    "arena_slab_set_exchange": (_i, [_vp, _i]),
+    "arena_slab_solve_phase": (_i, [_vp, _i, _vp, _vp, _vp]),
+    "arena_slab_barrier_status": (_i, [_vp]),
+    "arena_peer_barrier_selftest": (_i, [_i, _i, _i, ctypes.POINTER(_i)]),
     "arena_pow2_kernel_geometry": (_i, [_i, _i, ctypes.POINTER(_i)]),
     "arena_pencil_create": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _i, _i, _i, _vp]),
     "arena_pencil_create_loopback": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _i, _i]),
@@ -206,19 +214,29 @@ class Plan:
         return {names[i].decode(): ms[i] for i in range(ns.value)}, nsol.value
 
 
+XCHG_COPY, XCHG_PEER = 0, 1
+
+
 class Slab:
     """Slab decomposition over P ranks (include/arena_fft.h, arena_slab_*).
 
-    Slab(n, P, rank=r, nccl_id=bytes) — one rank of a multi-GPU solve (NCCL);
-    Slab(n, P, loopback=True)         — P virtual ranks on one device (testing).
+    Slab(n, P, rank=r, nccl_id=bytes) — one rank of a multi-GPU solve (NCCL all-to-alls);
+    Slab(n, P, rank=r, peer=True)     — one rank, exchange fused into K2 / K3 as stores
+                                        into the peers' workspaces (CUDA IPC); call
+                                        peer_attach(all ranks' peer_handles()) first;
+    Slab(n, P, loopback=True)         — P virtual ranks on one device (testing);
+                                        set_exchange(XCHG_PEER) for the peer-store kernels.
     """
 
     def __init__(self, n: int, nranks: int, rank: int = 0, nccl_id: Optional[bytes] = None,
-                 precision: int = 64, device: int = -1, loopback: bool = False):
+                 precision: int = 64, device: int = -1, loopback: bool = False, peer: bool = False):
         self._s = _vp()
         if loopback:
             _check(lib.arena_slab_create_loopback(ctypes.byref(self._s), int(n), int(precision), int(device),
                                                   int(nranks)), "arena_slab_create_loopback")
+        elif peer:
+            _check(lib.arena_slab_create_peer(ctypes.byref(self._s), int(n), int(precision), int(device),
+                                              int(nranks), int(rank)), "arena_slab_create_peer")
         else:
             if nccl_id is None:
                 raise ValueError("nccl_id required (see nccl_unique_id())")
@@ -241,6 +259,30 @@ class Slab:
             stream = torch.cuda.current_stream(f.device).cuda_stream
         _check(lib.arena_slab_solve_device(self._s, _vp(_ptr(f)), _vp(_ptr(u)), _vp(stream)),
                "arena_slab_solve_device")
+
+    def solve_phase(self, phase: int, f, u, stream: Optional[int] = None) -> None:
+        """Phase 0 (K1+K2), 1 (K3) or 2 (K4+K5); peer mode: synchronise the ranks in between."""
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(f.device).cuda_stream
+        _check(lib.arena_slab_solve_phase(self._s, int(phase), _vp(_ptr(f)), _vp(_ptr(u)), _vp(stream)),
+               "arena_slab_solve_phase")
+
+    def peer_handles(self) -> bytes:
+        nb = lib.arena_slab_peer_handle_bytes()
+        buf = ctypes.create_string_buffer(nb)
+        _check(lib.arena_slab_peer_export(self._s, buf, nb), "arena_slab_peer_export")
+        return buf.raw
+
+    def peer_attach(self, all_handles: bytes) -> None:
+        buf = ctypes.create_string_buffer(bytes(all_handles), len(all_handles))
+        _check(lib.arena_slab_peer_attach(self._s, buf, len(all_handles)), "arena_slab_peer_attach")
+
+    def set_exchange(self, mode: int) -> None:
+        _check(lib.arena_slab_set_exchange(self._s, int(mode)), "arena_slab_set_exchange")
+
+    def barrier_status(self) -> None:
+        _check(lib.arena_slab_barrier_status(self._s), "arena_slab_barrier_status")
 
     def close(self) -> None:
         if getattr(self, "_s", None) and self._s.value:

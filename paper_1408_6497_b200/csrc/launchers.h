@@ -7,6 +7,7 @@
 namespace arena_fft {
 
 constexpr int kPow2MaxN = 2048;
+constexpr int kMaxPeers = 8;  // ranks a slab solve can scatter to directly (peer-mapped workspaces)
 constexpr int kPow2Launches = 5;
 
 // Plan-owned cache of the TMA descriptors over the half-spectrum workspaces
@@ -50,6 +51,11 @@ struct Pow2Args {
   int* ctrs;     // fused z+y passes: device counters (ni + 1 ints); nullptr = unfused kernels
   int lag;       // fused schedule lag in planes
   int fuse;      // kFuseFwd | kFuseInv: which z+y pairs run fused (needs ctrs)
+  // Slab with peer-mapped workspaces: K2 / K3 store chunk c straight into
+  // peer_y[c] / peer_x[c] (rank c's C / B, advanced to this rank's chunk);
+  // nullptr = in-place (the exchange is a separate step).
+  void* const* peer_y = nullptr;
+  void* const* peer_x = nullptr;
 };
 enum : int { kFuseFwd = 1, kFuseInv = 2 };
 

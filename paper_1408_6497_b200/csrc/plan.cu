@@ -639,7 +639,71 @@ struct SlabRank {
   void* C = nullptr;  // workspace C: n * nj rows
   int* ctrs = nullptr;  // fused z+y counters (ni + 1), nullptr = unfused
   TmaCache tma;
+  // Peer exchange: rank d's C / B advanced to this rank's chunk (K2 / K3 store there).
+  void* peerC[kMaxPeers] = {};
+  void* peerB[kMaxPeers] = {};
 };
+
+// Barrier flags of the peer exchange: flags[d] of rank r = last epoch rank d
+// announced to r (written by d over NVLink).
+struct PeerFlags {
+  unsigned* peer[kMaxPeers];  // rank d's flag array
+  unsigned* mine;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Every rank announces `epoch` to every rank (release, system scope: the
+// rank's earlier peer stores — previous kernels on the stream — become visible
+// first), then waits until every rank has announced it (acquire).  Gives up
+// after 20 s and sets *err instead of hanging the GPU.
+__device__ void peer_barrier_body(const PeerFlags& pf, int rank, int P, unsigned epoch, int* err) {
+  const int d = threadIdx.x;
+  if (d < P) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pf.peer[d] + rank), "r"(epoch) : "memory");
+    const unsigned long long t0 = globaltimer_ns();
+    for (;;) {
+      unsigned v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(pf.mine + d) : "memory");
+      if (int(v - epoch) >= 0) break;
+      if (globaltimer_ns() - t0 > 20000000000ull) {
+        atomicExch(err, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void k_peer_barrier(const __grid_constant__ PeerFlags pf, int rank, int P, unsigned epoch, int* err) {
+  peer_barrier_body(pf, rank, P, epoch, err);
+}
+
+// Protocol self-test on ONE device: block r plays rank r (one cooperative
+// launch, so all blocks are co-resident).  Each round every block publishes
+// data[r] = round, passes the barrier, and checks it sees every block's value.
+__global__ void k_peer_barrier_selftest(unsigned* flags, volatile int* data, int P, int rounds, int* err, int* bad) {
+  const int r = blockIdx.x;
+  PeerFlags pf;
+  for (int d = 0; d < kMaxPeers; ++d) pf.peer[d] = flags + size_t(d < P ? d : 0) * P;
+  pf.mine = flags + size_t(r) * P;
+  for (int e = 1; e <= rounds; ++e) {
+    if (threadIdx.x == 0) {
+      __nanosleep(unsigned(r * 7919 + e * 104729) % 4000u);
+      data[r] = e;
+    }
+    __syncthreads();
+    peer_barrier_body(pf, r, P, unsigned(e), err);
+    if (threadIdx.x < P && data[threadIdx.x] < e) atomicAdd(bad, 1);
+    __syncthreads();
+  }
+}
 
 }  // namespace
 
@@ -651,6 +715,13 @@ struct arena_fft_slab {
   size_t ws_bytes = 0;     // bytes of one workspace (B or C)
   std::vector<SlabRank> ranks;  // loopback: P virtual ranks; NCCL: this rank only
   ncclComm_t comm = nullptr;
+  int xmode = ARENA_XCHG_COPY;  // ARENA_XCHG_PEER: K2 / K3 store into the peers' workspaces
+  bool attached = false;        // peer pointers of the other ranks opened (multi-process)
+  unsigned* flags = nullptr;    // this rank's barrier flags (P)
+  PeerFlags pflags{};
+  int* err = nullptr;           // barrier timeout flag
+  unsigned epoch = 0;
+  std::vector<void*> opened;    // IPC mappings to close
 };
 
 namespace {
@@ -659,6 +730,9 @@ void free_slab(arena_fft_slab* s) {
   if (!s) return;
   if (s->base) {
     DeviceGuard g(s->base->device);
+    for (void* p : s->opened) cudaIpcCloseMemHandle(p);
+    if (s->flags) cudaFree(s->flags);
+    if (s->err) cudaFree(s->err);
     for (SlabRank& r : s->ranks) {
       if (r.B) cudaFree(r.B);
       if (r.C) cudaFree(r.C);
@@ -712,7 +786,16 @@ arena_status slab_init(arena_fft_slab** out, int n, int prec, int device, int P,
       return fail(ARENA_ENOMEM, "slab counters");
     }
   }
-  if (!loopback) {
+  {
+    cudaError_t e;
+    if ((e = cudaMalloc(&s->flags, sizeof(unsigned) * size_t(P))) != cudaSuccess ||
+        (e = cudaMemset(s->flags, 0, sizeof(unsigned) * size_t(P))) != cudaSuccess ||
+        (e = cudaMalloc(&s->err, sizeof(int))) != cudaSuccess || (e = cudaMemset(s->err, 0, sizeof(int))) != cudaSuccess) {
+      free_slab(s);
+      return fail(ARENA_ENOMEM, "slab barrier flags: " + std::string(cudaGetErrorString(e)));
+    }
+  }
+  if (!loopback && id) {
     NcclApi* a = nccl_api();
     if (!a) {
       free_slab(s);
@@ -738,8 +821,29 @@ Pow2Args slab_args(arena_fft_slab* s, SlabRank& r, int rank, const void* f, void
 }
 
 cudaError_t slab_phase(arena_fft_slab* s, SlabRank& r, int rank, const void* f, void* u, cudaStream_t st, int phases) {
-  const Pow2Args a = slab_args(s, r, rank, f, u, st, phases);
+  Pow2Args a = slab_args(s, r, rank, f, u, st, phases);
+  if (s->xmode == ARENA_XCHG_PEER) {
+    a.peer_y = r.peerC;
+    a.peer_x = r.peerB;
+  }
   return s->base->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
+}
+
+// Loopback ranks in peer mode: rank v's tables point at the virtual ranks' buffers.
+void slab_fill_loopback_peers(arena_fft_slab* s) {
+  const size_t cb = s->chunk_elems * s->base->elem;
+  for (int v = 0; v < s->P; ++v)
+    for (int d = 0; d < s->P; ++d) {
+      s->ranks[v].peerC[d] = static_cast<char*>(s->ranks[d].C) + size_t(v) * cb;
+      s->ranks[v].peerB[d] = static_cast<char*>(s->ranks[d].B) + size_t(v) * cb;
+    }
+}
+
+arena_status slab_peer_barrier(arena_fft_slab* s, cudaStream_t st) {
+  ++s->epoch;
+  k_peer_barrier<<<1, 32, 0, st>>>(s->pflags, s->rank, s->P, s->epoch, s->err);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ARENA_OK : cuda_fail(e, "peer barrier");
 }
 
 // All-to-all between workspaces: forward (B chunk d of rank r -> C chunk r of rank d)
@@ -802,7 +906,11 @@ arena_status arena_slab_create_loopback(arena_fft_slab** out, int n, int precisi
 
 void arena_slab_destroy(arena_fft_slab* s) { free_slab(s); }
 
-int arena_slab_launches_per_solve(const arena_fft_slab* s) { return s ? s->base->launches() : 0; }
+int arena_slab_launches_per_solve(const arena_fft_slab* s) {
+  if (!s) return 0;
+  const bool barrier = s->xmode == ARENA_XCHG_PEER && !s->loopback && s->P > 1;
+  return s->base->launches() * int(s->ranks.size()) + (barrier ? 2 : 0);
+}
 
 arena_status arena_slab_info(const arena_fft_slab* s, int* ni, int* nj, size_t* chunk_bytes, size_t* workspace_bytes) {
   if (!s) return fail(ARENA_EINVAL, "slab is NULL");
@@ -813,33 +921,157 @@ arena_status arena_slab_info(const arena_fft_slab* s, int* ni, int* nj, size_t* 
   return ARENA_OK;
 }
 
+// One third of a slab solve.  Phase 0: K1, K2 (+ exchange #1 unless the
+// exchange is K2's own peer stores); 1: K3 (+ exchange #2); 2: K4, K5.  In peer
+// mode every rank must have finished phase p before any rank starts phase p+1
+// (arena_slab_solve_device inserts a device barrier; a caller driving the
+// phases itself synchronises the ranks between them).
+static arena_status slab_run_phase(arena_fft_slab* s, int phase, const void* d_f, void* d_u, cudaStream_t st) {
+  static const int kPh[3] = {kPhaseZY, kPhaseX, kPhaseYZ};
+  static const char* kWhat[3] = {"slab K1+K2", "slab K3", "slab K4+K5"};
+  if (phase < 0 || phase > 2) return fail(ARENA_EINVAL, "slab phase must be 0, 1 or 2");
+  if (s->xmode == ARENA_XCHG_PEER && !s->loopback && !s->attached)
+    return fail(ARENA_EINVAL, "peer exchange: call arena_slab_peer_attach first");
+  const size_t slab_bytes = size_t(s->ni) * s->n * s->n * s->base->elem;
+  const int nr = int(s->ranks.size());
+  for (int v = 0; v < nr; ++v) {
+    const int rank = s->loopback ? v : s->rank;
+    const char* f = static_cast<const char*>(d_f) + (s->loopback ? size_t(v) * slab_bytes : 0);
+    char* u = static_cast<char*>(d_u) + (s->loopback ? size_t(v) * slab_bytes : 0);
+    cudaError_t e = slab_phase(s, s->ranks[v], rank, f, u, st, kPh[phase]);
+    if (e != cudaSuccess) return cuda_fail(e, kWhat[phase]);
+  }
+  if (phase < 2 && s->xmode != ARENA_XCHG_PEER) return slab_exchange(s, st, phase == 0);
+  return ARENA_OK;
+}
+
 arena_status arena_slab_solve_device(arena_fft_slab* s, const void* d_f, void* d_u, void* stream) {
   if (!s || !d_f || !d_u) return fail(ARENA_EINVAL, "NULL slab or buffer");
   DeviceGuard g(s->base->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const size_t slab_bytes = size_t(s->ni) * s->n * s->n * s->base->elem;
-  auto fr = [&](int r) { return static_cast<const char*>(d_f) + (s->loopback ? size_t(r) * slab_bytes : 0); };
-  auto ur = [&](int r) { return static_cast<char*>(d_u) + (s->loopback ? size_t(r) * slab_bytes : 0); };
-  const int nr = int(s->ranks.size());
-  cudaError_t e;
-  for (int v = 0; v < nr; ++v) {
-    const int rank = s->loopback ? v : s->rank;
-    if ((e = slab_phase(s, s->ranks[v], rank, fr(v), ur(v), st, kPhaseZY)) != cudaSuccess)
-      return cuda_fail(e, "slab K1+K2");
-  }
-  arena_status stt = slab_exchange(s, st, true);
-  if (stt != ARENA_OK) return stt;
-  for (int v = 0; v < nr; ++v) {
-    const int rank = s->loopback ? v : s->rank;
-    if ((e = slab_phase(s, s->ranks[v], rank, fr(v), ur(v), st, kPhaseX)) != cudaSuccess) return cuda_fail(e, "slab K3");
-  }
-  if ((stt = slab_exchange(s, st, false)) != ARENA_OK) return stt;
-  for (int v = 0; v < nr; ++v) {
-    const int rank = s->loopback ? v : s->rank;
-    if ((e = slab_phase(s, s->ranks[v], rank, fr(v), ur(v), st, kPhaseYZ)) != cudaSuccess)
-      return cuda_fail(e, "slab K4+K5");
+  const bool barrier = s->xmode == ARENA_XCHG_PEER && !s->loopback && s->P > 1;
+  for (int phase = 0; phase < 3; ++phase) {
+    arena_status stt = slab_run_phase(s, phase, d_f, d_u, st);
+    if (stt != ARENA_OK) return stt;
+    if (barrier && phase < 2 && (stt = slab_peer_barrier(s, st)) != ARENA_OK) return stt;
   }
   return ARENA_OK;
+}
+
+arena_status arena_slab_solve_phase(arena_fft_slab* s, int phase, const void* d_f, void* d_u, void* stream) {
+  if (!s || !d_f || !d_u) return fail(ARENA_EINVAL, "NULL slab or buffer");
+  DeviceGuard g(s->base->device);
+  return slab_run_phase(s, phase, d_f, d_u, static_cast<cudaStream_t>(stream));
+}
+
+arena_status arena_slab_create_peer(arena_fft_slab** out, int n, int precision_bits, int device, int nranks,
+                                    int rank) {
+  if (nranks > kMaxPeers) return fail(ARENA_EUNSUPPORTED, "peer exchange supports at most 8 ranks");
+  arena_status st = slab_init(out, n, precision_bits, device, nranks, rank, 0, nullptr);
+  if (st == ARENA_OK) (*out)->xmode = ARENA_XCHG_PEER;
+  return st;
+}
+
+int arena_slab_peer_handle_bytes(void) { return int(3 * sizeof(cudaIpcMemHandle_t)); }
+
+arena_status arena_slab_peer_export(arena_fft_slab* s, void* out, int len) {
+  if (!s || !out || len < arena_slab_peer_handle_bytes()) return fail(ARENA_EINVAL, "handle buffer too small");
+  if (s->loopback) return fail(ARENA_EINVAL, "loopback slabs have no peers to export to");
+  DeviceGuard g(s->base->device);
+  cudaIpcMemHandle_t h[3];
+  cudaError_t e;
+  if ((e = cudaIpcGetMemHandle(&h[0], s->ranks[0].B)) != cudaSuccess ||
+      (e = cudaIpcGetMemHandle(&h[1], s->ranks[0].C)) != cudaSuccess ||
+      (e = cudaIpcGetMemHandle(&h[2], s->flags)) != cudaSuccess)
+    return cuda_fail(e, "cudaIpcGetMemHandle");
+  memcpy(out, h, sizeof h);
+  return ARENA_OK;
+}
+
+arena_status arena_slab_peer_attach(arena_fft_slab* s, const void* all, int len) {
+  const int hb = arena_slab_peer_handle_bytes();
+  if (!s || !all || len < hb * (s ? s->P : 0)) return fail(ARENA_EINVAL, "need every rank's handles");
+  if (s->loopback) return fail(ARENA_EINVAL, "loopback slabs need no attach");
+  if (s->P > kMaxPeers) return fail(ARENA_EUNSUPPORTED, "peer exchange supports at most 8 ranks");
+  if (s->attached) return ARENA_OK;
+  DeviceGuard g(s->base->device);
+  SlabRank& me = s->ranks[0];
+  const size_t cb = s->chunk_elems * s->base->elem;
+  for (int d = 0; d < s->P; ++d) {
+    void* ptr[3] = {me.B, me.C, s->flags};
+    if (d != s->rank) {
+      cudaIpcMemHandle_t h[3];
+      memcpy(h, static_cast<const char*>(all) + size_t(d) * hb, sizeof h);
+      for (int k = 0; k < 3; ++k) {
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr[k], h[k], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+        s->opened.push_back(ptr[k]);
+      }
+    }
+    me.peerB[d] = static_cast<char*>(ptr[0]) + size_t(s->rank) * cb;
+    me.peerC[d] = static_cast<char*>(ptr[1]) + size_t(s->rank) * cb;
+    s->pflags.peer[d] = static_cast<unsigned*>(ptr[2]);
+  }
+  s->pflags.mine = s->flags;
+  s->attached = true;
+  s->xmode = ARENA_XCHG_PEER;
+  return ARENA_OK;
+}
+
+arena_status arena_slab_set_exchange(arena_fft_slab* s, int mode) {
+  if (!s) return fail(ARENA_EINVAL, "slab is NULL");
+  if (mode == ARENA_XCHG_COPY) {
+    if (!s->loopback && !s->comm) return fail(ARENA_EINVAL, "this slab has no NCCL communicator");
+    s->xmode = mode;
+    return ARENA_OK;
+  }
+  if (mode != ARENA_XCHG_PEER) return fail(ARENA_EINVAL, "unknown exchange mode");
+  if (s->P > kMaxPeers) return fail(ARENA_EUNSUPPORTED, "peer exchange supports at most 8 ranks");
+  if (s->loopback) {
+    slab_fill_loopback_peers(s);
+  } else if (!s->attached) {
+    return fail(ARENA_EINVAL, "peer exchange: call arena_slab_peer_attach first");
+  }
+  s->xmode = mode;
+  return ARENA_OK;
+}
+
+arena_status arena_slab_barrier_status(arena_fft_slab* s) {
+  if (!s) return fail(ARENA_EINVAL, "slab is NULL");
+  DeviceGuard g(s->base->device);
+  int h = 0;
+  cudaError_t e = cudaMemcpy(&h, s->err, sizeof h, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "barrier status");
+  return h ? fail(ARENA_ECUDA, "peer barrier timed out (a rank did not arrive within 20 s)") : ARENA_OK;
+}
+
+arena_status arena_peer_barrier_selftest(int device, int nranks, int rounds, int* bad) {
+  if (nranks < 1 || nranks > kMaxPeers || rounds < 1 || !bad) return fail(ARENA_EINVAL, "bad self-test arguments");
+  DeviceGuard g(device);
+  unsigned* flags = nullptr;
+  int *data = nullptr, *err = nullptr, *dbad = nullptr;
+  cudaError_t e;
+  if ((e = cudaMalloc(&flags, sizeof(unsigned) * nranks * nranks)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  cudaMalloc(&data, sizeof(int) * nranks);
+  cudaMalloc(&err, sizeof(int));
+  cudaMalloc(&dbad, sizeof(int));
+  cudaMemset(flags, 0, sizeof(unsigned) * nranks * nranks);
+  cudaMemset(data, 0, sizeof(int) * nranks);
+  cudaMemset(err, 0, sizeof(int));
+  cudaMemset(dbad, 0, sizeof(int));
+  volatile int* vdata = data;
+  void* args[] = {&flags, (void*)&vdata, &nranks, &rounds, &err, &dbad};
+  e = cudaLaunchCooperativeKernel((const void*)k_peer_barrier_selftest, dim3(nranks), dim3(32), args, 0, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  int herr = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(bad, dbad, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(&herr, err, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(flags);
+  cudaFree(data);
+  cudaFree(err);
+  cudaFree(dbad);
+  if (e != cudaSuccess) return cuda_fail(e, "barrier self-test");
+  return herr ? fail(ARENA_ECUDA, "barrier self-test timed out") : ARENA_OK;
 }
 
 }  // extern "C"

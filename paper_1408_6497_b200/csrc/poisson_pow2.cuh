@@ -19,6 +19,7 @@
 #pragma once
 
 #include "fft_engine.cuh"
+#include "launchers.h"
 
 namespace arena_fft {
 
@@ -439,11 +440,23 @@ struct KSpan {
 // re-chunks j between its two exchanges).
 // PASS 2: x forward * Poisson symbol * x backward (layout C, tiles over (jl, k-tile)).
 // j0: global j of this rank's first local j (x pass symbol; 0 on one GPU).
-template <typename T, int N, int PASS>
+// Results of a pass scattered straight into other ranks' workspaces (slab
+// decomposition with peer-mapped buffers): output row `row`
+// of chunk c = row >> shift goes to base[c] + (row & (2^shift - 1)) * kq, where
+// base[c] is rank c's workspace advanced to this rank's chunk.  The all-to-all
+// is then the pass's own stores (over NVLink), overlapping the transform tile
+// by tile.
+template <typename V>
+struct PeerOut {
+  V* base[kMaxPeers];
+  int shift;
+};
+
+template <typename T, int N, int PASS, bool PEER = false>
 __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2)>::THREADS, PASS == 2 ? ARENA_TMA_MINB : ARENA_TMA_MINB_Y)
     k_strided_tma(const __grid_constant__ CUtensorMap tmap, vec2_t<T>* __restrict__ spec,
                   const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g, int nchunks, int j0, KSpan ks,
-                  vec2_t<T>* __restrict__ out, Layout gout) {
+                  vec2_t<T>* __restrict__ out, Layout gout, const __grid_constant__ PeerOut<vec2_t<T>> po) {
   using V = vec2_t<T>;
   using C = TmaCfg<T, N, (PASS < 2)>;
   constexpr int E = C::E, P = C::P, L = C::L, TILE = C::TILE;
@@ -583,18 +596,26 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2)>::THREADS, PASS == 2 ?
       line_fft_tail<N, E, L, +1>(v, cur, twp, t, l);
     }
     if (k < ks.kc) {
+      auto dst = [&](V* base, size_t row) -> V* {
+        if constexpr (PEER) {
+          return po.base[row >> po.shift] + (row & ((size_t(1) << po.shift) - 1)) * kq + k;
+        } else {
+          return base + row * kq + k;
+        }
+      };
       if constexpr (PASS < 2) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) st_out(out + rowB(gout, outer, t + P * e) * kq + k, v[e]);
+        for (int e = 0; e < E; ++e) st_out(dst(out, rowB(gout, outer, t + P * e)), v[e]);
       } else {
 #pragma unroll
-        for (int e = 0; e < E; ++e) st_out(spec + rowC(g, t + P * e, outer) * kq + k, v[e]);
+        for (int e = 0; e < E; ++e) st_out(dst(spec, rowC(g, t + P * e, outer)), v[e]);
       }
     }
     // No barrier needed here: every thread's last access to `cur` (the tile
     // read, or the last exchange read) is followed by a __syncthreads, so
     // thread 0 only refills it next iteration after all threads are done.
   }
+  if constexpr (PEER) __threadfence_system();  // peer stores performed before the ranks' barrier
 }
 
 }  // namespace arena_fft

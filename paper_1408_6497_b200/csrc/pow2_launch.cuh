@@ -93,16 +93,18 @@ inline const vec2_t<T>* stw_ptr(const Pow2Args& a, int which, int E) {
   return static_cast<const vec2_t<T>*>(a.stw) + stw_offset(a.n, which, E);
 }
 
-template <typename T, int N, int PASS>
+template <typename T, int N, int PASS, bool PEER = false>
 cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* spec, const Layout& g, T scale,
                                T four_pi2, KSpan ks = KSpan{N / 2 + 1, spec_pitch(N), 0}, void* out = nullptr,
-                               const Layout* gout = nullptr) {
+                               const Layout* gout = nullptr, const PeerOut<vec2_t<T>>* po = nullptr) {
   using C = TmaCfg<T, N, (PASS < 2)>;
   using V = vec2_t<T>;
-  auto kern = k_strided_tma<T, N, PASS>;
+  auto kern = k_strided_tma<T, N, PASS, PEER>;
   constexpr int SMEM = PASS == 2 ? C::SMEM_X : C::SMEM_Y;
-  cudaError_t e = ensure_smem<k_strided_tma<T, N, PASS>>(SMEM, C::THREADS);
+  cudaError_t e = ensure_smem<k_strided_tma<T, N, PASS, PEER>>(SMEM, C::THREADS);
   if (e) return e;
+  PeerOut<V> pov{};
+  if (po) pov = *po;
   int per_sm = 1;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, SMEM))) return e;
   const int tiles = (PASS < 2 ? g.ni : g.nj) * ((ks.kc + C::L - 1) / C::L);
@@ -110,7 +112,7 @@ cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* 
   if (grid > tiles) grid = tiles;
   kern<<<grid, C::THREADS, SMEM, a.stream>>>(map, static_cast<V*>(spec), stw_ptr<T>(a, 1, C::E), scale, four_pi2, g,
                                                a.nchunks, a.j0, ks, static_cast<V*>(out ? out : spec),
-                                               gout ? *gout : g);
+                                               gout ? *gout : g, pov);
   return cudaGetLastError();
 }
 
@@ -133,6 +135,19 @@ cudaError_t launch_ystream(const Pow2Args& a, const CUtensorMap& map, const Layo
     kern<<<grid, C::THREADS, C::SMEM, a.stream>>>(map, stw_ptr<T>(a, 1, C::E), g, ks, static_cast<V*>(out), gout);
     return cudaGetLastError();
   }
+}
+
+// Peer destinations of a scattering pass: chunk c -> peers[c] (rank c's
+// workspace, already advanced to this rank's chunk); chunk_rows = ni * nj.
+constexpr int kPeerMinN = 16;
+template <typename V>
+PeerOut<V> peer_table(void* const* peers, int nchunks, size_t chunk_rows) {
+  PeerOut<V> po{};
+  for (int c = 0; c < nchunks && c < kMaxPeers; ++c) po.base[c] = static_cast<V*>(peers[c]);
+  int sh = 0;
+  while ((size_t(1) << sh) < chunk_rows) ++sh;
+  po.shift = sh;
+  return po;
 }
 
 template <typename T, int N, int DIR>
@@ -210,7 +225,7 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   constexpr bool ys = ARENA_YSTREAM && YsCfg<T, NR>::OK;
   const KSpan kfull{NR / 2 + 1, spec_pitch(NR), 0};
   int mk = 0;
-  const bool fused = tma && a.ctrs != nullptr && FusedCfg<T, NR>::OK;
+  const bool fused = tma && a.ctrs != nullptr && FusedCfg<T, NR>::OK && !a.peer_y;
   if (fused && (a.fuse & kFuseFwd) && (a.phases & kPhaseZY)) {
     mark(a, mk++);
     if constexpr (FusedCfg<T, NR>::OK) {
@@ -221,7 +236,15 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
     k_zfwd<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw,
                                                                stw_ptr<T>(a, 0, CC::E), gB);
     mark(a, mk++);
-    if (tma) {
+    if (tma && a.peer_y) {
+      if constexpr (NR >= kPeerMinN) {
+        const PeerOut<V> po = peer_table<V>(a.peer_y, a.nchunks, size_t(a.ni) * a.nj);
+        e = launch_strided_tma<T, NR, 0, true>(a, *my, a.spec, gB, scale, four_pi2, kfull, nullptr, nullptr, &po);
+      } else {
+        e = cudaErrorNotSupported;
+      }
+      if (e) return e;
+    } else if (tma) {
       if constexpr (ys) e = launch_ystream<T, NR, 0>(a, *mys, gB, kfull, a.spec, gB);
       else e = launch_strided_tma<T, NR, 0>(a, *my, a.spec, gB, scale, four_pi2);
       if (e) return e;
@@ -233,7 +256,15 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   }
   if (a.phases & kPhaseX) {
     mark(a, mk++);
-    if (tma) {
+    if (tma && a.peer_x) {
+      if constexpr (NR >= kPeerMinN) {
+        const PeerOut<V> po = peer_table<V>(a.peer_x, a.nchunks, size_t(a.ni) * a.nj);
+        e = launch_strided_tma<T, NR, 2, true>(a, *mx, a.specC, gC, scale, four_pi2, kfull, nullptr, nullptr, &po);
+      } else {
+        e = cudaErrorNotSupported;
+      }
+      if (e) return e;
+    } else if (tma) {
       if ((e = launch_strided_tma<T, NR, 2>(a, *mx, a.specC, gC, scale, four_pi2))) return e;
     } else {
       if ((e = ensure_smem<k_xmid<T, NR>>(XC::SMEM, XC::THREADS))) return e;

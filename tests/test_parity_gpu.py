@@ -3,6 +3,7 @@
 Tolerances (BASELINE.json north_star): relative L2 <= 1e-12 vs the oracle in
 fp64, <= 1e-5 in fp32; spectral accuracy vs the analytic u where one exists.
 """
+import ctypes
 import os
 import subprocess
 
@@ -214,6 +215,109 @@ def test_slab_nccl_single_rank(cuda):
     s.solve_device(f, u)
     torch.cuda.synchronize()
     assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64
+
+
+@pytest.mark.parametrize("n,P", [(32, 2), (64, 4), (128, 8), (256, 2)])
+def test_slab_peer_loopback_vs_oracle(cuda, n, P):
+    """Peer exchange (K2 / K3 store their chunks straight into the owning rank's
+    workspace) with P virtual ranks on one GPU: the same kernels and pointer
+    tables the multi-GPU path uses over NVLink, checked against the oracle."""
+    torch = cuda
+    f_np = np.random.default_rng(3 * n + P).uniform(-1, 1, (n, n, n))
+    f = torch.from_numpy(f_np).cuda()
+    u = torch.empty_like(f)
+    s = arena.Slab(n, P, loopback=True)
+    s.set_exchange(arena.XCHG_PEER)
+    s.solve_device(f, u)
+    torch.cuda.synchronize()
+    assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64
+
+
+def test_slab_peer_loopback_1024_analytic(cuda):
+    torch = cuda
+    src, f, ua = _config_device(torch, 4)
+    u = torch.empty_like(f)
+    s = arena.Slab(1024, 8, loopback=True)
+    s.set_exchange(arena.XCHG_PEER)
+    s.solve_device(f, u)
+    torch.cuda.synchronize()
+    e = (torch.linalg.vector_norm(u - ua) / torch.linalg.vector_norm(ua)).item()
+    assert e <= 1e-12, e
+
+
+def test_slab_peer_single_rank(cuda):
+    """arena_slab_create_peer / export / attach with one rank (no IPC mapping needed)."""
+    torch = cuda
+    n = 64
+    f_np = np.random.default_rng(9).uniform(-1, 1, (n, n, n))
+    f = torch.from_numpy(f_np).cuda()
+    u = torch.empty_like(f)
+    s = arena.Slab(n, 1, rank=0, peer=True)
+    s.peer_attach(s.peer_handles())
+    s.solve_device(f, u)
+    torch.cuda.synchronize()
+    s.barrier_status()
+    assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_peer_barrier_protocol(cuda, P):
+    """The device barrier of the peer exchange (release / acquire at system
+    scope, epochs), all P ranks emulated by the blocks of ONE cooperative launch:
+    after each barrier every rank sees every rank's pre-barrier write."""
+    bad = ctypes.c_int(-1)
+    assert arena.lib.arena_peer_barrier_selftest(0, P, 500, ctypes.byref(bad)) == 0, arena.lib.arena_last_error()
+    assert bad.value == 0
+
+
+def _peer_ipc_rank(rank, world, port, n, f_np, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    ni = n // world
+    f = torch.from_numpy(np.ascontiguousarray(f_np[rank * ni:(rank + 1) * ni])).cuda()
+    u = torch.empty_like(f)
+    s = arena.Slab(n, world, rank=rank, peer=True, device=0)
+    hs = [None] * world
+    dist.all_gather_object(hs, s.peer_handles())
+    s.peer_attach(b"".join(hs))
+    for phase in range(3):  # the ranks share one GPU: synchronise on the host, not on the device
+        s.solve_phase(phase, f, u)
+        torch.cuda.synchronize()
+        dist.barrier()
+    us = [None] * world
+    dist.all_gather_object(us, u.cpu().numpy())
+    if rank == 0:
+        out.copy_(torch.from_numpy(np.concatenate(us).ravel()))
+    dist.barrier()
+    s.close()
+    dist.destroy_process_group()
+
+
+def test_slab_peer_ipc_two_processes(cuda):
+    """Two processes (two ranks) sharing this GPU map each other's workspaces with
+    CUDA IPC — the multi-GPU setup path — and run the peer-store kernels; the
+    phases are separated by host barriers (the device barrier needs one GPU per rank)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    torch = cuda
+    n, world = 64, 2
+    f_np = np.random.default_rng(77).uniform(-1, 1, (n, n, n))
+    out = torch.zeros(n ** 3, dtype=torch.float64).share_memory_()
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    mp.spawn(_peer_ipc_rank, args=(world, port, n, f_np, out), nprocs=world, join=True)
+    assert _rel(out.numpy().reshape(n, n, n), oracle.poisson_solve(f_np)) <= TOL64
 
 
 def test_batched_host_solves(cuda):

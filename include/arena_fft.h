@@ -156,6 +156,17 @@ arena_status arena_slab_set_exchange(arena_fft_slab* slab, int mode);
  * after phases 0 and 1).  In PEER mode the caller must synchronise all ranks
  * between phases (arena_slab_solve_device does it on the device). */
 arena_status arena_slab_solve_phase(arena_fft_slab* slab, int phase, const void* d_f, void* d_u, void* stream);
+/* Device-side verification (synchronous; fp64 accumulation with compensated
+ * sums).  arena_field_stats = GridField::mean / max_abs (grid.cpp:9-19) of a
+ * device field.  arena_field_compare = the gauge-aligned error of
+ * linf_rel_error (problems.cpp:88-106) on the grid: shift = mean(exact) -
+ * mean(num); linf_rel = max|num + shift - exact| / max|exact|; rel_l2 =
+ * ||num + shift - exact||_2 / ||exact - mean(exact)||_2.  Fields are `count`
+ * contiguous values (n^3 for a GridField).  Any output may be NULL. */
+arena_status arena_field_stats(size_t count, int precision_bits, const void* d_field, double* mean, double* max_abs);
+arena_status arena_field_compare(size_t count, int precision_bits, const void* d_num, const void* d_exact,
+                                 double* rel_l2, double* linf_rel, double* gauge_shift);
+
 /* ARENA_OK, or ARENA_ECUDA if a device barrier gave up waiting (20 s). */
 arena_status arena_slab_barrier_status(arena_fft_slab* slab);
 /* Check the peer barrier protocol on one device: one cooperative launch, block r

@@ -86,6 +86,10 @@ _sig = {
     "arena_slab_solve_phase": (_i, [_vp, _i, _vp, _vp, _vp]),
     "arena_slab_barrier_status": (_i, [_vp]),
     "arena_peer_barrier_selftest": (_i, [_i, _i, _i, ctypes.POINTER(_i)]),
+    "arena_field_stats": (_i, [ctypes.c_size_t, _i, _vp, ctypes.POINTER(ctypes.c_double),
+                               ctypes.POINTER(ctypes.c_double)]),
+    "arena_field_compare": (_i, [ctypes.c_size_t, _i, _vp, _vp, ctypes.POINTER(ctypes.c_double),
+                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "arena_pow2_kernel_geometry": (_i, [_i, _i, ctypes.POINTER(_i)]),
     "arena_pencil_create": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _i, _i, _i, _vp]),
     "arena_pencil_create_loopback": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _i, _i]),
@@ -404,6 +408,34 @@ def dft3_inverse(spec: np.ndarray, n: int) -> np.ndarray:
     p = get_plan(n, 64)
     with p.lock:
         return p.dft3_inverse_host(spec.reshape(n, n, n))
+
+
+def _prec_of(t) -> int:
+    import torch
+    if t.dtype == torch.float64:
+        return 64
+    if t.dtype == torch.float32:
+        return 32
+    raise TypeError("field must be float64 or float32")
+
+
+def field_stats(t):
+    """(mean, max_abs) of a contiguous CUDA tensor (GridField::mean / max_abs, grid.cpp:9-19), on the device."""
+    m, a = ctypes.c_double(), ctypes.c_double()
+    _check(lib.arena_field_stats(t.numel(), _prec_of(t), _vp(_ptr(t)), ctypes.byref(m), ctypes.byref(a)),
+           "arena_field_stats")
+    return m.value, a.value
+
+
+def field_compare(num, exact) -> dict:
+    """Gauge-aligned errors of num vs exact (problems.cpp:88-106 on the grid), on the device:
+    {"rel_l2", "linf_rel", "gauge_shift"}."""
+    if num.numel() != exact.numel() or num.dtype != exact.dtype:
+        raise ValueError("fields must have the same size and dtype")
+    r, li, sh = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    _check(lib.arena_field_compare(num.numel(), _prec_of(num), _vp(_ptr(num)), _vp(_ptr(exact)), ctypes.byref(r),
+                                   ctypes.byref(li), ctypes.byref(sh)), "arena_field_compare")
+    return {"rel_l2": r.value, "linf_rel": li.value, "gauge_shift": sh.value}
 
 
 class SpectralInterpolant:

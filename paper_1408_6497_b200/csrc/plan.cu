@@ -37,6 +37,15 @@ arena_status cuda_fail(cudaError_t e, const char* what) {
 
 bool is_pow2(int n) { return n >= 2 && (n & (n - 1)) == 0; }
 
+}  // namespace
+
+// For the other translation units (verify.cu): set the thread's arena_last_error.
+namespace arena_fft {
+arena_status set_error(arena_status s, const std::string& msg) { return fail(s, msg); }
+}  // namespace arena_fft
+
+namespace {
+
 // stage names by fused mask (0: none, 1: forward pair fused, 2: inverse pair, 3: both)
 const char* kStageNames[4][kPow2Launches] = {
     {"zfwd_r2c", "yfwd", "xmid_fwd_scale_inv", "yinv", "zinv_c2r"},

@@ -320,6 +320,36 @@ def test_slab_peer_ipc_two_processes(cuda):
     assert _rel(out.numpy().reshape(n, n, n), oracle.poisson_solve(f_np)) <= TOL64
 
 
+def test_field_stats_and_compare(cuda):
+    """Device verification reductions vs numpy: mean / max_abs (grid.cpp:9-19) and
+    the gauge-aligned l_inf / l2 errors of linf_rel_error (problems.cpp:88-106)."""
+    torch = cuda
+    rng = np.random.default_rng(11)
+    ex = rng.uniform(-1, 1, (48, 40, 64)) + 0.25
+    num = ex - 0.7 + 1e-9 * rng.standard_normal(ex.shape)  # a gauge offset plus a small error
+    te, tn = torch.from_numpy(ex).cuda(), torch.from_numpy(num).cuda()
+    m, a = arena.field_stats(te)
+    assert abs(m - ex.mean()) <= 1e-15 and a == np.abs(ex).max()
+    r = arena.field_compare(tn, te)
+    shift = ex.mean() - num.mean()
+    d = num + shift - ex
+    assert abs(r["gauge_shift"] - shift) <= 1e-14
+    assert abs(r["linf_rel"] - np.abs(d).max() / np.abs(ex).max()) <= 1e-6 * r["linf_rel"]
+    assert abs(r["rel_l2"] - np.linalg.norm(d) / np.linalg.norm(ex - ex.mean())) <= 1e-6 * r["rel_l2"]
+    r32 = arena.field_compare(tn.float(), te.float())
+    assert abs(r32["gauge_shift"] - shift) <= 1e-6
+
+
+def test_field_compare_config4_1024(cuda):
+    """The solve at 1024^3 checked on the device: gauge-aligned l_inf and l2 vs analytic u."""
+    torch = cuda
+    src, f, ua = _config_device(torch, 4)
+    u = torch.empty_like(f)
+    arena.Plan(1024).solve_device(f, u)
+    r = arena.field_compare(u, ua)
+    assert r["rel_l2"] <= 1e-12 and r["linf_rel"] <= 1e-12, r
+
+
 def test_batched_host_solves(cuda):
     """arena_poisson_solve_host_batch (copy/compute overlap) == independent solves."""
     torch = cuda

@@ -402,14 +402,40 @@ namespace arena_fft {
 #define ARENA_TMA_EARLY_Y 1  // y passes: request the next tile right after the last exchange
 #endif
 
+// fp32 variants (a complex float is 8 bytes, so 128-byte TMA rows need 16 lines).
+#ifndef ARENA_TMA_LROW
+#define ARENA_TMA_LROW 128  // bytes of a tile row (L adjacent k) at most
+#endif
+#ifndef ARENA_TMA_E32
+#define ARENA_TMA_E32 32
+#endif
+#ifndef ARENA_TMA_E_Y32
+#define ARENA_TMA_E_Y32 16  // fp32 y: 16-line tiles (128-byte rows), 1024 threads (B200: 1.73 vs 2.02 ms at E = 32)
+#endif
+#ifndef ARENA_TMA_X_TILE32
+#define ARENA_TMA_X_TILE32 ARENA_TMA_X_TILE
+#endif
+#ifndef ARENA_TMA_Y_TILE32
+#define ARENA_TMA_Y_TILE32 ARENA_TMA_Y_TILE
+#endif
+#ifndef ARENA_TMA_MINB32
+#define ARENA_TMA_MINB32 ARENA_TMA_MINB
+#endif
+#ifndef ARENA_TMA_MINB_Y32
+#define ARENA_TMA_MINB_Y32 ARENA_TMA_MINB_Y
+#endif
+
 // YP: configuration of the y passes (PASS 0/1) vs the x pass.
 template <typename T, int N, bool YP = false>
 struct TmaCfg {
+  static constexpr bool F64 = sizeof(T) == 8;
   static constexpr int VB = 2 * sizeof(T);
-  static constexpr int E = imin(YP ? ARENA_TMA_E_Y : ARENA_TMA_E, N);
+  static constexpr int E = imin(YP ? (F64 ? ARENA_TMA_E_Y : ARENA_TMA_E_Y32) : (F64 ? ARENA_TMA_E : ARENA_TMA_E32), N);
   static constexpr int P = N / E;
-  static constexpr int BUDGET = YP ? ARENA_TMA_Y_TILE : ARENA_TMA_X_TILE;
-  static constexpr int L = pow2_floor(imax(2, imin(8, BUDGET / (N * VB))));
+  static constexpr int BUDGET = YP ? (F64 ? ARENA_TMA_Y_TILE : ARENA_TMA_Y_TILE32)
+                                   : (F64 ? ARENA_TMA_X_TILE : ARENA_TMA_X_TILE32);
+  static constexpr int MINB = YP ? (F64 ? ARENA_TMA_MINB_Y : ARENA_TMA_MINB_Y32) : (F64 ? ARENA_TMA_MINB : ARENA_TMA_MINB32);
+  static constexpr int L = pow2_floor(imax(2, imin(ARENA_TMA_LROW / VB, BUDGET / (N * VB))));
   static constexpr int THREADS = L * P;
   static constexpr int NC = N / 2 + 1;
   static constexpr int KT = (NC + L - 1) / L;  // k tiles per line set
@@ -453,7 +479,7 @@ struct PeerOut {
 };
 
 template <typename T, int N, int PASS, bool PEER = false>
-__global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2)>::THREADS, PASS == 2 ? ARENA_TMA_MINB : ARENA_TMA_MINB_Y)
+__global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2)>::THREADS, TmaCfg<T, N, (PASS < 2)>::MINB)
     k_strided_tma(const __grid_constant__ CUtensorMap tmap, vec2_t<T>* __restrict__ spec,
                   const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g, int nchunks, int j0, KSpan ks,
                   vec2_t<T>* __restrict__ out, Layout gout, const __grid_constant__ PeerOut<vec2_t<T>> po) {

@@ -47,7 +47,7 @@ def _args():
     ap.add_argument("--decomp", default="slab", choices=("slab", "pencil"), help="multi-GPU decomposition")
     ap.add_argument("--pgrid", default=None, help="pencil process grid RxC (default: near-square, R <= C)")
     ap.add_argument("--xchg", default="peer", choices=("peer", "nccl"),
-                    help="slab exchange: peer = fused into K2/K3 as NVLink stores (CUDA IPC), nccl = send/recv")
+                    help="exchange: peer = fused into the passes as NVLink stores (CUDA IPC), nccl = send/recv")
     return ap.parse_args()
 
 
@@ -430,10 +430,13 @@ def run_slab(args, rank, world, local):
         return t.item() == 1
 
     def try_peer():
-        nb = arena.lib.arena_slab_peer_handle_bytes()
+        nb = arena.lib.arena_pencil_peer_handle_bytes() if pencil else arena.lib.arena_slab_peer_handle_bytes()
         s, err = None, None
         try:
-            s = arena.Slab(n, world, rank=rank, peer=True, precision=prec, device=local)
+            if pencil:
+                s = arena.Pencil(n, pr, pc, rank=rank, peer=True, precision=prec, device=local)
+            else:
+                s = arena.Slab(n, world, rank=rank, peer=True, precision=prec, device=local)
             hb = s.peer_handles()
         except Exception as exc:
             err, hb = exc, bytes(nb)
@@ -462,7 +465,7 @@ def run_slab(args, rank, world, local):
             return None, f"parity {r:.2e}"
         return s, None
 
-    xchg = "nccl" if pencil else args.xchg
+    xchg = args.xchg
     note = None
     slab = None
     if xchg == "peer":
@@ -533,8 +536,11 @@ def run_slab(args, rank, world, local):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if prec == 64 else "f32", "data": "synthetic",
             "config": {"workload": f"C{args.config}: {problems.CONFIG_TEXT[args.config]}", "n": n, "precision": prec,
-                       "decomposition": (f"pencil {pr}x{pc}, NCCL row/column all-to-alls (4 per solve)" if pencil
-                                         else f"slab x{world} over i, " + (
+                       "decomposition": ((f"pencil {pr}x{pc}, " + (
+                                             "4 row/column all-to-alls fused into K1-K4 as stores into the peers' "
+                                             "buffers (CUDA IPC over NVLink) + device flag barriers"
+                                             if xchg == "peer" else "NCCL row/column all-to-alls (4 per solve)"))
+                                         if pencil else f"slab x{world} over i, " + (
                                              "all-to-alls fused into K2/K3 as stores into the peers' "
                                              "workspaces (CUDA IPC over NVLink) + device flag barriers"
                                              if xchg == "peer" else "NCCL grouped send/recv all-to-all")),

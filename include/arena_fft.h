@@ -188,6 +188,18 @@ void arena_pencil_destroy(arena_fft_pencil* pencil);
 arena_status arena_pencil_info(const arena_fft_pencil* pencil, int* kq, size_t* buffer_bytes, size_t* block_bytes);
 int arena_pencil_launches_per_solve(const arena_fft_pencil* pencil);
 arena_status arena_pencil_solve_device(arena_fft_pencil* pencil, const void* d_f, void* d_u, void* stream);
+/* Peer exchange for the pencil (see ARENA_XCHG_PEER): K1 / K2 / K3 / K4 store
+ * their output chunks straight into the row / column peers' buffers; four
+ * device barriers per solve.  Phases of arena_pencil_solve_phase: 0 K1, 1 K2,
+ * 2 K3, 3 K4, 4 K5 (COPY mode: with the exchange after phases 0-3). */
+arena_status arena_pencil_create_peer(arena_fft_pencil** pencil, int n, int precision_bits, int device, int pr, int pc,
+                                      int rank);
+int arena_pencil_peer_handle_bytes(void);
+arena_status arena_pencil_peer_export(arena_fft_pencil* pencil, void* out, int len);
+arena_status arena_pencil_peer_attach(arena_fft_pencil* pencil, const void* all_handles, int len);
+arena_status arena_pencil_set_exchange(arena_fft_pencil* pencil, int mode);
+arena_status arena_pencil_solve_phase(arena_fft_pencil* pencil, int phase, const void* d_f, void* d_u, void* stream);
+arena_status arena_pencil_barrier_status(arena_fft_pencil* pencil);
 
 /* Batch evaluation of arena::SpectralInterpolant (fft_solver.cpp:89-114) on the
  * GPU: out[p] = sum_m Re(amp_m exp(2 pi i k_m . x_p)).  k: 3*nmodes ints (signed

@@ -86,6 +86,13 @@ _sig = {
     "arena_slab_solve_phase": (_i, [_vp, _i, _vp, _vp, _vp]),
     "arena_slab_barrier_status": (_i, [_vp]),
     "arena_peer_barrier_selftest": (_i, [_i, _i, _i, ctypes.POINTER(_i)]),
+    "arena_pencil_create_peer": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _i, _i, _i]),
+    "arena_pencil_peer_handle_bytes": (_i, []),
+    "arena_pencil_peer_export": (_i, [_vp, _vp, _i]),
+    "arena_pencil_peer_attach": (_i, [_vp, _vp, _i]),
+    "arena_pencil_set_exchange": (_i, [_vp, _i]),
+    "arena_pencil_solve_phase": (_i, [_vp, _i, _vp, _vp, _vp]),
+    "arena_pencil_barrier_status": (_i, [_vp]),
     "arena_field_stats": (_i, [ctypes.c_size_t, _i, _vp, ctypes.POINTER(ctypes.c_double),
                                ctypes.POINTER(ctypes.c_double)]),
     "arena_field_compare": (_i, [ctypes.c_size_t, _i, _vp, _vp, ctypes.POINTER(ctypes.c_double),
@@ -221,7 +228,62 @@ class Plan:
 XCHG_COPY, XCHG_PEER = 0, 1
 
 
-class Slab:
+class _Decomposition:
+    """Peer-exchange / phase methods shared by Slab and Pencil (prefix arena_slab_ / arena_pencil_)."""
+
+    _pfx = ""
+
+    def _fn(self, name):
+        return getattr(lib, f"arena_{self._pfx}_{name}")
+
+    def solve_device(self, f, u, stream: Optional[int] = None) -> None:
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(f.device).cuda_stream
+        _check(self._fn("solve_device")(self._s, _vp(_ptr(f)), _vp(_ptr(u)), _vp(stream)),
+               f"arena_{self._pfx}_solve_device")
+
+    def solve_phase(self, phase: int, f, u, stream: Optional[int] = None) -> None:
+        """One phase of a solve (slab 0-2, pencil 0-4); peer mode: synchronise the ranks in between."""
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(f.device).cuda_stream
+        _check(self._fn("solve_phase")(self._s, int(phase), _vp(_ptr(f)), _vp(_ptr(u)), _vp(stream)),
+               f"arena_{self._pfx}_solve_phase")
+
+    def peer_handles(self) -> bytes:
+        nb = self._fn("peer_handle_bytes")()
+        buf = ctypes.create_string_buffer(nb)
+        _check(self._fn("peer_export")(self._s, buf, nb), f"arena_{self._pfx}_peer_export")
+        return buf.raw
+
+    def peer_attach(self, all_handles: bytes) -> None:
+        buf = ctypes.create_string_buffer(bytes(all_handles), len(all_handles))
+        _check(self._fn("peer_attach")(self._s, buf, len(all_handles)), f"arena_{self._pfx}_peer_attach")
+
+    def set_exchange(self, mode: int) -> None:
+        _check(self._fn("set_exchange")(self._s, int(mode)), f"arena_{self._pfx}_set_exchange")
+
+    def barrier_status(self) -> None:
+        _check(self._fn("barrier_status")(self._s), f"arena_{self._pfx}_barrier_status")
+
+    @property
+    def launches_per_solve(self) -> int:
+        return self._fn("launches_per_solve")(self._s)
+
+    def close(self) -> None:
+        if getattr(self, "_s", None) and self._s.value:
+            self._fn("destroy")(self._s)
+            self._s = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Slab(_Decomposition):
     """Slab decomposition over P ranks (include/arena_fft.h, arena_slab_*).
 
     Slab(n, P, rank=r, nccl_id=bytes) — one rank of a multi-GPU solve (NCCL all-to-alls);
@@ -231,6 +293,8 @@ class Slab:
     Slab(n, P, loopback=True)         — P virtual ranks on one device (testing);
                                         set_exchange(XCHG_PEER) for the peer-store kernels.
     """
+
+    _pfx = "slab"
 
     def __init__(self, n: int, nranks: int, rank: int = 0, nccl_id: Optional[bytes] = None,
                  precision: int = 64, device: int = -1, loopback: bool = False, peer: bool = False):
@@ -253,66 +317,27 @@ class Slab:
                "arena_slab_info")
         self.ni, self.nj, self.chunk_bytes, self.workspace_bytes = ni.value, nj.value, cb.value, wb.value
 
-    @property
-    def launches_per_solve(self) -> int:
-        return lib.arena_slab_launches_per_solve(self._s)
 
-    def solve_device(self, f, u, stream: Optional[int] = None) -> None:
-        if stream is None:
-            import torch
-            stream = torch.cuda.current_stream(f.device).cuda_stream
-        _check(lib.arena_slab_solve_device(self._s, _vp(_ptr(f)), _vp(_ptr(u)), _vp(stream)),
-               "arena_slab_solve_device")
-
-    def solve_phase(self, phase: int, f, u, stream: Optional[int] = None) -> None:
-        """Phase 0 (K1+K2), 1 (K3) or 2 (K4+K5); peer mode: synchronise the ranks in between."""
-        if stream is None:
-            import torch
-            stream = torch.cuda.current_stream(f.device).cuda_stream
-        _check(lib.arena_slab_solve_phase(self._s, int(phase), _vp(_ptr(f)), _vp(_ptr(u)), _vp(stream)),
-               "arena_slab_solve_phase")
-
-    def peer_handles(self) -> bytes:
-        nb = lib.arena_slab_peer_handle_bytes()
-        buf = ctypes.create_string_buffer(nb)
-        _check(lib.arena_slab_peer_export(self._s, buf, nb), "arena_slab_peer_export")
-        return buf.raw
-
-    def peer_attach(self, all_handles: bytes) -> None:
-        buf = ctypes.create_string_buffer(bytes(all_handles), len(all_handles))
-        _check(lib.arena_slab_peer_attach(self._s, buf, len(all_handles)), "arena_slab_peer_attach")
-
-    def set_exchange(self, mode: int) -> None:
-        _check(lib.arena_slab_set_exchange(self._s, int(mode)), "arena_slab_set_exchange")
-
-    def barrier_status(self) -> None:
-        _check(lib.arena_slab_barrier_status(self._s), "arena_slab_barrier_status")
-
-    def close(self) -> None:
-        if getattr(self, "_s", None) and self._s.value:
-            lib.arena_slab_destroy(self._s)
-            self._s = _vp()
-
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
-
-
-class Pencil:
+class Pencil(_Decomposition):
     """Pencil decomposition over a Pr x Pc process grid (include/arena_fft.h, arena_pencil_*).
 
-    Pencil(n, Pr, Pc, rank=r, nccl_id=bytes) — one rank (its block (n/Pr) x (n/Pc) x n);
+    Pencil(n, Pr, Pc, rank=r, nccl_id=bytes) — one rank (its block (n/Pr) x (n/Pc) x n), NCCL;
+    Pencil(n, Pr, Pc, rank=r, peer=True)    — one rank, exchanges fused into K1-K4 as stores
+                                              into the peers' buffers (peer_attach first);
     Pencil(n, Pr, Pc, loopback=True)        — all ranks on one device (full field in/out).
     """
 
+    _pfx = "pencil"
+
     def __init__(self, n: int, pr: int, pc: int, rank: int = 0, nccl_id: Optional[bytes] = None,
-                 precision: int = 64, device: int = -1, loopback: bool = False):
+                 precision: int = 64, device: int = -1, loopback: bool = False, peer: bool = False):
         self._s = _vp()
         if loopback:
             _check(lib.arena_pencil_create_loopback(ctypes.byref(self._s), int(n), int(precision), int(device),
                                                     int(pr), int(pc)), "arena_pencil_create_loopback")
+        elif peer:
+            _check(lib.arena_pencil_create_peer(ctypes.byref(self._s), int(n), int(precision), int(device),
+                                                int(pr), int(pc), int(rank)), "arena_pencil_create_peer")
         else:
             if nccl_id is None:
                 raise ValueError("nccl_id required (see nccl_unique_id())")
@@ -323,28 +348,6 @@ class Pencil:
         kq, bb, kb = _i(), ctypes.c_size_t(), ctypes.c_size_t()
         _check(lib.arena_pencil_info(self._s, ctypes.byref(kq), ctypes.byref(bb), ctypes.byref(kb)), "arena_pencil_info")
         self.kq, self.buffer_bytes, self.block_bytes = kq.value, bb.value, kb.value
-
-    @property
-    def launches_per_solve(self) -> int:
-        return lib.arena_pencil_launches_per_solve(self._s)
-
-    def solve_device(self, f, u, stream: Optional[int] = None) -> None:
-        if stream is None:
-            import torch
-            stream = torch.cuda.current_stream(f.device).cuda_stream
-        _check(lib.arena_pencil_solve_device(self._s, _vp(_ptr(f)), _vp(_ptr(u)), _vp(stream)),
-               "arena_pencil_solve_device")
-
-    def close(self) -> None:
-        if getattr(self, "_s", None) and self._s.value:
-            lib.arena_pencil_destroy(self._s)
-            self._s = _vp()
-
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
 
 
 def nccl_unique_id() -> bytes:

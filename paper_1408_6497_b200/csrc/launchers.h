@@ -74,8 +74,17 @@ struct PencilArgs {
   int kq;            // k-chunk pitch (complex)
   cudaStream_t stream;
   TmaCache* tma;     // maps[0]: y over buf2 (Y), maps[1]: x over buf2 (C); y-inv map in tma2
-  TmaCache* tma2;    // maps[0]: y-inverse over buf1 (B2)
+  TmaCache* tma2;    // maps[0]: y-inverse over buf1 (B2); peer mode: maps[1] x over buf1, maps[2] y-inverse over buf2
   int sm_count;
+  // Peer exchange: every all-to-all is the stores of the pass before it.  The
+  // spectrum then lives in buf2 (Y, then B2 for the way back) and buf1 (C, then
+  // R for the way back): K1 -> row peer q's buf2, K2 -> column peer q's buf1,
+  // K3 -> column peer q's buf2, K4 -> row peer q's buf1, each advanced to this
+  // rank's chunk.  nullptr = NCCL / copy exchanges.
+  void* const* pz = nullptr;
+  void* const* py1 = nullptr;
+  void* const* px = nullptr;
+  void* const* py2 = nullptr;
 };
 enum : int { kPencilZ1 = 0, kPencilY1, kPencilX, kPencilY2, kPencilZ2 };
 cudaError_t pencil_phase_f64(const PencilArgs& a, int phase);

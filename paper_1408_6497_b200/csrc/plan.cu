@@ -714,6 +714,78 @@ __global__ void k_peer_barrier_selftest(unsigned* flags, volatile int* data, int
   }
 }
 
+// Peer-exchange state shared by the slab and pencil decompositions: this rank's
+// barrier flags, the peers' flag arrays, the IPC mappings to close.
+struct PeerSync {
+  unsigned* flags = nullptr;  // P
+  int* err = nullptr;
+  PeerFlags pf{};
+  unsigned epoch = 0;
+  std::vector<void*> opened;
+
+  cudaError_t init(int P) {
+    cudaError_t e;
+    if ((e = cudaMalloc(&flags, sizeof(unsigned) * size_t(P))) != cudaSuccess) return e;
+    if ((e = cudaMemset(flags, 0, sizeof(unsigned) * size_t(P))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&err, sizeof(int))) != cudaSuccess) return e;
+    return cudaMemset(err, 0, sizeof(int));
+  }
+  void release() {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    opened.clear();
+    if (flags) cudaFree(flags);
+    if (err) cudaFree(err);
+    flags = nullptr;
+    err = nullptr;
+  }
+  // Handles of `bufs` and of the flags, in that order.
+  arena_status export_handles(const std::vector<void*>& bufs, void* out) const {
+    std::vector<cudaIpcMemHandle_t> h(bufs.size() + 1);
+    for (size_t k = 0; k <= bufs.size(); ++k) {
+      cudaError_t e = cudaIpcGetMemHandle(&h[k], k < bufs.size() ? bufs[k] : static_cast<void*>(flags));
+      if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    }
+    memcpy(out, h.data(), h.size() * sizeof(cudaIpcMemHandle_t));
+    return ARENA_OK;
+  }
+  // ptrs[d][k]: buffer k of rank d (own buffers for d == rank); flag arrays into pf.
+  arena_status attach(const void* all, int P, int rank, const std::vector<void*>& mine,
+                      std::vector<std::vector<void*>>& ptrs) {
+    const size_t nb = mine.size() + 1, hb = nb * sizeof(cudaIpcMemHandle_t);
+    ptrs.assign(P, mine);
+    for (int d = 0; d < P; ++d) {
+      void* fl = flags;
+      if (d != rank) {
+        std::vector<cudaIpcMemHandle_t> h(nb);
+        memcpy(h.data(), static_cast<const char*>(all) + size_t(d) * hb, hb);
+        for (size_t k = 0; k < nb; ++k) {
+          void* ptr = nullptr;
+          cudaError_t e = cudaIpcOpenMemHandle(&ptr, h[k], cudaIpcMemLazyEnablePeerAccess);
+          if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+          opened.push_back(ptr);
+          if (k < mine.size()) ptrs[d][k] = ptr;
+          else fl = ptr;
+        }
+      }
+      pf.peer[d] = static_cast<unsigned*>(fl);
+    }
+    pf.mine = flags;
+    return ARENA_OK;
+  }
+  arena_status barrier(cudaStream_t st, int rank, int P) {
+    ++epoch;
+    k_peer_barrier<<<1, 32, 0, st>>>(pf, rank, P, epoch, err);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ARENA_OK : cuda_fail(e, "peer barrier");
+  }
+  arena_status status() const {
+    int h = 0;
+    cudaError_t e = cudaMemcpy(&h, err, sizeof h, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "barrier status");
+    return h ? fail(ARENA_ECUDA, "peer barrier timed out (a rank did not arrive within 20 s)") : ARENA_OK;
+  }
+};
+
 }  // namespace
 
 struct arena_fft_slab {
@@ -726,11 +798,7 @@ struct arena_fft_slab {
   ncclComm_t comm = nullptr;
   int xmode = ARENA_XCHG_COPY;  // ARENA_XCHG_PEER: K2 / K3 store into the peers' workspaces
   bool attached = false;        // peer pointers of the other ranks opened (multi-process)
-  unsigned* flags = nullptr;    // this rank's barrier flags (P)
-  PeerFlags pflags{};
-  int* err = nullptr;           // barrier timeout flag
-  unsigned epoch = 0;
-  std::vector<void*> opened;    // IPC mappings to close
+  PeerSync sync;
 };
 
 namespace {
@@ -739,9 +807,7 @@ void free_slab(arena_fft_slab* s) {
   if (!s) return;
   if (s->base) {
     DeviceGuard g(s->base->device);
-    for (void* p : s->opened) cudaIpcCloseMemHandle(p);
-    if (s->flags) cudaFree(s->flags);
-    if (s->err) cudaFree(s->err);
+    s->sync.release();
     for (SlabRank& r : s->ranks) {
       if (r.B) cudaFree(r.B);
       if (r.C) cudaFree(r.C);
@@ -795,14 +861,9 @@ arena_status slab_init(arena_fft_slab** out, int n, int prec, int device, int P,
       return fail(ARENA_ENOMEM, "slab counters");
     }
   }
-  {
-    cudaError_t e;
-    if ((e = cudaMalloc(&s->flags, sizeof(unsigned) * size_t(P))) != cudaSuccess ||
-        (e = cudaMemset(s->flags, 0, sizeof(unsigned) * size_t(P))) != cudaSuccess ||
-        (e = cudaMalloc(&s->err, sizeof(int))) != cudaSuccess || (e = cudaMemset(s->err, 0, sizeof(int))) != cudaSuccess) {
-      free_slab(s);
-      return fail(ARENA_ENOMEM, "slab barrier flags: " + std::string(cudaGetErrorString(e)));
-    }
+  if (cudaError_t e = s->sync.init(P)) {
+    free_slab(s);
+    return fail(ARENA_ENOMEM, "slab barrier flags: " + std::string(cudaGetErrorString(e)));
   }
   if (!loopback && id) {
     NcclApi* a = nccl_api();
@@ -848,12 +909,7 @@ void slab_fill_loopback_peers(arena_fft_slab* s) {
     }
 }
 
-arena_status slab_peer_barrier(arena_fft_slab* s, cudaStream_t st) {
-  ++s->epoch;
-  k_peer_barrier<<<1, 32, 0, st>>>(s->pflags, s->rank, s->P, s->epoch, s->err);
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? ARENA_OK : cuda_fail(e, "peer barrier");
-}
+arena_status slab_peer_barrier(arena_fft_slab* s, cudaStream_t st) { return s->sync.barrier(st, s->rank, s->P); }
 
 // All-to-all between workspaces: forward (B chunk d of rank r -> C chunk r of rank d)
 // or backward (C chunk d of rank r -> B chunk r of rank d).
@@ -987,14 +1043,7 @@ arena_status arena_slab_peer_export(arena_fft_slab* s, void* out, int len) {
   if (!s || !out || len < arena_slab_peer_handle_bytes()) return fail(ARENA_EINVAL, "handle buffer too small");
   if (s->loopback) return fail(ARENA_EINVAL, "loopback slabs have no peers to export to");
   DeviceGuard g(s->base->device);
-  cudaIpcMemHandle_t h[3];
-  cudaError_t e;
-  if ((e = cudaIpcGetMemHandle(&h[0], s->ranks[0].B)) != cudaSuccess ||
-      (e = cudaIpcGetMemHandle(&h[1], s->ranks[0].C)) != cudaSuccess ||
-      (e = cudaIpcGetMemHandle(&h[2], s->flags)) != cudaSuccess)
-    return cuda_fail(e, "cudaIpcGetMemHandle");
-  memcpy(out, h, sizeof h);
-  return ARENA_OK;
+  return s->sync.export_handles({s->ranks[0].B, s->ranks[0].C}, out);
 }
 
 arena_status arena_slab_peer_attach(arena_fft_slab* s, const void* all, int len) {
@@ -1005,23 +1054,14 @@ arena_status arena_slab_peer_attach(arena_fft_slab* s, const void* all, int len)
   if (s->attached) return ARENA_OK;
   DeviceGuard g(s->base->device);
   SlabRank& me = s->ranks[0];
+  std::vector<std::vector<void*>> ptrs;
+  arena_status st = s->sync.attach(all, s->P, s->rank, {me.B, me.C}, ptrs);
+  if (st != ARENA_OK) return st;
   const size_t cb = s->chunk_elems * s->base->elem;
   for (int d = 0; d < s->P; ++d) {
-    void* ptr[3] = {me.B, me.C, s->flags};
-    if (d != s->rank) {
-      cudaIpcMemHandle_t h[3];
-      memcpy(h, static_cast<const char*>(all) + size_t(d) * hb, sizeof h);
-      for (int k = 0; k < 3; ++k) {
-        cudaError_t e = cudaIpcOpenMemHandle(&ptr[k], h[k], cudaIpcMemLazyEnablePeerAccess);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
-        s->opened.push_back(ptr[k]);
-      }
-    }
-    me.peerB[d] = static_cast<char*>(ptr[0]) + size_t(s->rank) * cb;
-    me.peerC[d] = static_cast<char*>(ptr[1]) + size_t(s->rank) * cb;
-    s->pflags.peer[d] = static_cast<unsigned*>(ptr[2]);
+    me.peerB[d] = static_cast<char*>(ptrs[d][0]) + size_t(s->rank) * cb;
+    me.peerC[d] = static_cast<char*>(ptrs[d][1]) + size_t(s->rank) * cb;
   }
-  s->pflags.mine = s->flags;
   s->attached = true;
   s->xmode = ARENA_XCHG_PEER;
   return ARENA_OK;
@@ -1048,10 +1088,7 @@ arena_status arena_slab_set_exchange(arena_fft_slab* s, int mode) {
 arena_status arena_slab_barrier_status(arena_fft_slab* s) {
   if (!s) return fail(ARENA_EINVAL, "slab is NULL");
   DeviceGuard g(s->base->device);
-  int h = 0;
-  cudaError_t e = cudaMemcpy(&h, s->err, sizeof h, cudaMemcpyDeviceToHost);
-  if (e != cudaSuccess) return cuda_fail(e, "barrier status");
-  return h ? fail(ARENA_ECUDA, "peer barrier timed out (a rank did not arrive within 20 s)") : ARENA_OK;
+  return s->sync.status();
 }
 
 arena_status arena_peer_barrier_selftest(int device, int nranks, int rounds, int* bad) {
@@ -1102,6 +1139,11 @@ struct PencilRank {
   void* fblk = nullptr;  // loopback only: the rank's f / u blocks
   void* ublk = nullptr;
   TmaCache tma, tma2;
+  // Peer exchange destinations (PencilArgs::pz ...), per row / column peer q.
+  void* pz[kMaxPeers] = {};
+  void* py1[kMaxPeers] = {};
+  void* px[kMaxPeers] = {};
+  void* py2[kMaxPeers] = {};
 };
 
 }  // namespace
@@ -1112,6 +1154,11 @@ struct arena_fft_pencil {
   size_t buf_bytes = 0, blk_bytes = 0;
   std::vector<PencilRank> ranks;
   ncclComm_t world = nullptr, row = nullptr, col = nullptr;
+  int xmode = ARENA_XCHG_COPY;
+  bool attached = false;
+  PeerSync sync;
+  size_t row_chunk_bytes() const { return size_t(n / Pr) * (n / Pc) * kq * 2 * base->elem; }
+  size_t col_chunk_bytes() const { return size_t(n / Pr) * (n / Pr) * kq * 2 * base->elem; }
 };
 
 namespace {
@@ -1123,6 +1170,7 @@ void free_pencil(arena_fft_pencil* s) {
     for (PencilRank& r : s->ranks)
       for (void* p : {r.buf1, r.buf2, r.fblk, r.ublk})
         if (p) cudaFree(p);
+    s->sync.release();
     if (NcclApi* a = nccl_api()) {
       for (ncclComm_t c : {s->row, s->col, s->world})
         if (c) a->CommDestroy(c);
@@ -1175,7 +1223,11 @@ arena_status pencil_init(arena_fft_pencil** out, int n, int prec, int device, in
       return fail(ARENA_ENOMEM, "pencil buffers: " + std::string(cudaGetErrorString(e)));
     }
   }
-  if (!loopback) {
+  if (cudaError_t e = s->sync.init(Pr * Pc)) {
+    free_pencil(s);
+    return fail(ARENA_ENOMEM, "pencil barrier flags: " + std::string(cudaGetErrorString(e)));
+  }
+  if (!loopback && id) {
     NcclApi* a = nccl_api();
     auto split = reinterpret_cast<ncclResult_t (*)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*)>(
         a ? dlsym(a->h, "ncclCommSplit") : nullptr);
@@ -1221,7 +1273,27 @@ PencilArgs pencil_args(arena_fft_pencil* s, PencilRank& pr, int rank, const void
   a.tma = &pr.tma;
   a.tma2 = &pr.tma2;
   a.sm_count = p->sm_count;
+  if (s->xmode == ARENA_XCHG_PEER) {
+    a.pz = pr.pz;
+    a.py1 = pr.py1;
+    a.px = pr.px;
+    a.py2 = pr.py2;
+  }
   return a;
+}
+
+// Peer destinations of virtual rank rk = (r, c) given every rank's buffers.
+void pencil_fill_peers(arena_fft_pencil* s, PencilRank& me, int rk, const std::vector<std::vector<void*>>& bufs) {
+  const int r = rk / s->Pc, c = rk % s->Pc;
+  const size_t rb = s->row_chunk_bytes(), cb = s->col_chunk_bytes();
+  for (int q = 0; q < s->Pc; ++q) {  // row peers (r, q)
+    me.pz[q] = static_cast<char*>(bufs[r * s->Pc + q][1]) + size_t(c) * rb;
+    me.py2[q] = static_cast<char*>(bufs[r * s->Pc + q][0]) + size_t(c) * rb;
+  }
+  for (int q = 0; q < s->Pr; ++q) {  // column peers (q, c)
+    me.py1[q] = static_cast<char*>(bufs[q * s->Pc + c][0]) + size_t(r) * cb;
+    me.px[q] = static_cast<char*>(bufs[q * s->Pc + c][1]) + size_t(r) * cb;
+  }
 }
 
 // Row (same r) or column (same c) all-to-all from buf `from` to buf `to`
@@ -1280,7 +1352,11 @@ arena_status arena_pencil_create_loopback(arena_fft_pencil** out, int n, int pre
 
 void arena_pencil_destroy(arena_fft_pencil* s) { free_pencil(s); }
 
-int arena_pencil_launches_per_solve(const arena_fft_pencil* s) { return s ? 5 : 0; }
+int arena_pencil_launches_per_solve(const arena_fft_pencil* s) {
+  if (!s) return 0;
+  const bool barrier = s->xmode == ARENA_XCHG_PEER && !s->loopback && s->Pr * s->Pc > 1;
+  return 5 * int(s->ranks.size()) + (barrier ? 4 : 0);
+}
 
 arena_status arena_pencil_info(const arena_fft_pencil* s, int* kq, size_t* buffer_bytes, size_t* block_bytes) {
   if (!s) return fail(ARENA_EINVAL, "pencil is NULL");
@@ -1290,16 +1366,19 @@ arena_status arena_pencil_info(const arena_fft_pencil* s, int* kq, size_t* buffe
   return ARENA_OK;
 }
 
-arena_status arena_pencil_solve_device(arena_fft_pencil* s, const void* d_f, void* d_u, void* stream) {
-  if (!s || !d_f || !d_u) return fail(ARENA_EINVAL, "NULL pencil or buffer");
-  DeviceGuard g(s->base->device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+// Phase p of a pencil solve: 0 K1 (+ row exchange), 1 K2 (+ column exchange),
+// 2 K3 (+ column exchange back), 3 K4 (+ row exchange back), 4 K5.  Loopback
+// phases 0 / 4 also scatter f into / gather u from the virtual ranks' blocks.
+static arena_status pencil_run_phase(arena_fft_pencil* s, int phase, const void* d_f, void* d_u, cudaStream_t st) {
+  static const int kPh[5] = {kPencilZ1, kPencilY1, kPencilX, kPencilY2, kPencilZ2};
+  if (phase < 0 || phase > 4) return fail(ARENA_EINVAL, "pencil phase must be 0 .. 4");
+  if (s->xmode == ARENA_XCHG_PEER && !s->loopback && !s->attached)
+    return fail(ARENA_EINVAL, "peer exchange: call arena_pencil_peer_attach first");
   const int n = s->n, ni = n / s->Pr, nj = n / s->Pc;
   const size_t elem = s->base->elem;
   const int nr = int(s->ranks.size());
   cudaError_t e;
-  // loopback: scatter the full field into the virtual ranks' blocks
-  if (s->loopback) {
+  if (s->loopback && phase == 0) {  // scatter the full field into the virtual ranks' blocks
     for (int rk = 0; rk < nr; ++rk) {
       const int r = rk / s->Pc, c = rk % s->Pc;
       const char* src = static_cast<const char*>(d_f) + (size_t(r) * ni * n + size_t(c) * nj) * n * elem;
@@ -1308,29 +1387,24 @@ arena_status arena_pencil_solve_device(arena_fft_pencil* s, const void* d_f, voi
         return cuda_fail(e, "pencil scatter");
     }
   }
-  auto run = [&](int phase) -> arena_status {
-    for (int v = 0; v < nr; ++v) {
-      const int rank = s->loopback ? v : s->rank;
-      PencilRank& pr = s->ranks[v];
-      const void* f = s->loopback ? pr.fblk : d_f;
-      void* u = s->loopback ? pr.ublk : d_u;
-      const PencilArgs a = pencil_args(s, pr, rank, f, u, st);
-      cudaError_t err = s->base->prec == 64 ? pencil_phase_f64(a, phase) : pencil_phase_f32(a, phase);
-      if (err != cudaSuccess) return cuda_fail(err, "pencil phase");
-    }
-    return ARENA_OK;
-  };
-  arena_status r;
-  if ((r = run(kPencilZ1)) != ARENA_OK) return r;
-  if ((r = pencil_exchange(s, st, true, 1, 2)) != ARENA_OK) return r;   // R -> Y
-  if ((r = run(kPencilY1)) != ARENA_OK) return r;                       // Y -> B2
-  if ((r = pencil_exchange(s, st, false, 1, 2)) != ARENA_OK) return r;  // B2 -> C
-  if ((r = run(kPencilX)) != ARENA_OK) return r;
-  if ((r = pencil_exchange(s, st, false, 2, 1)) != ARENA_OK) return r;  // C -> B2
-  if ((r = run(kPencilY2)) != ARENA_OK) return r;                       // B2 -> Y
-  if ((r = pencil_exchange(s, st, true, 2, 1)) != ARENA_OK) return r;   // Y -> R
-  if ((r = run(kPencilZ2)) != ARENA_OK) return r;
-  if (s->loopback) {
+  for (int v = 0; v < nr; ++v) {
+    const int rank = s->loopback ? v : s->rank;
+    PencilRank& pr = s->ranks[v];
+    const void* f = s->loopback ? pr.fblk : d_f;
+    void* u = s->loopback ? pr.ublk : d_u;
+    const PencilArgs a = pencil_args(s, pr, rank, f, u, st);
+    cudaError_t err = s->base->prec == 64 ? pencil_phase_f64(a, kPh[phase]) : pencil_phase_f32(a, kPh[phase]);
+    if (err != cudaSuccess) return cuda_fail(err, "pencil phase");
+  }
+  if (s->xmode != ARENA_XCHG_PEER) {
+    arena_status r = ARENA_OK;
+    if (phase == 0) r = pencil_exchange(s, st, true, 1, 2);   // R -> Y
+    if (phase == 1) r = pencil_exchange(s, st, false, 1, 2);  // B2 -> C
+    if (phase == 2) r = pencil_exchange(s, st, false, 2, 1);  // C -> B2
+    if (phase == 3) r = pencil_exchange(s, st, true, 2, 1);   // Y -> R
+    if (r != ARENA_OK) return r;
+  }
+  if (s->loopback && phase == 4) {
     for (int rk = 0; rk < nr; ++rk) {
       const int rr = rk / s->Pc, c = rk % s->Pc;
       char* dst = static_cast<char*>(d_u) + (size_t(rr) * ni * n + size_t(c) * nj) * n * elem;
@@ -1340,6 +1414,85 @@ arena_status arena_pencil_solve_device(arena_fft_pencil* s, const void* d_f, voi
     }
   }
   return ARENA_OK;
+}
+
+arena_status arena_pencil_solve_device(arena_fft_pencil* s, const void* d_f, void* d_u, void* stream) {
+  if (!s || !d_f || !d_u) return fail(ARENA_EINVAL, "NULL pencil or buffer");
+  DeviceGuard g(s->base->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int P = s->Pr * s->Pc;
+  const bool barrier = s->xmode == ARENA_XCHG_PEER && !s->loopback && P > 1;
+  for (int phase = 0; phase < 5; ++phase) {
+    arena_status r = pencil_run_phase(s, phase, d_f, d_u, st);
+    if (r != ARENA_OK) return r;
+    if (barrier && phase < 4 && (r = s->sync.barrier(st, s->rank, P)) != ARENA_OK) return r;
+  }
+  return ARENA_OK;
+}
+
+arena_status arena_pencil_solve_phase(arena_fft_pencil* s, int phase, const void* d_f, void* d_u, void* stream) {
+  if (!s || !d_f || !d_u) return fail(ARENA_EINVAL, "NULL pencil or buffer");
+  DeviceGuard g(s->base->device);
+  return pencil_run_phase(s, phase, d_f, d_u, static_cast<cudaStream_t>(stream));
+}
+
+arena_status arena_pencil_create_peer(arena_fft_pencil** out, int n, int precision_bits, int device, int pr, int pc,
+                                      int rank) {
+  if (pr * pc > kMaxPeers) return fail(ARENA_EUNSUPPORTED, "peer exchange supports at most 8 ranks");
+  arena_status st = pencil_init(out, n, precision_bits, device, pr, pc, rank, 0, nullptr);
+  if (st == ARENA_OK) (*out)->xmode = ARENA_XCHG_PEER;
+  return st;
+}
+
+int arena_pencil_peer_handle_bytes(void) { return int(3 * sizeof(cudaIpcMemHandle_t)); }
+
+arena_status arena_pencil_peer_export(arena_fft_pencil* s, void* out, int len) {
+  if (!s || !out || len < arena_pencil_peer_handle_bytes()) return fail(ARENA_EINVAL, "handle buffer too small");
+  if (s->loopback) return fail(ARENA_EINVAL, "loopback pencils have no peers to export to");
+  DeviceGuard g(s->base->device);
+  return s->sync.export_handles({s->ranks[0].buf1, s->ranks[0].buf2}, out);
+}
+
+arena_status arena_pencil_peer_attach(arena_fft_pencil* s, const void* all, int len) {
+  const int P = s ? s->Pr * s->Pc : 0;
+  if (!s || !all || len < arena_pencil_peer_handle_bytes() * P) return fail(ARENA_EINVAL, "need every rank's handles");
+  if (s->loopback) return fail(ARENA_EINVAL, "loopback pencils need no attach");
+  if (P > kMaxPeers) return fail(ARENA_EUNSUPPORTED, "peer exchange supports at most 8 ranks");
+  if (s->attached) return ARENA_OK;
+  DeviceGuard g(s->base->device);
+  std::vector<std::vector<void*>> bufs;
+  arena_status st = s->sync.attach(all, P, s->rank, {s->ranks[0].buf1, s->ranks[0].buf2}, bufs);
+  if (st != ARENA_OK) return st;
+  pencil_fill_peers(s, s->ranks[0], s->rank, bufs);
+  s->attached = true;
+  s->xmode = ARENA_XCHG_PEER;
+  return ARENA_OK;
+}
+
+arena_status arena_pencil_set_exchange(arena_fft_pencil* s, int mode) {
+  if (!s) return fail(ARENA_EINVAL, "pencil is NULL");
+  if (mode == ARENA_XCHG_COPY) {
+    if (!s->loopback && !s->world) return fail(ARENA_EINVAL, "this pencil has no NCCL communicators");
+    s->xmode = mode;
+    return ARENA_OK;
+  }
+  if (mode != ARENA_XCHG_PEER) return fail(ARENA_EINVAL, "unknown exchange mode");
+  if (s->Pr * s->Pc > kMaxPeers) return fail(ARENA_EUNSUPPORTED, "peer exchange supports at most 8 ranks");
+  if (s->loopback) {
+    std::vector<std::vector<void*>> bufs;
+    for (PencilRank& r : s->ranks) bufs.push_back({r.buf1, r.buf2});
+    for (int rk = 0; rk < int(s->ranks.size()); ++rk) pencil_fill_peers(s, s->ranks[rk], rk, bufs);
+  } else if (!s->attached) {
+    return fail(ARENA_EINVAL, "peer exchange: call arena_pencil_peer_attach first");
+  }
+  s->xmode = mode;
+  return ARENA_OK;
+}
+
+arena_status arena_pencil_barrier_status(arena_fft_pencil* s) {
+  if (!s) return fail(ARENA_EINVAL, "pencil is NULL");
+  DeviceGuard g(s->base->device);
+  return s->sync.status();
 }
 
 }  // extern "C"

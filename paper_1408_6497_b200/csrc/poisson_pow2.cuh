@@ -654,10 +654,12 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2)>::THREADS, TmaCfg<T, N
 // back.  Inside a chunk rows are in Layout(ni, nj) order.
 namespace arena_fft {
 
-template <typename T, int NR>
+// PEER: k-chunk c goes straight to po.base[c] (row peer c's Y buffer, advanced
+// to this rank's chunk) instead of chunk c of R — the row all-to-all fused into K1.
+template <typename T, int NR, bool PEER = false>
 __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
     k_zfwd_pencil(const T* __restrict__ f, vec2_t<T>* __restrict__ R, const vec2_t<T>* __restrict__ tw,
-                  const vec2_t<T>* __restrict__ stw, Layout gz, int kq) {
+                  const vec2_t<T>* __restrict__ stw, Layout gz, int kq, const __grid_constant__ PeerOut<vec2_t<T>> po) {
   using V = vec2_t<T>;
   using C = ContigCfg<T, NR>;
   constexpr int M = C::M, E = C::E, P = C::P, L = C::L;
@@ -677,7 +679,11 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
   const size_t chunk = size_t(gz.ni) * gz.nj;
   auto put = [&](int k, V x) {
     const int c = k / kq;
-    R[(size_t(c) * chunk + rin) * kq + (k - c * kq)] = x;
+    if constexpr (PEER) {
+      po.base[c][rin * kq + (k - c * kq)] = x;
+    } else {
+      R[(size_t(c) * chunk + rin) * kq + (k - c * kq)] = x;
+    }
   };
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -690,6 +696,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
     put(k, V{T(0.5) * (A.x + B.x + WD.y), T(0.5) * (A.y + B.y - WD.x)});
     if (k == 0) put(M, V{A.x - A.y, T(0)});
   }
+  if constexpr (PEER) __threadfence_system();
 }
 
 template <typename T, int NR>

@@ -324,6 +324,8 @@ cudaError_t pencil_phase_n(const PencilArgs& a, int phase) {
     if ((e = encode_map<T, NR>(a.tma->maps[0], a.buf2, gY, a.Pc, true, ks.kc, ks.kq))) return e;
     if ((e = encode_map<T, NR>(a.tma->maps[1], a.buf2, gC, a.Pr, false, ks.kc, ks.kq))) return e;
     if ((e = encode_map<T, NR>(a.tma2->maps[0], a.buf1, gB2, a.Pr, true, ks.kc, ks.kq))) return e;
+    if ((e = encode_map<T, NR>(a.tma2->maps[1], a.buf1, gC, a.Pr, false, ks.kc, ks.kq))) return e;
+    if ((e = encode_map<T, NR>(a.tma2->maps[2], a.buf2, gB2, a.Pr, true, ks.kc, ks.kq))) return e;
     a.tma->specB = a.buf2;
     a.tma->n = NR;
     a.tma->ni = ni;
@@ -333,29 +335,59 @@ cudaError_t pencil_phase_n(const PencilArgs& a, int phase) {
   const CUtensorMap& mY = *reinterpret_cast<const CUtensorMap*>(a.tma->maps[0]);
   const CUtensorMap& mC = *reinterpret_cast<const CUtensorMap*>(a.tma->maps[1]);
   const CUtensorMap& mB2 = *reinterpret_cast<const CUtensorMap*>(a.tma2->maps[0]);
+  const CUtensorMap& mC1 = *reinterpret_cast<const CUtensorMap*>(a.tma2->maps[1]);   // peer: C in buf1
+  const CUtensorMap& mB2b = *reinterpret_cast<const CUtensorMap*>(a.tma2->maps[2]);  // peer: B2 in buf2
+  const bool peer = a.pz != nullptr;
+  const size_t rows_row = size_t(ni) * nj, rows_col = size_t(ni) * nj2;  // rows per row / column chunk
   const V* tw = static_cast<const V*>(a.tw);
   const V* stwz = static_cast<const V*>(a.stw) + stw_offset(NR, 0, CC::E);
   const unsigned zgrid = unsigned((size_t(ni) * nj) / CC::L);
   switch (phase) {
     case kPencilZ1:
+      if (peer) {
+        if ((e = ensure_smem<k_zfwd_pencil<T, NR, true>>(CC::SMEM, CC::THREADS))) return e;
+        const PeerOut<V> po = peer_table<V>(a.pz, a.Pc, rows_row);
+        k_zfwd_pencil<T, NR, true><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f), nullptr,
+                                                                                tw, stwz, gz, a.kq, po);
+        break;
+      }
       if ((e = ensure_smem<k_zfwd_pencil<T, NR>>(CC::SMEM, CC::THREADS))) return e;
       k_zfwd_pencil<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f),
-                                                                      static_cast<V*>(a.buf1), tw, stwz, gz, a.kq);
+                                                                      static_cast<V*>(a.buf1), tw, stwz, gz, a.kq,
+                                                                      PeerOut<V>{});
       break;
-    case kPencilY1:  // Y (buf2) -> B2 (buf1)
+    case kPencilY1:  // Y (buf2) -> B2 (buf1); peer: -> column peers' C (buf1)
       if (!has_k) break;
       pa.nchunks = a.Pc;
-      if ((e = launch_strided_tma<T, NR, 0>(pa, mY, a.buf2, gY, scale, four_pi2, ks, a.buf1, &gB2))) return e;
+      if (peer) {
+        const PeerOut<V> po = peer_table<V>(a.py1, a.Pr, rows_col);
+        e = launch_strided_tma<T, NR, 0, true>(pa, mY, a.buf2, gY, scale, four_pi2, ks, nullptr, &gB2, &po);
+      } else {
+        e = launch_strided_tma<T, NR, 0>(pa, mY, a.buf2, gY, scale, four_pi2, ks, a.buf1, &gB2);
+      }
+      if (e) return e;
       break;
-    case kPencilX:
+    case kPencilX:  // C (buf2) in place; peer: C (buf1) -> column peers' B2 (buf2)
       if (!has_k) break;
       pa.nchunks = a.Pr;
-      if ((e = launch_strided_tma<T, NR, 2>(pa, mC, a.buf2, gC, scale, four_pi2, ks))) return e;
+      if (peer) {
+        const PeerOut<V> po = peer_table<V>(a.px, a.Pr, rows_col);
+        e = launch_strided_tma<T, NR, 2, true>(pa, mC1, a.buf1, gC, scale, four_pi2, ks, nullptr, nullptr, &po);
+      } else {
+        e = launch_strided_tma<T, NR, 2>(pa, mC, a.buf2, gC, scale, four_pi2, ks);
+      }
+      if (e) return e;
       break;
-    case kPencilY2:  // B2 (buf1) -> Y (buf2)
+    case kPencilY2:  // B2 (buf1) -> Y (buf2); peer: B2 (buf2) -> row peers' R (buf1)
       if (!has_k) break;
       pa.nchunks = a.Pr;
-      if ((e = launch_strided_tma<T, NR, 1>(pa, mB2, a.buf1, gB2, scale, four_pi2, ks, a.buf2, &gY))) return e;
+      if (peer) {
+        const PeerOut<V> po = peer_table<V>(a.py2, a.Pc, rows_row);
+        e = launch_strided_tma<T, NR, 1, true>(pa, mB2b, a.buf2, gB2, scale, four_pi2, ks, nullptr, &gY, &po);
+      } else {
+        e = launch_strided_tma<T, NR, 1>(pa, mB2, a.buf1, gB2, scale, four_pi2, ks, a.buf2, &gY);
+      }
+      if (e) return e;
       break;
     case kPencilZ2:
       if ((e = ensure_smem<k_zinv_pencil<T, NR>>(CC::SMEM, CC::THREADS))) return e;

@@ -422,6 +422,89 @@ def test_pencil_loopback_vs_oracle(cuda, n, pr, pc):
     assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64
 
 
+@pytest.mark.parametrize("n,pr,pc", [(64, 2, 2), (64, 1, 4), (128, 2, 4), (128, 4, 2), (256, 2, 2), (256, 2, 1),
+                                     (64, 1, 1)])
+def test_pencil_peer_loopback_vs_oracle(cuda, n, pr, pc):
+    """Pencil with the exchanges fused into K1-K4 (peer stores into the row / column
+    peers' buffers), Pr x Pc virtual ranks on one GPU, against the oracle."""
+    torch = cuda
+    f_np = np.random.default_rng(7 * n + 10 * pr + pc).uniform(-1, 1, (n, n, n))
+    f = torch.from_numpy(f_np).cuda()
+    u = torch.empty_like(f)
+    p = arena.Pencil(n, pr, pc, loopback=True)
+    p.set_exchange(arena.XCHG_PEER)
+    p.solve_device(f, u)
+    torch.cuda.synchronize()
+    assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64
+
+
+def test_pencil_peer_loopback_1024_2x4_analytic(cuda):
+    torch = cuda
+    src, f, ua = _config_device(torch, 4)
+    u = torch.empty_like(f)
+    p = arena.Pencil(1024, 2, 4, loopback=True)
+    p.set_exchange(arena.XCHG_PEER)
+    p.solve_device(f, u)
+    r = arena.field_compare(u, ua)
+    assert r["rel_l2"] <= 1e-12, r
+
+
+def _pencil_ipc_rank(rank, world, port, n, pr, pc, f_np, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    ni, nj = n // pr, n // pc
+    r, c = rank // pc, rank % pc
+    blk = np.ascontiguousarray(f_np[r * ni:(r + 1) * ni, c * nj:(c + 1) * nj])
+    f = torch.from_numpy(blk).cuda()
+    u = torch.empty_like(f)
+    p = arena.Pencil(n, pr, pc, rank=rank, peer=True, device=0)
+    hs = [None] * world
+    dist.all_gather_object(hs, p.peer_handles())
+    p.peer_attach(b"".join(hs))
+    for phase in range(5):  # one GPU shared by the ranks: host barriers between the phases
+        p.solve_phase(phase, f, u)
+        torch.cuda.synchronize()
+        dist.barrier()
+    us = [None] * world
+    dist.all_gather_object(us, u.cpu().numpy())
+    if rank == 0:
+        full = np.empty((n, n, n))
+        for q, b in enumerate(us):
+            rr, cc = q // pc, q % pc
+            full[rr * ni:(rr + 1) * ni, cc * nj:(cc + 1) * nj] = b
+        out.copy_(torch.from_numpy(full.ravel()))
+    dist.barrier()
+    p.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("pr,pc", [(1, 2), (2, 1)])
+def test_pencil_peer_ipc_two_processes(cuda, pr, pc):
+    """Two processes sharing this GPU as a 1x2 / 2x1 pencil grid, buffers mapped
+    with CUDA IPC, peer-store kernels, host barriers between the phases."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    torch = cuda
+    n = 64
+    f_np = np.random.default_rng(78 + pr).uniform(-1, 1, (n, n, n))
+    out = torch.zeros(n ** 3, dtype=torch.float64).share_memory_()
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    mp.spawn(_pencil_ipc_rank, args=(2, port, n, pr, pc, f_np, out), nprocs=2, join=True)
+    assert _rel(out.numpy().reshape(n, n, n), oracle.poisson_solve(f_np)) <= TOL64
+
+
 def test_pencil_loopback_1024_2x4_analytic(cuda):
     torch = cuda
     src, f, ua = _config_device(torch, 4)

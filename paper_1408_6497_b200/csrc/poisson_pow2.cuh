@@ -41,6 +41,9 @@ __host__ __device__ constexpr int spec_pitch(int n) { return (n / 2 + 1 + 7) / 8
 #ifndef ARENA_STRIDED_E
 #define ARENA_STRIDED_E 16  // points per thread, y / x kernels
 #endif
+#ifndef ARENA_CONTIG_SMALL_N
+#define ARENA_CONTIG_SMALL_N 512  // B200: 512^3 z passes 0.50 -> 0.39 ms, 256^3 0.10 -> 0.07 ms
+#endif
 #ifndef ARENA_CONTIG_E
 #define ARENA_CONTIG_E 32  // points per thread, z kernels
 #endif
@@ -77,7 +80,12 @@ struct StridedCfg {  // y (PASS 0) / x (PASS 1) passes: lines along a strided ax
 template <typename T, int NR>
 struct ContigCfg {  // z passes: rows of NR reals = M = NR/2 complex
   static constexpr int M = NR / 2;
-  static constexpr int E = imin(ARENA_CONTIG_E, M);
+  // Short rows (n <= ARENA_CONTIG_SMALL_N): 16 points per thread and twice the
+  // resident warps (B200, 256^3: z passes 0.10 -> 0.07 ms; at n = 1024 E = 16
+  // with 16 CTAs/SM spills).
+  static constexpr bool SMALL = NR <= ARENA_CONTIG_SMALL_N;
+  static constexpr int E = imin(SMALL ? 16 : ARENA_CONTIG_E, M);
+  static constexpr int MINB = SMALL ? 2 * ARENA_CONTIG_MINB : ARENA_CONTIG_MINB;
   static constexpr int P = M / E;
   static constexpr int VB = 2 * sizeof(T);
   // rows per CTA (a power of two, so it divides the n^2 rows): aim for 256
@@ -206,7 +214,7 @@ __device__ __forceinline__ void zfwd_rows(const T* __restrict__ f, vec2_t<T>* __
 }
 
 template <typename T, int NR>
-__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
+__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::MINB)
     k_zfwd(const T* __restrict__ f, vec2_t<T>* __restrict__ S, const vec2_t<T>* __restrict__ tw,
            const vec2_t<T>* __restrict__ stw, Layout g) {
   using C = ContigCfg<T, NR>;
@@ -272,7 +280,7 @@ __device__ __forceinline__ void zinv_rows(const vec2_t<T>* __restrict__ S, T* __
 }
 
 template <typename T, int NR>
-__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
+__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::MINB)
     k_zinv(const vec2_t<T>* __restrict__ S, T* __restrict__ u, const vec2_t<T>* __restrict__ tw,
            const vec2_t<T>* __restrict__ stw, Layout g) {
   using C = ContigCfg<T, NR>;
@@ -406,6 +414,9 @@ namespace arena_fft {
 #ifndef ARENA_TMA_LROW
 #define ARENA_TMA_LROW 128  // bytes of a tile row (L adjacent k) at most
 #endif
+#ifndef ARENA_TMA_Y_SMALL
+#define ARENA_TMA_Y_SMALL 65536  // tile bytes up to which the y passes run two CTAs per SM (512^3: y 0.53 -> 0.46 ms)
+#endif
 #ifndef ARENA_TMA_E32
 #define ARENA_TMA_E32 32
 #endif
@@ -434,8 +445,10 @@ struct TmaCfg {
   static constexpr int P = N / E;
   static constexpr int BUDGET = YP ? (F64 ? ARENA_TMA_Y_TILE : ARENA_TMA_Y_TILE32)
                                    : (F64 ? ARENA_TMA_X_TILE : ARENA_TMA_X_TILE32);
-  static constexpr int MINB = YP ? (F64 ? ARENA_TMA_MINB_Y : ARENA_TMA_MINB_Y32) : (F64 ? ARENA_TMA_MINB : ARENA_TMA_MINB32);
   static constexpr int L = pow2_floor(imax(2, imin(ARENA_TMA_LROW / VB, BUDGET / (N * VB))));
+  static constexpr int MINB0 = YP ? (F64 ? ARENA_TMA_MINB_Y : ARENA_TMA_MINB_Y32) : (F64 ? ARENA_TMA_MINB : ARENA_TMA_MINB32);
+  // y passes with tiles of <= 64 KB (n <= 512): two CTAs per SM
+  static constexpr int MINB = (YP && N * L * VB <= ARENA_TMA_Y_SMALL) ? imax(MINB0, 2) : MINB0;
   static constexpr int THREADS = L * P;
   static constexpr int NC = N / 2 + 1;
   static constexpr int KT = (NC + L - 1) / L;  // k tiles per line set
@@ -657,7 +670,7 @@ namespace arena_fft {
 // PEER: k-chunk c goes straight to po.base[c] (row peer c's Y buffer, advanced
 // to this rank's chunk) instead of chunk c of R — the row all-to-all fused into K1.
 template <typename T, int NR, bool PEER = false>
-__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
+__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::MINB)
     k_zfwd_pencil(const T* __restrict__ f, vec2_t<T>* __restrict__ R, const vec2_t<T>* __restrict__ tw,
                   const vec2_t<T>* __restrict__ stw, Layout gz, int kq, const __grid_constant__ PeerOut<vec2_t<T>> po) {
   using V = vec2_t<T>;
@@ -700,7 +713,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
 }
 
 template <typename T, int NR>
-__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ARENA_CONTIG_MINB)
+__global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::MINB)
     k_zinv_pencil(const vec2_t<T>* __restrict__ R, T* __restrict__ u, const vec2_t<T>* __restrict__ tw,
                   const vec2_t<T>* __restrict__ stw, Layout gz, int kq) {
   using V = vec2_t<T>;

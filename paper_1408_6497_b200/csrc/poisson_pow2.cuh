@@ -144,6 +144,15 @@ inline Layout make_layout(int ni, int nj) {
   return g;
 }
 
+// The single-GPU geometry (one chunk of n x n rows, full k range, in
+// place) as compile-time constants, so every row / address computation folds
+// into constant strides (kernels with FIXED = true ignore their runtime geometry).
+__host__ __device__ constexpr int ilog2_c(int x) { return x <= 1 ? 0 : 1 + ilog2_c(x >> 1); }
+template <int N>
+__host__ __device__ constexpr Layout fixed_layout() {
+  return Layout{N, N, ilog2_c(N), ilog2_c(N), ilog2_c(N < ARENA_JBLOCK ? N : ARENA_JBLOCK)};
+}
+
 // The Poisson symbol of fft_solver.cpp:66-79, k2 == 0 ? 0 : scale / (four_pi2 * k2),
 // with the division done as a hardware reciprocal estimate refined by Newton
 // steps (no slow path / divergence); within 2 ulp of the IEEE quotient.
@@ -213,11 +222,12 @@ __device__ __forceinline__ void zfwd_rows(const T* __restrict__ f, vec2_t<T>* __
   }
 }
 
-template <typename T, int NR>
+template <typename T, int NR, bool FIXED = false>
 __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::MINB)
     k_zfwd(const T* __restrict__ f, vec2_t<T>* __restrict__ S, const vec2_t<T>* __restrict__ tw,
-           const vec2_t<T>* __restrict__ stw, Layout g) {
+           const vec2_t<T>* __restrict__ stw, Layout g_) {
   using C = ContigCfg<T, NR>;
+  const Layout g = FIXED ? fixed_layout<NR>() : g_;
   zfwd_rows<T, NR, C::E, C::L, kSyncCta>(f, S, tw, stw, g, size_t(blockIdx.x) * C::L, smem_base<vec2_t<T>>(),
                                          threadIdx.x);
 }
@@ -279,11 +289,12 @@ __device__ __forceinline__ void zinv_rows(const vec2_t<T>* __restrict__ S, T* __
   for (int e = 0; e < E; ++e) st_out(dst + t + P * e, v[e]);
 }
 
-template <typename T, int NR>
+template <typename T, int NR, bool FIXED = false>
 __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::MINB)
     k_zinv(const vec2_t<T>* __restrict__ S, T* __restrict__ u, const vec2_t<T>* __restrict__ tw,
-           const vec2_t<T>* __restrict__ stw, Layout g) {
+           const vec2_t<T>* __restrict__ stw, Layout g_) {
   using C = ContigCfg<T, NR>;
+  const Layout g = FIXED ? fixed_layout<NR>() : g_;
   zinv_rows<T, NR, C::E, C::L, kSyncCta, false>(S, u, tw, stw, g, size_t(blockIdx.x) * C::L, smem_base<vec2_t<T>>(),
                                                 threadIdx.x);
 }
@@ -491,11 +502,18 @@ struct PeerOut {
   int shift;
 };
 
-template <typename T, int N, int PASS, bool PEER = false>
+template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false>
 __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2)>::THREADS, TmaCfg<T, N, (PASS < 2)>::MINB)
     k_strided_tma(const __grid_constant__ CUtensorMap tmap, vec2_t<T>* __restrict__ spec,
-                  const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g, int nchunks, int j0, KSpan ks,
-                  vec2_t<T>* __restrict__ out, Layout gout, const __grid_constant__ PeerOut<vec2_t<T>> po) {
+                  const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g_, int nchunks_, int j0_, KSpan ks_,
+                  vec2_t<T>* __restrict__ out_, Layout gout_, const __grid_constant__ PeerOut<vec2_t<T>> po) {
+  static_assert(!(FIXED && PEER), "the fixed geometry is the single-GPU one");
+  const Layout g = FIXED ? fixed_layout<N>() : g_;
+  const Layout gout = FIXED ? fixed_layout<N>() : gout_;
+  const int nchunks = FIXED ? 1 : nchunks_;
+  const int j0 = FIXED ? 0 : j0_;
+  const KSpan ks = FIXED ? KSpan{N / 2 + 1, spec_pitch(N), 0} : ks_;
+  vec2_t<T>* __restrict__ out = FIXED ? spec : out_;
   using V = vec2_t<T>;
   using C = TmaCfg<T, N, (PASS < 2)>;
   constexpr int E = C::E, P = C::P, L = C::L, TILE = C::TILE;

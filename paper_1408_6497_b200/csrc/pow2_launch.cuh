@@ -93,15 +93,15 @@ inline const vec2_t<T>* stw_ptr(const Pow2Args& a, int which, int E) {
   return static_cast<const vec2_t<T>*>(a.stw) + stw_offset(a.n, which, E);
 }
 
-template <typename T, int N, int PASS, bool PEER = false>
+template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false>
 cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* spec, const Layout& g, T scale,
                                T four_pi2, KSpan ks = KSpan{N / 2 + 1, spec_pitch(N), 0}, void* out = nullptr,
                                const Layout* gout = nullptr, const PeerOut<vec2_t<T>>* po = nullptr) {
   using C = TmaCfg<T, N, (PASS < 2)>;
   using V = vec2_t<T>;
-  auto kern = k_strided_tma<T, N, PASS, PEER>;
+  auto kern = k_strided_tma<T, N, PASS, PEER, FIXED>;
   constexpr int SMEM = PASS == 2 ? C::SMEM_X : C::SMEM_Y;
-  cudaError_t e = ensure_smem<k_strided_tma<T, N, PASS, PEER>>(SMEM, C::THREADS);
+  cudaError_t e = ensure_smem<k_strided_tma<T, N, PASS, PEER, FIXED>>(SMEM, C::THREADS);
   if (e) return e;
   PeerOut<V> pov{};
   if (po) pov = *po;
@@ -189,6 +189,8 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   if (size_t(a.ni) * NR % CC::L) return cudaErrorInvalidValue;
   if ((e = ensure_smem<k_zfwd<T, NR>>(CC::SMEM, CC::THREADS))) return e;
   if ((e = ensure_smem<k_zinv<T, NR>>(CC::SMEM, CC::THREADS))) return e;
+  if ((e = ensure_smem<k_zfwd<T, NR, true>>(CC::SMEM, CC::THREADS))) return e;
+  if ((e = ensure_smem<k_zinv<T, NR, true>>(CC::SMEM, CC::THREADS))) return e;
   const Layout gB = make_layout(a.ni, NR / a.nchunks);  // (local i, global j) chunks of nj
   const Layout gC = make_layout(NR / a.nchunks, a.nj);  // (global i, local j) chunks of ni
   const unsigned zgrid = unsigned((size_t(a.ni) * NR) / CC::L);
@@ -224,6 +226,10 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   const CUtensorMap* mys = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[3]) : nullptr;
   constexpr bool ys = ARENA_YSTREAM && YsCfg<T, NR>::OK;
   const KSpan kfull{NR / 2 + 1, spec_pitch(NR), 0};
+  // one GPU, in place: the x kernel's compile-time geometry (FIXED) applies (B200
+  // 1024^3: x 4.53 -> 4.32 ms fp64, 2.57 -> 2.20 ms fp32; the y passes measured
+  // slower that way, 1.72 -> 2.06 ms fp32, and keep the runtime geometry)
+  const bool single = a.nchunks == 1 && a.ni == NR && a.nj == NR && a.specC == a.spec && a.j0 == 0;
   int mk = 0;
   const bool fused = tma && a.ctrs != nullptr && FusedCfg<T, NR>::OK && !a.peer_y;
   if (fused && (a.fuse & kFuseFwd) && (a.phases & kPhaseZY)) {
@@ -233,8 +239,12 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
     }
   } else if (a.phases & kPhaseZY) {
     mark(a, mk++);
-    k_zfwd<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw,
-                                                               stw_ptr<T>(a, 0, CC::E), gB);
+    if (single)
+      k_zfwd<T, NR, true><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw,
+                                                                     stw_ptr<T>(a, 0, CC::E), gB);
+    else
+      k_zfwd<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw,
+                                                                 stw_ptr<T>(a, 0, CC::E), gB);
     mark(a, mk++);
     if (tma && a.peer_y) {
       if constexpr (NR >= kPeerMinN) {
@@ -265,7 +275,9 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
       }
       if (e) return e;
     } else if (tma) {
-      if ((e = launch_strided_tma<T, NR, 2>(a, *mx, a.specC, gC, scale, four_pi2))) return e;
+      if (single) e = launch_strided_tma<T, NR, 2, false, true>(a, *mx, a.specC, gC, scale, four_pi2);
+      else e = launch_strided_tma<T, NR, 2>(a, *mx, a.specC, gC, scale, four_pi2);
+      if (e) return e;
     } else {
       if ((e = ensure_smem<k_xmid<T, NR>>(XC::SMEM, XC::THREADS))) return e;
       k_xmid<T, NR><<<dim3((a.nc + XC::L - 1) / XC::L, NR), XC::THREADS, XC::SMEM, a.stream>>>(
@@ -290,8 +302,12 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
           S, stw_ptr<T>(a, 1, SC::E), gB);
     }
     mark(a, mk++);
-    k_zinv<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw, stw_ptr<T>(a, 0, CC::E),
-                                                               gB);
+    if (single)
+      k_zinv<T, NR, true><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw,
+                                                                     stw_ptr<T>(a, 0, CC::E), gB);
+    else
+      k_zinv<T, NR><<<zgrid, CC::THREADS, CC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw,
+                                                                 stw_ptr<T>(a, 0, CC::E), gB);
     mark(a, mk++);
   }
   return cudaGetLastError();

@@ -76,6 +76,42 @@ def test_random_pow2_vs_oracle(cuda, n):
     assert _rel(u, oracle.poisson_solve(f)) <= TOL64
 
 
+@pytest.mark.parametrize("n", [2, 256, 512])
+def test_random_pow2_large_vs_oracle(cuda, n):
+    f = np.random.default_rng(n + 1).uniform(-1, 1, (n, n, n))
+    u = _device_solve(cuda, f)
+    assert _rel(u, oracle.poisson_solve(f)) <= TOL64
+
+
+@pytest.mark.parametrize("n", [8, 32, 128, 512])
+def test_random_pow2_fp32_vs_oracle(cuda, n):
+    """fp32 kernels on random data: rel L2 <= 1e-5 vs the fp64 oracle."""
+    torch = cuda
+    f_np = np.random.default_rng(n + 2).uniform(-1, 1, (n, n, n))
+    f = torch.from_numpy(f_np).float().cuda()
+    u = torch.empty_like(f)
+    arena.get_plan(n, 32).solve_device(f, u)
+    torch.cuda.synchronize()
+    assert _rel(u.double().cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL32
+
+
+@pytest.mark.parametrize("kind", ["slab", "pencil"])
+@pytest.mark.parametrize("xchg", ["copy", "peer"])
+def test_decomposition_fp32_loopback(cuda, kind, xchg):
+    torch = cuda
+    n = 128
+    f_np = np.random.default_rng(5).uniform(-1, 1, (n, n, n))
+    f = torch.from_numpy(f_np).float().cuda()
+    u = torch.empty_like(f)
+    d = arena.Slab(n, 4, precision=32, loopback=True) if kind == "slab" else \
+        arena.Pencil(n, 2, 2, precision=32, loopback=True)
+    if xchg == "peer":
+        d.set_exchange(arena.XCHG_PEER)
+    d.solve_device(f, u)
+    torch.cuda.synchronize()
+    assert _rel(u.double().cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL32
+
+
 @pytest.mark.parametrize("n", [3, 6, 12, 18, 20, 24, 30, 36, 48, 96])
 def test_random_generic_vs_oracle(cuda, n):
     f = np.random.default_rng(n).uniform(-1, 1, (n, n, n))

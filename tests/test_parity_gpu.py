@@ -386,6 +386,35 @@ def test_field_compare_config4_1024(cuda):
     assert r["rel_l2"] <= 1e-12 and r["linf_rel"] <= 1e-12, r
 
 
+def test_concurrent_host_solves_one_plan(cuda):
+    """The reference solver is reentrant (fft_solver.cpp:10-11: only planning is
+    serialised); arena_poisson_solve_host on ONE plan from several threads at once
+    must serialise on the plan's own lock and give every caller its own answer."""
+    import threading
+
+    n = 64
+    p = arena.Plan(n)
+    fs = [np.random.default_rng(100 + i).uniform(-1, 1, (n, n, n)) for i in range(8)]
+    us = [np.empty_like(x) for x in fs]
+    errs = []
+
+    def worker(idx):
+        try:
+            for i in range(idx, len(fs), 4):
+                p.solve_host(fs[i], us[i])  # ctypes drops the GIL: the calls really overlap
+        except Exception as exc:  # pragma: no cover - reported below
+            errs.append(exc)
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for f, u in zip(fs, us):
+        assert _rel(u, oracle.poisson_solve(f)) <= TOL64
+
+
 def test_batched_host_solves(cuda):
     """arena_poisson_solve_host_batch (copy/compute overlap) == independent solves."""
     torch = cuda

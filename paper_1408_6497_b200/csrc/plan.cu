@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/arena_fft.h"
+#include "host_staging.h"
 #include "launchers.h"
 
 using namespace arena_fft;
@@ -98,6 +99,7 @@ struct arena_fft_plan {
   void* d_work = nullptr;  // n^3 complex, dft3 only
   cudaStream_t hstream = nullptr;
   std::mutex host_mu;  // one host-path call in flight per plan
+  Stager* stager = nullptr;  // pinned staging ring for pageable host buffers (lazy)
   // batched host path: double-buffered device fields, copy-in / copy-out streams
   void* bin[2] = {nullptr, nullptr};
   void* bout[2] = {nullptr, nullptr};
@@ -171,6 +173,7 @@ void free_plan(arena_fft_plan* p) {
   for (auto& ge : p->graphs) cudaGraphExecDestroy(ge.exec);
   if (p->s_out) cudaStreamDestroy(p->s_out);
   delete p->tma;
+  delete p->stager;
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   delete p;
 }
@@ -402,11 +405,25 @@ arena_status arena_poisson_solve_host(arena_fft_plan* p, const void* f, void* u)
   arena_status st = ensure_host_buffers(p, false);
   if (st != ARENA_OK) return st;
   const size_t bytes = p->real_bytes();
-  cudaError_t e = cudaMemcpyAsync(p->d_in, f, bytes, cudaMemcpyHostToDevice, p->hstream);
+  // Pageable buffers (a GridField's std::vector) go through the pinned staging ring.
+  const bool fpin = host_ptr_pinned(f), upin = host_ptr_pinned(u);
+  cudaError_t e;
+  if ((!fpin || !upin) && !p->stager) {
+    p->stager = new (std::nothrow) Stager;
+    if (!p->stager) return fail(ARENA_ENOMEM, "staging ring");
+    if ((e = p->stager->init()) != cudaSuccess) {
+      delete p->stager;
+      p->stager = nullptr;
+      return cuda_fail(e, "pinned staging buffers");
+    }
+  }
+  e = fpin ? cudaMemcpyAsync(p->d_in, f, bytes, cudaMemcpyHostToDevice, p->hstream)
+           : p->stager->h2d(p->d_in, f, bytes, p->hstream);
   if (e != cudaSuccess) return cuda_fail(e, "H2D f");
   if ((st = enqueue_solve(p, p->d_in, p->d_out, p->hstream)) != ARENA_OK) return st;
-  if ((e = cudaMemcpyAsync(u, p->d_out, bytes, cudaMemcpyDeviceToHost, p->hstream)) != cudaSuccess)
-    return cuda_fail(e, "D2H u");
+  e = upin ? cudaMemcpyAsync(u, p->d_out, bytes, cudaMemcpyDeviceToHost, p->hstream)
+           : p->stager->d2h(u, p->d_out, bytes, p->hstream);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H u");
   if ((e = cudaStreamSynchronize(p->hstream)) != cudaSuccess) return cuda_fail(e, "poisson solve");
   return ARENA_OK;
 }

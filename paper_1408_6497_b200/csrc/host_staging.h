@@ -113,7 +113,7 @@ class Stager {
       const int s = int(c % kSlots);
       const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
       cudaError_t e;
-      if (c >= size_t(kSlots) && (e = cudaEventSynchronize(ev_[s])) != cudaSuccess) return e;
+      if ((e = cudaEventSynchronize(ev_[s])) != cudaSuccess) return e;  // slot free (also across calls)
       pool_->copy(pin_[s], static_cast<const char*>(src) + off, len);
       if ((e = cudaMemcpyAsync(static_cast<char*>(dst) + off, pin_[s], len, cudaMemcpyHostToDevice, st))) return e;
       if ((e = cudaEventRecord(ev_[s], st)) != cudaSuccess) return e;

@@ -263,6 +263,28 @@ arena_status ensure_host_buffers(arena_fft_plan* p, bool work) {
   return ARENA_OK;
 }
 
+// Host <-> device copy on the plan's host stream: pinned buffers directly,
+// pageable ones through the staging ring (host_staging.h).  to_host waits.
+cudaError_t host_copy(arena_fft_plan* p, void* dst, const void* src, size_t bytes, bool to_host) {
+  const void* host = to_host ? dst : src;
+  if (host_ptr_pinned(host)) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice,
+                                    p->hstream);
+    return (e || !to_host) ? e : cudaStreamSynchronize(p->hstream);
+  }
+  if (!p->stager) {
+    p->stager = new (std::nothrow) Stager;
+    if (!p->stager) return cudaErrorMemoryAllocation;
+    cudaError_t e = p->stager->init();
+    if (e != cudaSuccess) {
+      delete p->stager;
+      p->stager = nullptr;
+      return e;
+    }
+  }
+  return to_host ? p->stager->d2h(dst, src, bytes, p->hstream) : p->stager->h2d(dst, src, bytes, p->hstream);
+}
+
 }  // namespace
 
 extern "C" {
@@ -405,26 +427,10 @@ arena_status arena_poisson_solve_host(arena_fft_plan* p, const void* f, void* u)
   arena_status st = ensure_host_buffers(p, false);
   if (st != ARENA_OK) return st;
   const size_t bytes = p->real_bytes();
-  // Pageable buffers (a GridField's std::vector) go through the pinned staging ring.
-  const bool fpin = host_ptr_pinned(f), upin = host_ptr_pinned(u);
-  cudaError_t e;
-  if ((!fpin || !upin) && !p->stager) {
-    p->stager = new (std::nothrow) Stager;
-    if (!p->stager) return fail(ARENA_ENOMEM, "staging ring");
-    if ((e = p->stager->init()) != cudaSuccess) {
-      delete p->stager;
-      p->stager = nullptr;
-      return cuda_fail(e, "pinned staging buffers");
-    }
-  }
-  e = fpin ? cudaMemcpyAsync(p->d_in, f, bytes, cudaMemcpyHostToDevice, p->hstream)
-           : p->stager->h2d(p->d_in, f, bytes, p->hstream);
+  cudaError_t e = host_copy(p, p->d_in, f, bytes, false);  // pageable GridField data: staged
   if (e != cudaSuccess) return cuda_fail(e, "H2D f");
   if ((st = enqueue_solve(p, p->d_in, p->d_out, p->hstream)) != ARENA_OK) return st;
-  e = upin ? cudaMemcpyAsync(u, p->d_out, bytes, cudaMemcpyDeviceToHost, p->hstream)
-           : p->stager->d2h(u, p->d_out, bytes, p->hstream);
-  if (e != cudaSuccess) return cuda_fail(e, "D2H u");
-  if ((e = cudaStreamSynchronize(p->hstream)) != cudaSuccess) return cuda_fail(e, "poisson solve");
+  if ((e = host_copy(p, u, p->d_out, bytes, true)) != cudaSuccess) return cuda_fail(e, "D2H u");
   return ARENA_OK;
 }
 
@@ -534,12 +540,10 @@ arena_status arena_dft3_forward_host(arena_fft_plan* p, const void* g_host, void
   std::lock_guard<std::mutex> lk(p->host_mu);
   arena_status st = ensure_host_buffers(p, false);
   if (st != ARENA_OK) return st;
-  cudaError_t e = cudaMemcpyAsync(p->d_in, g_host, p->real_bytes(), cudaMemcpyHostToDevice, p->hstream);
+  cudaError_t e = host_copy(p, p->d_in, g_host, p->real_bytes(), false);
   if (e != cudaSuccess) return cuda_fail(e, "H2D g");
   if ((st = dft3_fwd_enqueue(p, p->d_in, p->d_out, p->hstream)) != ARENA_OK) return st;
-  if ((e = cudaMemcpyAsync(spec_host, p->d_out, 2 * p->real_bytes(), cudaMemcpyDeviceToHost, p->hstream)))
-    return cuda_fail(e, "D2H spec");
-  if ((e = cudaStreamSynchronize(p->hstream)) != cudaSuccess) return cuda_fail(e, "dft3_forward");
+  if ((e = host_copy(p, spec_host, p->d_out, 2 * p->real_bytes(), true))) return cuda_fail(e, "dft3_forward");
   return ARENA_OK;
 }
 
@@ -549,12 +553,10 @@ arena_status arena_dft3_inverse_host(arena_fft_plan* p, const void* spec_host, v
   std::lock_guard<std::mutex> lk(p->host_mu);
   arena_status st = ensure_host_buffers(p, true);
   if (st != ARENA_OK) return st;
-  cudaError_t e = cudaMemcpyAsync(p->d_in, spec_host, 2 * p->real_bytes(), cudaMemcpyHostToDevice, p->hstream);
+  cudaError_t e = host_copy(p, p->d_in, spec_host, 2 * p->real_bytes(), false);
   if (e != cudaSuccess) return cuda_fail(e, "H2D spec");
   if ((st = dft3_inv_enqueue(p, p->d_in, p->d_out, p->d_work, p->hstream)) != ARENA_OK) return st;
-  if ((e = cudaMemcpyAsync(g_host, p->d_out, p->real_bytes(), cudaMemcpyDeviceToHost, p->hstream)))
-    return cuda_fail(e, "D2H g");
-  if ((e = cudaStreamSynchronize(p->hstream)) != cudaSuccess) return cuda_fail(e, "dft3_inverse");
+  if ((e = host_copy(p, g_host, p->d_out, p->real_bytes(), true))) return cuda_fail(e, "dft3_inverse");
   return ARENA_OK;
 }
 

@@ -41,6 +41,9 @@ __host__ __device__ constexpr int spec_pitch(int n) { return (n / 2 + 1 + 7) / 8
 #ifndef ARENA_STRIDED_E
 #define ARENA_STRIDED_E 16  // points per thread, y / x kernels
 #endif
+#ifndef ARENA_CONTIG_LARGE_N
+#define ARENA_CONTIG_LARGE_N 2048
+#endif
 #ifndef ARENA_CONTIG_SMALL_N
 #define ARENA_CONTIG_SMALL_N 512  // B200: 512^3 z passes 0.50 -> 0.39 ms, 256^3 0.10 -> 0.07 ms
 #endif
@@ -84,8 +87,11 @@ struct ContigCfg {  // z passes: rows of NR reals = M = NR/2 complex
   // resident warps (B200, 256^3: z passes 0.10 -> 0.07 ms; at n = 1024 E = 16
   // with 16 CTAs/SM spills).
   static constexpr bool SMALL = NR <= ARENA_CONTIG_SMALL_N;
-  static constexpr int E = imin(SMALL ? 16 : ARENA_CONTIG_E, M);
-  static constexpr int MINB = SMALL ? 2 * ARENA_CONTIG_MINB : ARENA_CONTIG_MINB;
+  // n >= ARENA_CONTIG_LARGE_N (2048: M = 1024): E = 32 spills ~1 KB, so 16 points
+  // per thread with half the CTAs per SM (128 registers).
+  static constexpr bool LARGE = NR >= ARENA_CONTIG_LARGE_N;
+  static constexpr int E = imin((SMALL || LARGE) ? 16 : ARENA_CONTIG_E, M);
+  static constexpr int MINB = SMALL ? 2 * ARENA_CONTIG_MINB : (LARGE ? ARENA_CONTIG_MINB / 2 : ARENA_CONTIG_MINB);
   static constexpr int P = M / E;
   static constexpr int VB = 2 * sizeof(T);
   // rows per CTA (a power of two, so it divides the n^2 rows): aim for 256

@@ -6,6 +6,7 @@
 //     -I include tools/l2_probe.cu paper_1408_6497_b200/csrc/pow2_f64.cu \
 //     paper_1408_6497_b200/csrc/stage_twiddles.cu -lcuda -o tools/l2_probe
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <vector>
 
@@ -23,7 +24,7 @@ using namespace arena_fft;
   } while (0)
 
 int main(int argc, char** argv) {
-  const int n = 1024, nc = n / 2 + 1, ncp = (nc + 7) / 8 * 8;
+  const int n = argc > 1 ? atoi(argv[1]) : 1024, nc = n / 2 + 1, ncp = (nc + 7) / 8 * 8;
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   std::vector<double> tw(2 * n);
@@ -39,7 +40,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&dstw, st.size() * 8));
   CK(cudaMemcpy(dtw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dstw, st.data(), st.size() * 8, cudaMemcpyHostToDevice));
-  const int planes_list[] = {4, 8, 512};
+  const int planes_list[] = {4, 8, n >= 2048 ? 128 : 512};
   printf("planes  MB(f+spec)   zfwd_us/plane  yfwd_us/plane  x_us/line-set  yinv_us/plane  zinv_us/plane\n");
   for (int planes : planes_list) {
     const size_t fb = size_t(planes) * n * n * 8, sb = size_t(planes) * n * ncp * 16;

@@ -141,5 +141,8 @@ def test_pencil_kq_properties():
     assert pencil_kq(64, 4) == 10  # 8- and 4-aligned pitches would leave rank 3 empty
     for n in (64, 128, 1024, 2048):  # the device pencil path needs n >= 64
         for pc in (1, 2, 4, 8):
-            kq = pencil_kq(n, pc)
-            assert (pc - 1) * kq < n // 2 + 1 <= pc * kq  # every chunk non-empty, all k covered
+            kq, nc = pencil_kq(n, pc), n // 2 + 1
+            assert nc <= pc * kq  # all k covered
+            w = -(-nc // pc)
+            if (pc - 1) * w < nc:  # a non-empty last chunk is possible: the pitch keeps it
+                assert (pc - 1) * kq < nc

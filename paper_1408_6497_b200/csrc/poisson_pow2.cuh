@@ -18,6 +18,7 @@
 // packed even/odd pairs (a double2 load of two reals) plus an O(n) split.
 #pragma once
 
+#include "async_copy.cuh"
 #include "fft_engine.cuh"
 #include "launchers.h"
 
@@ -61,6 +62,14 @@ __host__ __device__ constexpr int spec_pitch(int n) { return (n / 2 + 1 + 7) / 8
 #ifndef ARENA_X_SMEM
 #define ARENA_X_SMEM (64 * 1024)  // shared-memory budget per x tile
 #endif
+#ifndef ARENA_Z_PF
+#define ARENA_Z_PF 1  // z passes: each CTA prefetches into L2 (one bulk request) the rows of the
+                      // CTA this many waves of resident CTAs ahead, so that CTA's loads hit L2
+                      // (B200 A/B, 1024^3 fp64: K1 3.40 -> 3.05 ms; 0: off)
+#endif
+#ifndef ARENA_SMS
+#define ARENA_SMS 148  // B200 SM count (sets the prefetch distance of the z passes)
+#endif
 #ifndef ARENA_JBLOCK
 #define ARENA_JBLOCK 8  // j-block of the half-spectrum layout (see Layout)
 #endif
@@ -102,6 +111,7 @@ struct ContigCfg {  // z passes: rows of NR reals = M = NR/2 complex
   static constexpr int THREADS = L * P;
   static constexpr int SMEM_X = (M * L + L) * VB;
   static constexpr int SMEM = SMEM_X;
+  static constexpr int PF = ARENA_Z_PF * ARENA_SMS * MINB;  // L2 prefetch distance (CTAs)
 };
 
 __device__ __forceinline__ int signed_freq(int k, int n) { return k <= n / 2 ? k : k - n; }  // fft_solver.hpp:19
@@ -234,6 +244,10 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::M
            const vec2_t<T>* __restrict__ stw, Layout g_) {
   using C = ContigCfg<T, NR>;
   const Layout g = FIXED ? fixed_layout<NR>() : g_;
+  if constexpr (ARENA_Z_PF > 0) {
+    const unsigned b = blockIdx.x + C::PF;
+    if (threadIdx.x == 0 && b < gridDim.x) bulk_prefetch_l2(f + size_t(b) * C::L * NR, C::L * NR * sizeof(T));
+  }
   zfwd_rows<T, NR, C::E, C::L, kSyncCta>(f, S, tw, stw, g, size_t(blockIdx.x) * C::L, smem_base<vec2_t<T>>(),
                                          threadIdx.x);
 }
@@ -301,6 +315,14 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::M
            const vec2_t<T>* __restrict__ stw, Layout g_) {
   using C = ContigCfg<T, NR>;
   const Layout g = FIXED ? fixed_layout<NR>() : g_;
+  if constexpr (ARENA_Z_PF > 0) {
+    const unsigned b = blockIdx.x + C::PF;
+    if (threadIdx.x < C::L && b < gridDim.x) {
+      const size_t row = size_t(b) * C::L + threadIdx.x;
+      constexpr int ncp = spec_pitch(NR);
+      bulk_prefetch_l2(S + rowB(g, int(row / NR), int(row % NR)) * ncp, ncp * sizeof(vec2_t<T>));
+    }
+  }
   zinv_rows<T, NR, C::E, C::L, kSyncCta, false>(S, u, tw, stw, g, size_t(blockIdx.x) * C::L, smem_base<vec2_t<T>>(),
                                                 threadIdx.x);
 }
@@ -402,7 +424,10 @@ namespace arena_fft {
 #define ARENA_TMA_TWSMEM_Y 0  // same for the y passes
 #endif
 #ifndef ARENA_TMA_L2PF
-#define ARENA_TMA_L2PF 0  // also prefetch the tile this many iterations ahead into L2 (0: off)
+#define ARENA_TMA_L2PF 0  // also prefetch the tile this many iterations ahead into L2 (0: off; B200
+                          // 1024^3: x 4.3 -> 6.1 ms at 1, and the same with per-thread
+                          // prefetch.global.L2 of the next tile's rows — the strided passes lose
+                          // to any early L2 traffic, unlike the z passes, ARENA_Z_PF)
 #endif
 
 // y passes (B200 A/B, 1024^3): 8-line tiles (128-byte TMA rows), one CTA per SM,

@@ -42,6 +42,9 @@ def _args():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--inplace", action="store_true",
+                    help="solve in place (u aliases f): f + workspace only, so 2048^3 fp64 fits one GPU "
+                         "(default for n >= 2048); parity then from one solve of a fresh f, checked in plane blocks")
     ap.add_argument("--cpu-n", type=int, default=512, help="grid of the bounded CPU sample")
     ap.add_argument("--slab", action="store_true", help="use the slab (NCCL) path even with one rank")
     ap.add_argument("--decomp", default="slab", choices=("slab", "pencil"), help="multi-GPU decomposition")
@@ -219,6 +222,44 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _inplace_parity(plan, src, f, sh, prec, block=64):
+    """In-place mode: solve a fresh f once (u overwrites f) and compare with the analytic u
+    generated block by block of planes — the gauge-aligned errors of arena_field_compare
+    (problems.cpp:88-106) accumulated over the blocks in two passes, fp64 sums."""
+    import torch
+
+    from paper_1408_6497_b200 import problems
+
+    n = src.n
+    f64 = torch.empty((n, n, n), dtype=torch.float64, device="cuda") if prec != 64 else f
+    problems.fill_device(src, "f", f64, 64, sh)
+    f64 -= f64.mean()
+    if prec != 64:
+        f.copy_(f64)
+        del f64
+    plan.solve_device(f, f, sh)
+    torch.cuda.synchronize()
+    buf = torch.empty((block, n, n), dtype=torch.float64, device="cuda")
+    su = sa = 0.0
+    amax = 0.0
+    for i0 in range(0, n, block):
+        problems.fill_device(src, "u", buf, 64, sh, i0, block)
+        su += f[i0:i0 + block].double().sum().item()
+        sa += buf.sum().item()
+        amax = max(amax, buf.abs().max().item())
+    N = float(n) ** 3
+    shift, mean_e = (sa - su) / N, sa / N
+    d2 = e2 = dmax = 0.0
+    for i0 in range(0, n, block):
+        problems.fill_device(src, "u", buf, 64, sh, i0, block)
+        d = f[i0:i0 + block].double() + shift - buf
+        d2 += (d * d).sum().item()
+        dmax = max(dmax, d.abs().max().item())
+        e2 += ((buf - mean_e) ** 2).sum().item()
+    del buf
+    return math.sqrt(d2 / e2), dmax / amax
+
+
 def run_ours(args, rank, world, local):
     import numpy as np
     import torch
@@ -240,7 +281,10 @@ def run_ours(args, rank, world, local):
     problems.fill_device(src, "f", f64, 64, sh)
     f64 -= f64.mean()
     f = f64 if prec == 64 else f64.float()
-    u = torch.empty_like(f)
+    inplace = args.inplace or n >= 2048
+    if inplace and prec != 64:
+        del f64
+    u = f if inplace else torch.empty_like(f)
     plan = arena.Plan(n, prec, local)
     launches = plan.launches_per_solve
 
@@ -285,11 +329,14 @@ def run_ours(args, rank, world, local):
 
     # ---- parity of the timed output vs the analytic solution (band-limited source: exact)
     # (device reductions, arena_field_compare: gauge-aligned as problems.cpp:88-106)
-    ua = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
-    problems.fill_device(src, "u", ua, 64, sh)
-    cmp = arena.field_compare(u if prec == 64 else u.double(), ua)
-    rel_an, linf_an = cmp["rel_l2"], cmp["linf_rel"]
-    del ua
+    if inplace:
+        rel_an, linf_an = _inplace_parity(plan, src, f, sh, prec)
+    else:
+        ua = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+        problems.fill_device(src, "u", ua, 64, sh)
+        cmp = arena.field_compare(u if prec == 64 else u.double(), ua)
+        rel_an, linf_an = cmp["rel_l2"], cmp["linf_rel"]
+        del ua
 
     # ---- roofline of the dominant kernel
     peak, peak_kind = _peaks()
@@ -313,7 +360,10 @@ def run_ours(args, rank, world, local):
     # arena_poisson_solve_host_batch overlaps the copy-in of step s+1 and the copy-out of step s-1
     # with the solve of step s (PCIe is full duplex), the way a user streams many fields.
     e2e = None
-    if not args.no_e2e:
+    if inplace and not args.no_e2e:  # 4 pinned n^3 host buffers would not fit the host
+        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": n ** 3 * elem, "d2h_bytes_per_step": n ** 3 * elem,
+               "skipped": "in-place large-n run: the e2e host stream needs 4 pinned n^3 buffers"}
+    elif not args.no_e2e:
         hf = [torch.empty((n, n, n), dtype=dt, pin_memory=True) for _ in range(2)]
         hu = [torch.empty((n, n, n), dtype=dt, pin_memory=True) for _ in range(2)]
         for h in hf:
@@ -355,7 +405,8 @@ def run_ours(args, rank, world, local):
             "dtype": "f64" if prec == 64 else "f32", "data": "synthetic",
             "config": {"workload": f"C{args.config}: {problems.CONFIG_TEXT[args.config]}", "n": n,
                        "precision": prec, "decomposition": "single-GPU" if world == 1 else f"{world} replicas",
-                       "l2": "inputs larger than L2 (8.6 GB field), no flush",
+                       "l2": f"inputs larger than L2 ({n ** 3 * elem / 1e9:.1f} GB field), no flush",
+                       "in_place": inplace,
                        "path": "pow2" if plan.path == arena.PATH_POW2 else "generic"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,

@@ -17,7 +17,7 @@ struct alignas(64) TmaCache {
                               // half-row y boxes over B (k_ystream)
   const void* specB = nullptr;
   const void* specC = nullptr;
-  int n = 0, ni = 0, nj = 0, nchunks = 0;
+  int n = 0, ni = 0, nj = 0, nchunks = 0, quad = 0;
 };
 
 // Solve phases (bit mask): the slab path runs them around its two exchanges.
@@ -56,6 +56,8 @@ struct Pow2Args {
   // nullptr = in-place (the exchange is a separate step).
   void* const* peer_y = nullptr;
   void* const* peer_x = nullptr;
+  // Single GPU: quadrant formulation (poisson_quad.cuh), H = n/2-point y / x lines.
+  int quad = 0;
 };
 enum : int { kFuseFwd = 1, kFuseInv = 2 };
 

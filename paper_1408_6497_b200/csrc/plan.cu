@@ -92,6 +92,7 @@ struct arena_fft_plan {
   bool use_graphs = false;
   int lag = 2;
   int fuse = 0;             // kFuseFwd | kFuseInv
+  int quad = 0;             // quadrant formulation (poisson_quad.cuh)
   int sm_count = 148;
   // host-boundary resources (lazily allocated)
   void* d_in = nullptr;
@@ -240,6 +241,7 @@ arena_status enqueue_kernels(arena_fft_plan* p, const void* d_f, void* d_u, cuda
   if (p->path == ARENA_PATH_POW2) {
     Pow2Args a{d_f, d_u, p->spec, p->tw, p->stw, p->n, p->nc, p->ncp, s, ev, p->tma, p->sm_count,
                /*ni*/ p->n, /*nj*/ p->n, /*nchunks*/ 1, /*j0*/ 0, /*specC*/ p->spec, kPhaseAll, p->ctrs, p->lag, p->fuse};
+    a.quad = p->quad;
     e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
   } else {
     GenArgs a{&p->gplan, p->tw, p->n, p->nc, p->ncp, s, ev};
@@ -349,6 +351,16 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
       }
     }
     if (const char* lg = std::getenv("ARENA_FFT_FUSED_LAG")) p->lag = std::atoi(lg);
+    // Quadrant formulation (poisson_quad.cuh): default for n >= 2048, where the n-point
+    // y / x tiles no longer fit 128-byte rows in shared memory, and for fp64 n = 512.
+    // B200 A/B (ms per solve, plain / quadrant): 2048^3 fp64 178 / 148, fp32 95 / 84;
+    // 1024^3 17.5 / 18.2; 512^3 fp64 2.10 / 2.01, fp32 1.10 / 1.10; 256^3 0.295 / 0.307.
+    // ARENA_FFT_QUAD = 0 | 1 overrides (any n >= 32 with the TMA kernels).
+    {
+      const char* qz = std::getenv("ARENA_FFT_QUAD");
+      const bool want = qz ? std::string(qz) == "1" : (n >= 2048 || (n == 512 && precision_bits == 64));
+      p->quad = (want && p->tma && n >= 32 && !p->fuse) ? 1 : 0;
+    }
   } else {
     p->path = ARENA_PATH_GENERIC;
     if (!gen_plan_make(n, &p->gplan)) {

@@ -478,8 +478,12 @@ namespace arena_fft {
 #define ARENA_TMA_MINB_Y32 ARENA_TMA_MINB_Y
 #endif
 
-// YP: configuration of the y passes (PASS 0/1) vs the x pass.
-template <typename T, int N, bool YP = false>
+// YP: configuration of the y passes (PASS 0/1) vs the x pass.  XW: the x pass
+// takes the wide (two-budget, one CTA per SM) tile regardless of its row width.
+#ifndef ARENA_QUAD_XW
+#define ARENA_QUAD_XW 1  // quadrant x pass: 128-byte rows (B200 2048^3: 64-byte rows re-read 1.7x in L2)
+#endif
+template <typename T, int N, bool YP = false, bool XW = false>
 struct TmaCfg {
   static constexpr bool F64 = sizeof(T) == 8;
   static constexpr int VB = 2 * sizeof(T);
@@ -489,7 +493,8 @@ struct TmaCfg {
                                     : (F64 ? ARENA_TMA_X_TILE : ARENA_TMA_X_TILE32);
   // Long x lines (n >= 2048 fp64): a 64 KB tile would leave rows of 32 bytes, so the x
   // pass takes a tile twice as wide (one CTA per SM) — B200 2048^3: x 98.8 -> 51.1 ms.
-  static constexpr bool WIDEX = !YP && imax(1, BUDGET0 / (N * VB)) * VB < 64;
+  static constexpr int ROWB = imax(1, BUDGET0 / (N * VB)) * VB;  // tile row bytes at the base budget
+  static constexpr bool WIDEX = !YP && ((XW && ROWB < 128) || ROWB < 64);
   static constexpr int BUDGET = WIDEX ? 2 * BUDGET0 : BUDGET0;
   static constexpr int L = pow2_floor(imax(2, imin(ARENA_TMA_LROW / VB, BUDGET / (N * VB))));
   static constexpr int MINB0 = WIDEX ? 1
@@ -538,26 +543,34 @@ struct PeerOut {
   int shift;
 };
 
-template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false>
-__global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2)>::THREADS, TmaCfg<T, N, (PASS < 2)>::MINB)
+// QUAD: the quadrant layout of an n = 2N grid (poisson_quad.cuh): four chunks of
+// N x N rows, one per (i parity, j parity) of the frequency; lines stay inside a
+// chunk, tile index gt = (chunk * lines + outer) * KT + k-tile, and the symbol
+// reads ki = 2 i' + ci, kj = 2 j' + cj of the n-point transform.
+template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false, bool QUAD = false>
+__global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), QUAD && PASS == 2 && ARENA_QUAD_XW>::THREADS,
+                                  TmaCfg<T, N, (PASS < 2), QUAD && PASS == 2 && ARENA_QUAD_XW>::MINB)
     k_strided_tma(const __grid_constant__ CUtensorMap tmap, vec2_t<T>* __restrict__ spec,
                   const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g_, int nchunks_, int j0_, KSpan ks_,
                   vec2_t<T>* __restrict__ out_, Layout gout_, const __grid_constant__ PeerOut<vec2_t<T>> po) {
   static_assert(!(FIXED && PEER), "the fixed geometry is the single-GPU one");
+  static_assert(!(QUAD && PEER), "the quadrant layout is single-GPU");
   const Layout g = FIXED ? fixed_layout<N>() : g_;
   const Layout gout = FIXED ? fixed_layout<N>() : gout_;
   const int nchunks = FIXED ? 1 : nchunks_;
   const int j0 = FIXED ? 0 : j0_;
-  const KSpan ks = FIXED ? KSpan{N / 2 + 1, spec_pitch(N), 0} : ks_;
+  // FIXED: the single-GPU geometry (QUAD: a chunk of the 2N grid's quadrant layout)
+  const KSpan ks = FIXED ? (QUAD ? KSpan{N + 1, spec_pitch(2 * N), 0} : KSpan{N / 2 + 1, spec_pitch(N), 0}) : ks_;
   vec2_t<T>* __restrict__ out = FIXED ? spec : out_;
   using V = vec2_t<T>;
-  using C = TmaCfg<T, N, (PASS < 2)>;
+  using C = TmaCfg<T, N, (PASS < 2), QUAD && PASS == 2 && ARENA_QUAD_XW>;
   constexpr int E = C::E, P = C::P, L = C::L, TILE = C::TILE;
   constexpr uint32_t TILE_BYTES = TILE * sizeof(V);
   constexpr int NBUF = C::NBUF;
   const int KT = (ks.kc + L - 1) / L;
   const size_t kq = size_t(ks.kq);
-  const int NT = (PASS < 2 ? g.ni : g.nj) * KT;
+  const int NL = (PASS < 2 ? g.ni : g.nj) * KT;  // tiles per chunk (QUAD) / in all
+  const int NT = NL * (QUAD ? 4 : 1);
   constexpr bool TWS = PASS == 2 ? bool(ARENA_TMA_TWSMEM_X) : bool(ARENA_TMA_TWSMEM_Y);
   V* bufs = smem_base<V>();
   V* tws = bufs + NBUF * TILE;
@@ -581,16 +594,18 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2)>::THREADS, TmaCfg<T, N
   }();
 
   auto issue = [&](int gt, V* dst, uint64_t* b) {
+    const int qd = QUAD ? gt / NL : 0;
+    if constexpr (QUAD) gt -= qd * NL;
     const int outer = gt / KT, kt = gt % KT;
     mbar_arrive_expect_tx(b, TILE_BYTES);
-    if constexpr (PASS < 2) {  // y tile: fixed il = outer, all j
-      tma_load_5d(dst, &tmap, b, 2 * kt * L, 0, outer, 0, 0);
+    if constexpr (PASS < 2) {  // y tile: fixed il = outer, all j (QUAD: of chunk qd)
+      tma_load_5d(dst, &tmap, b, 2 * kt * L, 0, outer, 0, qd);
     } else {  // x tile: fixed jl = outer, all i (chunk c, il blocks of IB)
       const int IB = tma_ib(g.ni);
       const int jb = (1 << g.jbs) - 1;
-      for (int c = 0; c < nchunks; ++c)
+      for (int c = qd; c < (QUAD ? qd + 1 : nchunks); ++c)
         for (int q = 0; q < g.ni; q += IB)
-          tma_load_5d(dst + (size_t(c) * g.ni + q) * L, &tmap, b, 2 * kt * L, outer & jb, q, outer >> g.jbs, c);
+          tma_load_5d(dst + (size_t(c - qd) * g.ni + q) * L, &tmap, b, 2 * kt * L, outer & jb, q, outer >> g.jbs, c);
     }
   };
   auto prefetch = [&](int gt) {  // same boxes, into L2 only
@@ -652,8 +667,10 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2)>::THREADS, TmaCfg<T, N
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = cur[(t + P * e) * L + l];
     __syncthreads();  // the tile buffer becomes exchange scratch
-    const int outer = gt / KT;
-    const int k = (gt % KT) * L + l;
+    const int qd = QUAD ? gt / NL : 0;
+    const int gl = QUAD ? gt - qd * NL : gt;
+    const int outer = gl / KT;
+    const int k = (gl % KT) * L + l;
     auto release = [&]() {  // buffer free (all exchange reads done): request the next tile
       if constexpr (EARLY) {
         const int gn = gt + gridDim.x;
@@ -673,11 +690,12 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2)>::THREADS, TmaCfg<T, N
       line_fft_tail<N, E, L, +1>(v, cur, twp, t, l);
     } else {
       line_fft<N, E, L, -1>(v, cur, twp, t, l);
-      const T kj = T(signed_freq(j0 + outer, N)), kk = T(ks.k0 + k);
+      const T kj = QUAD ? T(signed_freq(2 * outer + (qd & 1), 2 * N)) : T(signed_freq(j0 + outer, N));
+      const T kk = T(ks.k0 + k);
       const T c = kj * kj + kk * kk;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const T ki = T(signed_freq(t + P * e, N));
+        const T ki = QUAD ? T(signed_freq(2 * (t + P * e) + (qd >> 1), 2 * N)) : T(signed_freq(t + P * e, N));
         const T k2 = ki * ki + c;
         const T m = poisson_symbol(k2, scale, four_pi2);
         v[e].x *= m;
@@ -698,10 +716,12 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2)>::THREADS, TmaCfg<T, N
       };
       if constexpr (PASS < 2) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) st_out(dst(out, rowB(gout, outer, t + P * e)), v[e]);
+        for (int e = 0; e < E; ++e)
+          st_out(dst(out, QUAD ? lrow(gout, qd, outer, t + P * e) : rowB(gout, outer, t + P * e)), v[e]);
       } else {
 #pragma unroll
-        for (int e = 0; e < E; ++e) st_out(dst(spec, rowC(g, t + P * e, outer)), v[e]);
+        for (int e = 0; e < E; ++e)
+          st_out(dst(spec, QUAD ? lrow(g, qd, t + P * e, outer) : rowC(g, t + P * e, outer)), v[e]);
       }
     }
     // No barrier needed here: every thread's last access to `cur` (the tile

@@ -9,6 +9,7 @@
 
 #include "launchers.h"
 #include "poisson_fused.cuh"
+#include "poisson_quad.cuh"
 #include "poisson_ystream.cuh"
 
 namespace arena_fft {
@@ -59,8 +60,9 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // TMA descriptor of a workspace in Layout g (5-D, see k_strided_tma).
 template <typename T, int N>
 cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool ybox, int kc = N / 2 + 1,
-                       int kq = spec_pitch(N), int ly = TmaCfg<T, N, true>::L) {
-  constexpr int LX = TmaCfg<T, N, false>::L;
+                       int kq = spec_pitch(N), int ly = TmaCfg<T, N, true>::L, bool one_chunk = false,
+                       int lx = TmaCfg<T, N, false>::L) {
+  const int LX = lx;
   const int LY = ly;
   auto enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
@@ -73,7 +75,7 @@ cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   cuuint32_t box[5];
   if (ybox) {
-    box[0] = 2 * LY; box[1] = JB; box[2] = 1; box[3] = g.nj / JB; box[4] = nchunks;
+    box[0] = 2 * LY; box[1] = JB; box[2] = 1; box[3] = g.nj / JB; box[4] = one_chunk ? 1 : nchunks;
   } else {
     box[0] = 2 * LX; box[1] = 1; box[2] = tma_ib(g.ni); box[3] = 1; box[4] = 1;
   }
@@ -93,24 +95,25 @@ inline const vec2_t<T>* stw_ptr(const Pow2Args& a, int which, int E) {
   return static_cast<const vec2_t<T>*>(a.stw) + stw_offset(a.n, which, E);
 }
 
-template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false>
+template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false, bool QUAD = false>
 cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* spec, const Layout& g, T scale,
                                T four_pi2, KSpan ks = KSpan{N / 2 + 1, spec_pitch(N), 0}, void* out = nullptr,
                                const Layout* gout = nullptr, const PeerOut<vec2_t<T>>* po = nullptr) {
-  using C = TmaCfg<T, N, (PASS < 2)>;
+  using C = TmaCfg<T, N, (PASS < 2), QUAD && PASS == 2 && ARENA_QUAD_XW>;
   using V = vec2_t<T>;
-  auto kern = k_strided_tma<T, N, PASS, PEER, FIXED>;
+  auto kern = k_strided_tma<T, N, PASS, PEER, FIXED, QUAD>;
   constexpr int SMEM = PASS == 2 ? C::SMEM_X : C::SMEM_Y;
-  cudaError_t e = ensure_smem<k_strided_tma<T, N, PASS, PEER, FIXED>>(SMEM, C::THREADS);
+  cudaError_t e = ensure_smem<k_strided_tma<T, N, PASS, PEER, FIXED, QUAD>>(SMEM, C::THREADS);
   if (e) return e;
   PeerOut<V> pov{};
   if (po) pov = *po;
   int per_sm = 1;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, SMEM))) return e;
-  const int tiles = (PASS < 2 ? g.ni : g.nj) * ((ks.kc + C::L - 1) / C::L);
+  const int tiles = (PASS < 2 ? g.ni : g.nj) * ((ks.kc + C::L - 1) / C::L) * (QUAD ? 4 : 1);
   int grid = a.sm_count * (per_sm > 0 ? per_sm : 1);
   if (grid > tiles) grid = tiles;
-  kern<<<grid, C::THREADS, SMEM, a.stream>>>(map, static_cast<V*>(spec), stw_ptr<T>(a, 1, C::E), scale, four_pi2, g,
+  // stage twiddles of N-point lines: table `which` 1 (N = n), 0 (N = n/2, quadrant lines)
+  kern<<<grid, C::THREADS, SMEM, a.stream>>>(map, static_cast<V*>(spec), stw_ptr<T>(a, QUAD ? 0 : 1, C::E), scale, four_pi2, g,
                                                a.nchunks, a.j0, ks, static_cast<V*>(out ? out : spec),
                                                gout ? *gout : g, pov);
   return cudaGetLastError();
@@ -175,8 +178,70 @@ inline void mark(const Pow2Args& a, int i) {
   if (a.ev) cudaEventRecord(a.ev[i], a.stream);
 }
 
+// Single-GPU quadrant path (poisson_quad.cuh): K1q, then the H-point y / x / y
+// TMA passes on the four quadrant chunks, then K5q.
+template <typename T, int NR>
+cudaError_t launch_quad(const Pow2Args& a) {
+  if constexpr (!(QuadZCfg<T, NR>::OK && NR / 2 >= 8)) {
+    return cudaErrorNotSupported;
+  } else {
+    constexpr int H = NR / 2;
+    using V = vec2_t<T>;
+    using QC = QuadZCfg<T, NR>;
+    cudaError_t e;
+    if (!a.tma || a.nchunks != 1 || a.specC != a.spec || a.ni != NR || a.nj != NR) return cudaErrorNotSupported;
+    if (a.ncp != spec_pitch(NR) || a.nc != NR / 2 + 1) return cudaErrorInvalidValue;
+    if ((e = ensure_smem<k_zfwd_quad<T, NR>>(QC::SMEM, QC::THREADS))) return e;
+    if ((e = ensure_smem<k_zinv_quad<T, NR>>(QC::SMEM, QC::THREADS))) return e;
+    const Layout gq = make_layout(H, H);
+    const KSpan ks{NR / 2 + 1, spec_pitch(NR), 0};
+    TmaCache* c = a.tma;
+    if (c->specB != a.spec || c->specC != a.spec || c->n != NR || c->nchunks != 4 || !c->quad) {
+      if ((e = encode_map<T, H>(c->maps[0], a.spec, gq, 4, true, ks.kc, ks.kq, TmaCfg<T, H, true>::L, true))) return e;
+      if ((e = encode_map<T, H>(c->maps[1], a.spec, gq, 4, false, ks.kc, ks.kq, TmaCfg<T, H, true>::L, false,
+                                TmaCfg<T, H, false, ARENA_QUAD_XW>::L)))
+        return e;
+      c->specB = c->specC = a.spec;
+      c->n = NR;
+      c->ni = c->nj = H;
+      c->nchunks = 4;
+      c->quad = 1;
+    }
+    const CUtensorMap* my = reinterpret_cast<const CUtensorMap*>(c->maps[0]);
+    const CUtensorMap* mx = reinterpret_cast<const CUtensorMap*>(c->maps[1]);
+    const T scale = T(1.0 / (double(NR) * NR * NR));  // fft_solver.cpp:67
+    const T four_pi2 = T(4.0 * M_PI * M_PI);           // fft_solver.cpp:66
+    const V* tw = static_cast<const V*>(a.tw);
+    V* S = static_cast<V*>(a.spec);
+    const unsigned qgrid = unsigned(H) * H;
+    int mk = 0;
+    if (a.phases & kPhaseZY) {
+      mark(a, mk++);
+      k_zfwd_quad<T, NR><<<qgrid, QC::THREADS, QC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw,
+                                                                     stw_ptr<T>(a, 0, QC::E), gq);
+      mark(a, mk++);
+      if ((e = launch_strided_tma<T, H, 0, false, false, true>(a, *my, a.spec, gq, scale, four_pi2, ks))) return e;
+    }
+    if (a.phases & kPhaseX) {
+      mark(a, mk++);
+      // compile-time quadrant geometry for the x pass, as the single-GPU x pass (FIXED)
+      if ((e = launch_strided_tma<T, H, 2, false, true, true>(a, *mx, a.spec, gq, scale, four_pi2, ks))) return e;
+    }
+    if (a.phases & kPhaseYZ) {
+      mark(a, mk++);
+      if ((e = launch_strided_tma<T, H, 1, false, false, true>(a, *my, a.spec, gq, scale, four_pi2, ks))) return e;
+      mark(a, mk++);
+      k_zinv_quad<T, NR><<<qgrid, QC::THREADS, QC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw,
+                                                                     stw_ptr<T>(a, 0, QC::E), gq);
+      mark(a, mk++);
+    }
+    return cudaGetLastError();
+  }
+}
+
 template <typename T, int NR>
 cudaError_t launch_pow2_n(const Pow2Args& a) {
+  if (a.quad) return launch_quad<T, NR>(a);
   using V = vec2_t<T>;
   using CC = ContigCfg<T, NR>;
   using SC = StridedCfg<T, NR, 0>;
@@ -201,7 +266,7 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   if (tma) {
     TmaCache* c = a.tma;
     if (c->specB != a.spec || c->specC != a.specC || c->n != NR || c->ni != a.ni || c->nj != a.nj ||
-        c->nchunks != a.nchunks) {
+        c->nchunks != a.nchunks || c->quad) {
       if ((e = encode_map<T, NR>(c->maps[0], a.spec, gB, a.nchunks, true))) return e;
       if ((e = encode_map<T, NR>(c->maps[1], a.specC, gC, a.nchunks, false))) return e;
       if ((e = encode_map<T, NR>(c->maps[2], a.spec, gB, a.nchunks, true, NR / 2 + 1, spec_pitch(NR),
@@ -218,6 +283,7 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
       c->ni = a.ni;
       c->nj = a.nj;
       c->nchunks = a.nchunks;
+      c->quad = 0;
     }
   }
   const CUtensorMap* my = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[0]) : nullptr;

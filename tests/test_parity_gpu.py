@@ -618,3 +618,37 @@ def test_graph_replay_small_n(cuda):
     for o in outs:
         assert _rel(o.cpu().numpy(), ref1) <= TOL64
     assert _rel(u.cpu().numpy(), oracle.poisson_solve(f2.cpu().numpy())) <= TOL64
+
+
+@pytest.mark.parametrize("n", [32, 64, 128, 256, 512])
+@pytest.mark.parametrize("precision", [64, 32])
+def test_quadrant_path_vs_oracle(cuda, n, precision, monkeypatch):
+    """The quadrant formulation (poisson_quad.cuh: the first radix-2 step of the i
+    and j transforms in the z passes, four n/2-point quadrant problems for the
+    strided passes), forced at small n, against the oracle."""
+    torch = cuda
+    monkeypatch.setenv("ARENA_FFT_QUAD", "1")
+    f_np = np.random.default_rng(n + 7).uniform(-1, 1, (n, n, n))
+    dt = torch.float64 if precision == 64 else torch.float32
+    f = torch.from_numpy(f_np).to(dtype=dt, device="cuda")
+    u = torch.empty_like(f)
+    p = arena.Plan(n, precision)
+    p.solve_device(f, u)
+    torch.cuda.synchronize()
+    ref = oracle.poisson_solve(f_np if precision == 64 else f.double().cpu().numpy())
+    assert _rel(u.double().cpu().numpy(), ref) <= (TOL64 if precision == 64 else TOL32)
+    p.set_stage_timing(True)
+    p.solve_device(f, u)
+    times, _ = p.stage_times()
+    assert len(times) == 5, times
+
+
+def test_quadrant_path_1024_analytic(cuda, monkeypatch):
+    """Quadrant formulation at 1024^3 (config 4) against the analytic solution, in place."""
+    torch = cuda
+    monkeypatch.setenv("ARENA_FFT_QUAD", "1")
+    src, f, ua = _config_device(torch, 4)
+    arena.Plan(1024).solve_device(f, f)
+    torch.cuda.synchronize()
+    e = (torch.linalg.vector_norm(f - ua) / torch.linalg.vector_norm(ua)).item()
+    assert e <= 1e-12, e

@@ -134,8 +134,8 @@ def algorithmic_bytes(n: int, elem: int):
     per = {"zfwd_r2c": R + C, "yfwd": 2 * C, "xmid_fwd_scale_inv": 2 * C, "yinv": 2 * C, "zinv_c2r": C + R,
            # L2-fused pairs: HBM sees f read + spectrum write (and the reverse) once
            "zy_fused_fwd": R + C, "yz_fused_inv": C + R,
-           # generic (any n) path: seven sweeps
-           "gen_z_r2c": R + C, "gen_y_fwd": 2 * C, "gen_x_fwd": 2 * C, "gen_scale": 2 * C, "gen_x_inv": 2 * C,
+           # generic (any n) path: five sweeps (x forward * symbol * x backward fused)
+           "gen_z_r2c": R + C, "gen_y_fwd": 2 * C, "gen_xmid_fwd_scale_inv": 2 * C,
            "gen_y_inv": 2 * C, "gen_z_c2r": C + R}
     return per, 2 * R + 8 * C
 

@@ -2,10 +2,12 @@
 // n, grid.hpp:18; its own tests solve at n = 12 and transform at n = 6, 10,
 // test_fft.cpp:45,77,136).  Not the benchmarked path: up to 8 adjacent lines
 // per CTA staged in shared memory (so the strided y / x passes load and store
-// 128-byte rows), Stockham stages with compile-time radix-2/3/4/5/7 butterflies
-// and a direct O(R) sum for larger prime factors; every n >= 2 is handled.
-// B200, fp64: 384^3 in 6.8 ms, 768^3 in 83 ms (the power-of-two path: 1024^3 in
-// 17.7 ms).
+// 128-byte rows), Stockham stages with compile-time radix-2/3/4/5/7/8
+// butterflies (constant twiddles) and a direct O(R) sum for larger prime
+// factors; every n >= 2 is handled.  Five sweeps: the x pass runs forward *
+// symbol * backward in one kernel (G_XPOISSON).  B200, fp64: 384^3 in 5.2 ms,
+// 768^3 in 37 ms, 1000^3 in 85 ms (seven sweeps and table twiddles: 6.8 / 83 /
+// 156 ms; the power-of-two path: 1024^3 in 17.4 ms).
 //
 // Same conventions as fft_solver.cpp: r2c along the last axis keeping
 // k in [0, n/2], c2r treating its input as Hermitian (imaginary parts of the
@@ -21,7 +23,55 @@ namespace arena_fft {
 
 namespace {
 
-enum GenMode { G_R2C = 0, G_C2R = 1, G_C2C = 2, G_R2C_FULL = 3, G_C2C_TO_REAL = 4 };
+// G_XPOISSON: the x pass of the solve in one sweep — forward stages, the
+// Poisson symbol of fft_solver.cpp:66-79, backward stages (as K3 of the
+// power-of-two path), so the solve is five sweeps instead of seven.
+enum GenMode { G_R2C = 0, G_C2R = 1, G_C2C = 2, G_R2C_FULL = 3, G_C2C_TO_REAL = 4, G_XPOISSON = 5 };
+
+// cos / sin(2 pi m / R), 0 <= m < R, for the odd radices with compile-time
+// butterflies (literal constants: folded once the loops are unrolled).
+template <int R>
+__host__ __device__ constexpr double cosR(int m) {
+  if (R == 3) return m == 0 ? 1.0 : -0.5;
+  if (R == 5) return m == 0 ? 1.0 : (m == 1 || m == 4) ? 0.30901699437494745 : -0.8090169943749475;
+  return m == 0 ? 1.0 : (m == 1 || m == 6) ? 0.6234898018587336 : (m == 2 || m == 5) ? -0.22252093395631434 : -0.9009688679024191;
+}
+template <int R>
+__host__ __device__ constexpr double sinR(int m) {
+  if (R == 3) return m == 0 ? 0.0 : m == 1 ? 0.8660254037844386 : -0.8660254037844386;
+  if (R == 5) {
+    const double s1 = 0.9510565162951535, s2 = 0.5877852522924731;
+    return m == 0 ? 0.0 : m == 1 ? s1 : m == 2 ? s2 : m == 3 ? -s2 : -s1;
+  }
+  const double s1 = 0.7818314824680298, s2 = 0.9749279121818236, s3 = 0.4338837391175582;
+  return m == 0 ? 0.0 : m == 1 ? s1 : m == 2 ? s2 : m == 3 ? s3 : m == 4 ? -s3 : m == 5 ? -s2 : -s1;
+}
+
+// R-point DFT of a[] in registers, sign S, every twiddle a compile-time constant:
+// the power-of-two radices by the engine's Dft, 3 / 5 / 7 by the direct sum.
+template <typename T, int R, int S>
+__device__ __forceinline__ void small_dft(vec2_t<T> (&a)[R]) {
+  using V = vec2_t<T>;
+  if constexpr ((R & (R - 1)) == 0) {
+    Dft<R, S>::run(a);
+  } else {
+    V o[R];
+#pragma unroll
+    for (int s2 = 0; s2 < R; ++s2) {
+      T re = a[0].x, im = a[0].y;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        // a * exp(S 2 pi i m / R) = a * (c + i sn), c = cos, sn = S sin (m = r s2 mod R)
+        const T c = T(cosR<R>((r * s2) % R)), sn = T(S * sinR<R>((r * s2) % R));
+        re = fma(a[r].x, c, fma(-a[r].y, sn, re));
+        im = fma(a[r].y, c, fma(a[r].x, sn, im));
+      }
+      o[s2] = V{re, im};
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) a[r] = o[r];
+  }
+}
 
 // Line q -> (a, b) = (q / cnt_b, q % cnt_b); element x of the line at
 // base + a*sa + b*sb + x*es.  Lines with b >= valid_b are skipped.
@@ -60,18 +110,11 @@ __device__ __forceinline__ void gen_stage_bfly(const vec2_t<T>* b0, vec2_t<T>* b
       }
       a[r] = x;
     }
+    if (sign < 0) small_dft<T, R, -1>(a);
+    else small_dft<T, R, +1>(a);
     const int obase = grp * NSR + jj;
 #pragma unroll
-    for (int s2 = 0; s2 < R; ++s2) {
-      T re = a[0].x, im = a[0].y;
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const V w = twi<T>(tw, ((r * s2) % R) * nR, sign);  // W_R^{r s2}
-        re = fma(a[r].x, w.x, fma(-a[r].y, w.y, re));
-        im = fma(a[r].x, w.y, fma(a[r].y, w.x, im));
-      }
-      b1[(obase + s2 * NS) * L + l] = V{re, im};
-    }
+    for (int s2 = 0; s2 < R; ++s2) b1[(obase + s2 * NS) * L + l] = a[s2];
   }
 }
 
@@ -164,23 +207,47 @@ __global__ void k_gen_lines(const void* in, void* out, GenPlan pl, GenGeom g,
   }
   __syncthreads();
 
-  // ---- Stockham stages
-  int NS = 1;
-  for (int st = 0; st < pl.nst; ++st) {
-    const int R = pl.radix[st];
-    switch (R) {
-      case 2: gen_stage_bfly<T, 2>(b0, b1, L, n, NS, tw, sign); break;
-      case 3: gen_stage_bfly<T, 3>(b0, b1, L, n, NS, tw, sign); break;
-      case 4: gen_stage_bfly<T, 4>(b0, b1, L, n, NS, tw, sign); break;
-      case 5: gen_stage_bfly<T, 5>(b0, b1, L, n, NS, tw, sign); break;
-      case 7: gen_stage_bfly<T, 7>(b0, b1, L, n, NS, tw, sign); break;
-      default: gen_stage_direct<T>(b0, b1, L, n, NS, R, tw, sign); break;
+  // ---- Stockham stages (result in b0)
+  auto stages = [&](int sgn) {
+    int NS = 1;
+    for (int st = 0; st < pl.nst; ++st) {
+      const int R = pl.radix[st];
+      switch (R) {
+        case 2: gen_stage_bfly<T, 2>(b0, b1, L, n, NS, tw, sgn); break;
+        case 3: gen_stage_bfly<T, 3>(b0, b1, L, n, NS, tw, sgn); break;
+        case 4: gen_stage_bfly<T, 4>(b0, b1, L, n, NS, tw, sgn); break;
+        case 5: gen_stage_bfly<T, 5>(b0, b1, L, n, NS, tw, sgn); break;
+        case 7: gen_stage_bfly<T, 7>(b0, b1, L, n, NS, tw, sgn); break;
+        case 8: gen_stage_bfly<T, 8>(b0, b1, L, n, NS, tw, sgn); break;
+        default: gen_stage_direct<T>(b0, b1, L, n, NS, R, tw, sgn); break;
+      }
+      __syncthreads();
+      V* t = b0;
+      b0 = b1;
+      b1 = t;
+      NS *= R;
+    }
+  };
+  if constexpr (MODE == G_XPOISSON) {
+    // line q = (j, k) of the x pass (geometry gx: a = j, b = k); position x = i
+    stages(-1);
+    const T four_pi2 = T(4.0 * M_PI * M_PI);  // fft_solver.cpp:66
+    for (int idx = threadIdx.x; idx < L * n; idx += blockDim.x) {
+      int l, x;
+      split(idx, n, l, x);
+      const long long q = q0 + l;
+      const int j = int(q / g.cnt_b), k = int(q % g.cnt_b);
+      const T ki = T(x <= n / 2 ? x : x - n), kj = T(j <= n / 2 ? j : j - n), kk = T(k);
+      const T k2 = ki * ki + kj * kj + kk * kk;
+      const T m = (k2 == T(0)) ? T(0) : out_scale / (four_pi2 * k2);  // out_scale = 1/n^3
+      V& v = b0[x * L + l];
+      v.x *= m;
+      v.y *= m;
     }
     __syncthreads();
-    V* t = b0;
-    b0 = b1;
-    b1 = t;
-    NS *= R;
+    stages(+1);
+  } else {
+    stages(sign);
   }
 
   // ---- store
@@ -191,34 +258,19 @@ __global__ void k_gen_lines(const void* in, void* out, GenPlan pl, GenGeom g,
     if (!line_ok(l)) continue;
     const V v = b0[x * L + l];
     if (MODE == G_C2R || MODE == G_C2C_TO_REAL) static_cast<T*>(out)[out_base(l) + x * g.oes] = v.x * out_scale;
+    else if (MODE == G_XPOISSON) static_cast<V*>(out)[out_base(l) + x * g.oes] = v;
     else static_cast<V*>(out)[out_base(l) + x * g.oes] = v;
   }
 }
 
-// Poisson symbol on the half spectrum S[(i*n+j)*ncp + k], fft_solver.cpp:66-79.
-template <typename T>
-__global__ void k_gen_scale(vec2_t<T>* __restrict__ S, int n, int nc, int ncp, T scale, T four_pi2) {
-  const long long total = (long long)n * n * nc;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int k = int(idx % nc);
-    const long long ij = idx / nc;
-    const int j = int(ij % n), i = int(ij / n);
-    const T ki = T(i <= n / 2 ? i : i - n), kj = T(j <= n / 2 ? j : j - n), kk = T(k);
-    const T k2 = ki * ki + kj * kj + kk * kk;
-    const T m = (k2 == T(0)) ? T(0) : scale / (four_pi2 * k2);
-    vec2_t<T>& v = S[ij * ncp + k];
-    v.x *= m;
-    v.y *= m;
-  }
-}
-
-// Lines per CTA: the largest power of two <= 8 whose two L x n buffers fit in
-// 200 KB (n <= gen_max_n always allows L = 1); the strided passes use all 8
-// when they fit (128-byte rows).
-inline int gen_lines_per_cta(int n, int vb) {
-  int L = 8;
-  while (L > 1 && size_t(2) * n * L * vb > 200 * 1024) L /= 2;
+// Lines per CTA.  Strided passes (es != 1): up to 8 adjacent lines (128-byte
+// rows) within ~100 KB so two CTAs share an SM, else fewer; contiguous passes:
+// rows are contiguous anyway, so at most 2 lines within ~48 KB (four CTAs per
+// SM hide the load latency).  B200, 768^3: 83 ms with 8 lines everywhere.
+inline int gen_lines_per_cta(int n, int vb, bool strided) {
+  int L = strided ? 8 : 2;
+  const size_t cap = strided ? 100 * 1024 : 48 * 1024;
+  while (L > 1 && size_t(2) * n * L * vb > cap) L /= 2;
   return L;
 }
 
@@ -226,7 +278,7 @@ template <typename T, int MODE>
 cudaError_t run_lines(const GenArgs& a, const void* in, void* out, long long nlines, const GenGeom& g, int sign,
                       T out_scale) {
   const int vb = int(2 * sizeof(T));
-  const int L = gen_lines_per_cta(a.n, vb);
+  const int L = gen_lines_per_cta(a.n, vb, g.es != 1);
   const size_t smem = size_t(2) * a.n * L * vb;
   static bool attr_done[64] = {};
   int dev = 0;
@@ -261,20 +313,16 @@ cudaError_t gen_poisson(const GenArgs& a, const void* f, void* u, void* spec) {
   if ((e = run_lines<T, G_C2C>(a, spec, spec, (long long)n * ncp, gy, -1, T(1)))) return e;
   // x c2c forward: lines (j, k), element i at j*ncp + k + i*n*ncp
   GenGeom gx{ncp, 1, (long long)n * ncp, ncp, 1, (long long)n * ncp, ncp, nc};
+  // x: forward * Poisson symbol (fft_solver.cpp:66-79) * backward, one sweep
   gmark(a, 2);
-  if ((e = run_lines<T, G_C2C>(a, spec, spec, (long long)n * ncp, gx, -1, T(1)))) return e;
+  if ((e = run_lines<T, G_XPOISSON>(a, spec, spec, (long long)n * ncp, gx, -1, T(1.0 / (double(n) * n * n)))))
+    return e;
   gmark(a, 3);
-  k_gen_scale<T><<<1184, 256, 0, a.stream>>>(static_cast<vec2_t<T>*>(spec), n, nc, ncp,
-                                             T(1.0 / (double(n) * n * n)), T(4.0 * M_PI * M_PI));
-  if ((e = cudaGetLastError())) return e;
-  gmark(a, 4);
-  if ((e = run_lines<T, G_C2C>(a, spec, spec, (long long)n * ncp, gx, +1, T(1)))) return e;
-  gmark(a, 5);
   if ((e = run_lines<T, G_C2C>(a, spec, spec, (long long)n * ncp, gy, +1, T(1)))) return e;
   // z c2r: rows of S -> rows of u
-  gmark(a, 6);
+  gmark(a, 4);
   e = run_lines<T, G_C2R>(a, spec, u, nn, GenGeom{ncp, 0, 1, n, 0, 1, 1, 1}, +1, T(1));
-  gmark(a, 7);
+  gmark(a, 5);
   return e;
 }
 
@@ -314,7 +362,8 @@ bool gen_plan_make(int n, GenPlan* p) {
   p->n = n;
   p->nst = 0;
   int m = n;
-  // radix 4 first, then 2, then odd primes ascending
+  // radix 8, then 4, then 2, then odd primes ascending
+  while (m % 8 == 0 && p->nst < kGenMaxStages) { p->radix[p->nst++] = 8; m /= 8; }
   while (m % 4 == 0 && p->nst < kGenMaxStages) { p->radix[p->nst++] = 4; m /= 4; }
   while (m % 2 == 0 && p->nst < kGenMaxStages) { p->radix[p->nst++] = 2; m /= 2; }
   for (int q = 3; m > 1 && p->nst < kGenMaxStages; q += 2) {

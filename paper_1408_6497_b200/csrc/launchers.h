@@ -135,7 +135,7 @@ struct GenArgs {
 // Poisson solve f -> u (device, n^3 real) via the half-spectrum workspace spec.
 cudaError_t gen_poisson_f64(const GenArgs& a, const void* f, void* u, void* spec);
 cudaError_t gen_poisson_f32(const GenArgs& a, const void* f, void* u, void* spec);
-constexpr int kGenLaunches = 7;
+constexpr int kGenLaunches = 5;
 // dft3_forward: real g (n^3) -> complex spec (n^3, interleaved).  dft3_inverse:
 // complex spec -> real g = Re(backward)/n^3 using `work` (n^3 complex) as scratch.
 cudaError_t gen_dft3_forward_f64(const GenArgs& a, const void* g, void* spec);

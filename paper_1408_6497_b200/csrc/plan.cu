@@ -53,8 +53,8 @@ const char* kStageNames[4][kPow2Launches] = {
     {"zy_fused_fwd", "xmid_fwd_scale_inv", "yinv", "zinv_c2r", nullptr},
     {"zfwd_r2c", "yfwd", "xmid_fwd_scale_inv", "yz_fused_inv", nullptr},
     {"zy_fused_fwd", "xmid_fwd_scale_inv", "yz_fused_inv", nullptr, nullptr}};
-const char* kGenNames[kGenLaunches] = {"gen_z_r2c", "gen_y_fwd", "gen_x_fwd", "gen_scale",
-                                       "gen_x_inv", "gen_y_inv", "gen_z_c2r"};
+const char* kGenNames[kGenLaunches] = {"gen_z_r2c", "gen_y_fwd", "gen_xmid_fwd_scale_inv", "gen_y_inv",
+                                       "gen_z_c2r"};
 
 struct DeviceGuard {
   int prev = -1;

@@ -483,7 +483,18 @@ namespace arena_fft {
 #ifndef ARENA_QUAD_XW
 #define ARENA_QUAD_XW 1  // quadrant x pass: 128-byte rows (B200 2048^3: 64-byte rows re-read 1.7x in L2)
 #endif
+#ifndef ARENA_X_WIDE64
+#define ARENA_X_WIDE64 1  // fp64 x pass: 128-byte rows too (1024^3: one 8-warp CTA per SM, 4.35 -> 4.30 ms;
+                          // fp32 measured slower that way, 2.31 -> 2.50 ms)
+#endif
 template <typename T, int N, bool YP = false, bool XW = false>
+struct TmaCfg;
+// XW of the x pass (TmaCfg<T, N, false, x_wide<T, QUAD>()>)
+template <typename T, bool QUAD>
+constexpr bool x_wide() {
+  return QUAD ? bool(ARENA_QUAD_XW) : (sizeof(T) == 8 && bool(ARENA_X_WIDE64));
+}
+template <typename T, int N, bool YP, bool XW>
 struct TmaCfg {
   static constexpr bool F64 = sizeof(T) == 8;
   static constexpr int VB = 2 * sizeof(T);
@@ -548,8 +559,8 @@ struct PeerOut {
 // chunk, tile index gt = (chunk * lines + outer) * KT + k-tile, and the symbol
 // reads ki = 2 i' + ci, kj = 2 j' + cj of the n-point transform.
 template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false, bool QUAD = false>
-__global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), QUAD && PASS == 2 && ARENA_QUAD_XW>::THREADS,
-                                  TmaCfg<T, N, (PASS < 2), QUAD && PASS == 2 && ARENA_QUAD_XW>::MINB)
+__global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, QUAD>()>::THREADS,
+                                  TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, QUAD>()>::MINB)
     k_strided_tma(const __grid_constant__ CUtensorMap tmap, vec2_t<T>* __restrict__ spec,
                   const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g_, int nchunks_, int j0_, KSpan ks_,
                   vec2_t<T>* __restrict__ out_, Layout gout_, const __grid_constant__ PeerOut<vec2_t<T>> po) {
@@ -563,7 +574,7 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), QUAD && PASS == 2 && 
   const KSpan ks = FIXED ? (QUAD ? KSpan{N + 1, spec_pitch(2 * N), 0} : KSpan{N / 2 + 1, spec_pitch(N), 0}) : ks_;
   vec2_t<T>* __restrict__ out = FIXED ? spec : out_;
   using V = vec2_t<T>;
-  using C = TmaCfg<T, N, (PASS < 2), QUAD && PASS == 2 && ARENA_QUAD_XW>;
+  using C = TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, QUAD>()>;
   constexpr int E = C::E, P = C::P, L = C::L, TILE = C::TILE;
   constexpr uint32_t TILE_BYTES = TILE * sizeof(V);
   constexpr int NBUF = C::NBUF;

@@ -61,7 +61,7 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 template <typename T, int N>
 cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool ybox, int kc = N / 2 + 1,
                        int kq = spec_pitch(N), int ly = TmaCfg<T, N, true>::L, bool one_chunk = false,
-                       int lx = TmaCfg<T, N, false>::L) {
+                       int lx = TmaCfg<T, N, false, x_wide<T, false>()>::L) {
   const int LX = lx;
   const int LY = ly;
   auto enc = tensor_map_encoder();
@@ -99,7 +99,7 @@ template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false, bo
 cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* spec, const Layout& g, T scale,
                                T four_pi2, KSpan ks = KSpan{N / 2 + 1, spec_pitch(N), 0}, void* out = nullptr,
                                const Layout* gout = nullptr, const PeerOut<vec2_t<T>>* po = nullptr) {
-  using C = TmaCfg<T, N, (PASS < 2), QUAD && PASS == 2 && ARENA_QUAD_XW>;
+  using C = TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, QUAD>()>;
   using V = vec2_t<T>;
   auto kern = k_strided_tma<T, N, PASS, PEER, FIXED, QUAD>;
   constexpr int SMEM = PASS == 2 ? C::SMEM_X : C::SMEM_Y;
@@ -199,7 +199,7 @@ cudaError_t launch_quad(const Pow2Args& a) {
     if (c->specB != a.spec || c->specC != a.spec || c->n != NR || c->nchunks != 4 || !c->quad) {
       if ((e = encode_map<T, H>(c->maps[0], a.spec, gq, 4, true, ks.kc, ks.kq, TmaCfg<T, H, true>::L, true))) return e;
       if ((e = encode_map<T, H>(c->maps[1], a.spec, gq, 4, false, ks.kc, ks.kq, TmaCfg<T, H, true>::L, false,
-                                TmaCfg<T, H, false, ARENA_QUAD_XW>::L)))
+                                TmaCfg<T, H, false, x_wide<T, true>()>::L)))
         return e;
       c->specB = c->specC = a.spec;
       c->n = NR;

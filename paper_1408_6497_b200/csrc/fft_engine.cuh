@@ -62,6 +62,24 @@ __device__ __forceinline__ V cmul_si(V a) {
   return S > 0 ? V{-a.y, a.x} : V{a.y, -a.x};
 }
 
+// fp32: the same operations on packed pairs (sm_100 FADD2 / FMUL2 / FFMA2: one
+// instruction for both components; the fp32 passes are issue-bound).
+#ifndef ARENA_F32X2
+#define ARENA_F32X2 2  // 0: off, 1: sums, 2: sums and products
+#endif
+#if ARENA_F32X2
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __ffma2_rn(b, make_float2(-1.f, -1.f), a); }
+#endif
+#if ARENA_F32X2 >= 2  // products too (the operand broadcasts cost MOVs)
+__device__ __forceinline__ float2 cmul(float2 a, float2 w) {
+  return __ffma2_rn(make_float2(a.x, a.x), w, __fmul2_rn(make_float2(a.y, a.y), make_float2(-w.y, w.x)));
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 w) {
+  return __ffma2_rn(make_float2(a.x, a.x), make_float2(w.x, -w.y), __fmul2_rn(make_float2(a.y, a.y), make_float2(w.y, w.x)));
+}
+#endif
+
 // cos(2 pi m / 64), m = 0..16 (first quadrant), double-rounded.
 constexpr double kCos64[17] = {1.0,
                                0.9951847266721969,
@@ -104,6 +122,11 @@ __device__ __forceinline__ V cmul_const(V a) {
     using T = decltype(a.x);
     constexpr T c = T(cos64(m));
     constexpr T s = T(S * sin64(m));
+#if ARENA_F32X2 >= 2
+    if constexpr (sizeof(T) == 4) {
+      return __ffma2_rn(make_float2(a.x, a.x), make_float2(c, s), __fmul2_rn(make_float2(a.y, a.y), make_float2(-s, c)));
+    }
+#endif
     return V{fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c)};
   }
 }

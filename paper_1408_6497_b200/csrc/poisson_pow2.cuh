@@ -189,7 +189,10 @@ __device__ __forceinline__ double poisson_symbol(double k2, double scale, double
 }
 __device__ __forceinline__ float poisson_symbol(float k2, float scale, float four_pi2) {
   const float d = four_pi2 * k2;
-  float r = __frcp_rn(d);
+  float r;
+  // MUFU.RCP (<= 1 ulp): the IEEE __frcp_rn is a subroutine call per element, and the
+  // fp32 tolerance (1e-5) is far above an ulp
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
   return k2 == 0.0f ? 0.0f : scale * r;
 }
 

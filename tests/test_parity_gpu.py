@@ -652,3 +652,24 @@ def test_quadrant_path_1024_analytic(cuda, monkeypatch):
     torch.cuda.synchronize()
     e = (torch.linalg.vector_norm(f - ua) / torch.linalg.vector_norm(ua)).item()
     assert e <= 1e-12, e
+
+
+@pytest.mark.parametrize("quad", ["0", "1"])
+@pytest.mark.parametrize("n,precision", [(64, 64), (128, 64), (256, 64), (128, 32), (512, 32)])
+def test_repeat_bitwise_deterministic(cuda, n, precision, quad, monkeypatch):
+    """No atomics anywhere on the path, so repeated solves must agree bit for bit; a
+    shared-memory race (compute-sanitizer is unavailable on the GPU pool) would show
+    up as run-to-run differences."""
+    torch = cuda
+    monkeypatch.setenv("ARENA_FFT_QUAD", quad)
+    monkeypatch.setenv("ARENA_FFT_GRAPHS", "0")
+    dt = torch.float64 if precision == 64 else torch.float32
+    f = torch.from_numpy(np.random.default_rng(n + 3).uniform(-1, 1, (n, n, n))).to(dtype=dt, device="cuda")
+    p = arena.Plan(n, precision)
+    u0 = torch.empty_like(f)
+    p.solve_device(f, u0)
+    u = torch.empty_like(f)
+    for _ in range(12):
+        p.solve_device(f, u)
+        torch.cuda.synchronize()
+        assert torch.equal(u, u0)

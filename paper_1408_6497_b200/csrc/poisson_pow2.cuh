@@ -71,8 +71,12 @@ __host__ __device__ constexpr int spec_pitch(int n) { return (n / 2 + 1 + 7) / 8
 #define ARENA_SMS 148  // B200 SM count (sets the prefetch distance of the z passes)
 #endif
 #ifndef ARENA_JBLOCK
-#define ARENA_JBLOCK 8  // j-block of the half-spectrum layout (see Layout)
+#define ARENA_JBLOCK 64  // j-block of the half-spectrum layout (see Layout).  B200 A/B (ms per solve,
+                         // JB = 8 / 32 / 64): 1024^3 fp64 16.68 / 16.40 / 16.38 (y passes 3.41 -> 3.19,
+                         // x 4.13 -> 4.23), 512^3 2.007 / 1.957 / 1.945, 2048^3 143.3 / 141.6 / 141.5;
+                         // JB = 4: 16.87, 128: 16.36 fp64 but fp32 worse
 #endif
+
 
 // ------------------------------------------------------------ configuration
 // E: points per thread; L: lines per CTA.  Shared memory per CTA is
@@ -118,13 +122,14 @@ __device__ __forceinline__ int signed_freq(int k, int n) { return k <= n / 2 ? k
 
 // Half-spectrum layout, shared by the single-GPU and the slab (multi-GPU)
 // paths.  A workspace holds P chunks of ni x nj rows of ncp complex; inside a
-// chunk rows are blocked by JB = min(8, nj) in j:
+// chunk rows are blocked by JB = min(ARENA_JBLOCK, nj) in j:
 //   row(c, il, jl) = c*ni*nj + ((jl / JB)*ni + il)*JB + jl % JB.
-// Single GPU: P = 1, ni = nj = n, so row(i, j) = ((j/8)*n + i)*8 + j%8 — a y tile
-// (fixed i) reads n/8 contiguous 8-row chunks and an x tile (fixed j) reads rows
-// 8*ncp apart; with plain row-major rows the x pass touched n different 2 MB
-// pages per tile and its access pattern alone capped at 3.1 TB/s on B200
-// (tools/pattern_bw.cu; 6.2-6.4 TB/s blocked).
+// Single GPU: P = 1, ni = nj = n, so row(i, j) = ((j/JB)*n + i)*JB + j%JB — a y
+// tile (fixed i) reads n/JB contiguous JB-row chunks and an x tile (fixed j)
+// reads rows JB*ncp apart; with plain row-major rows the x pass touched n
+// different 2 MB pages per tile and its access pattern alone capped at 3.1 TB/s
+// on B200 (tools/pattern_bw.cu; 6.2-6.4 TB/s with JB = 8).  Larger blocks trade
+// a little x for more y (JB = 64: y 3.41 -> 3.19 ms, x 4.13 -> 4.23 ms at 1024^3).
 // Slab over P ranks (ni = nj = n/P): layout B (K1/K2/K4/K5 on a rank's i-slab)
 // puts j in chunk c = j / nj, so the block for peer c is contiguous; layout C
 // (K3 on a j-slab) puts i in chunk c = i / ni — exactly what arrives from rank c.

@@ -72,7 +72,7 @@ def test_full_solve_model_vs_oracle(n):
 def test_blocked_row_layout_is_a_bijection(n):
     """row_off (poisson_pow2.cuh): S rows grouped in j-blocks of JB; every (i, j)
     gets its own ncp-element row inside the n*n*ncp workspace."""
-    jb = min(8, n)
+    jb = min(64, n)  # ARENA_JBLOCK
     ncp = (n // 2 + 1 + 7) // 8 * 8
     i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
     rows = ((j // jb) * n + i) * jb + (j % jb)

@@ -23,12 +23,12 @@ def _ilog2(x):
 
 
 class Layout:
-    """Mirror of poisson_pow2.cuh Layout (JB = min(8, nj))."""
+    """Mirror of poisson_pow2.cuh Layout (JB = min(ARENA_JBLOCK = 64, nj))."""
 
     def __init__(self, ni, nj):
         self.ni, self.nj = ni, nj
         self.nis, self.njs = _ilog2(ni), _ilog2(nj)
-        self.jbs = _ilog2(min(8, nj))
+        self.jbs = _ilog2(min(64, nj))
 
     def lrow(self, c, il, jl):
         jb = 1 << self.jbs

@@ -78,6 +78,33 @@ void run_blocked(double2* a, int n, int ncp, int nc, double bytes, int B) {
   printf("blocked B=%3d L=%d E=%d  y %7.1f GB/s   x %7.1f GB/s\n", B, L, E, bytes / ty / 1e6, bytes / tx / 1e6);
 }
 
+// k-tiled layout S[kt][i][j][8 k] (the k axis split in 128-byte tiles, outermost):
+// a y tile (kt, i) is one contiguous 128 KB block, an x tile (kt, j) reads 128 B
+// at a 128 KB stride; blockIdx.x = the line (fastest), blockIdx.y = kt.
+template <int N, int E, int L, bool XPAT>
+__global__ void __launch_bounds__(L * N / E) ktiled_rw(double2* __restrict__ a) {
+  constexpr int P = N / E;
+  const int l = threadIdx.x % L, t = threadIdx.x / L;
+  const long long kt = blockIdx.y, line = blockIdx.x;
+  double2* base = a + kt * (long long)N * N * L + l;
+  double2 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const long long r = t + P * e;
+    v[e] = __ldcs(base + (XPAT ? (r * N + line) : (line * N + r)) * L);
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    v[e].x *= 1.0000001;
+    v[e].y *= 0.9999999;
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const long long r = t + P * e;
+    __stcs(base + (XPAT ? (r * N + line) : (line * N + r)) * L, v[e]);
+  }
+}
+
 __global__ void copy_rw(double2* __restrict__ a, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     double2 v = __ldcs(a + i);
@@ -139,6 +166,12 @@ int main() {
   run_strided<4, 8>(a, n, ncp, nc, bytes);
   run_strided<8, 8>(a, n, ncp, nc, bytes);
   run_strided<16, 16>(a, n, ncp, nc, bytes);
+  {
+    dim3 grid(n, ncp / 8);
+    float ty = time_ms([&] { ktiled_rw<1024, 16, 8, false><<<grid, 8 * 1024 / 16>>>(a); });
+    float tx = time_ms([&] { ktiled_rw<1024, 16, 8, true><<<grid, 8 * 1024 / 16>>>(a); });
+    printf("k-tiled L=8 E=16  y %7.1f GB/s   x %7.1f GB/s\n", bytes / ty / 1e6, bytes / tx / 1e6);
+  }
   for (int B : {1, 2, 4, 8, 16, 32, 64, 128}) {
     run_blocked<4, 16>(a, n, ncp, nc, bytes, B);
     run_blocked<8, 16>(a, n, ncp, nc, bytes, B);

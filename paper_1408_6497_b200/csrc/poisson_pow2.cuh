@@ -772,6 +772,10 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::M
   constexpr int SW = engine_swizzle<M, E>();
   V* sm = smem_base<V>();
   const int l = threadIdx.x % L, t = threadIdx.x / L;
+  if constexpr (ARENA_Z_PF > 0) {  // as k_zfwd: the rows one resident wave ahead into L2
+    const unsigned b = blockIdx.x + C::PF;
+    if (threadIdx.x == 0 && b < gridDim.x) bulk_prefetch_l2(f + size_t(b) * C::L * NR, C::L * NR * sizeof(T));
+  }
   const size_t row = size_t(blockIdx.x) * L + l;  // il * nj + jl
   const V* src = reinterpret_cast<const V*>(f + row * NR);
   V v[E];
@@ -819,6 +823,16 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::M
   const size_t row = size_t(blockIdx.x) * L + l;
   const size_t rin = lrow(gz, 0, int(row >> gz.njs), int(row & (gz.nj - 1)));
   const size_t chunk = size_t(gz.ni) * gz.nj;
+  if constexpr (ARENA_Z_PF > 0) {  // the k-chunks of the rows one resident wave ahead into L2
+    const unsigned b = blockIdx.x + C::PF;
+    const int nch = (M + 1 + kq - 1) / kq;
+    if (b < gridDim.x && threadIdx.x < L * nch) {
+      const size_t rb = size_t(b) * L + threadIdx.x % L;
+      const int c = threadIdx.x / L;
+      const size_t rinb = lrow(gz, 0, int(rb >> gz.njs), int(rb & (gz.nj - 1)));
+      bulk_prefetch_l2(R + (size_t(c) * chunk + rinb) * kq, kq * sizeof(V));
+    }
+  }
   auto get = [&](int k) {
     const int c = k / kq;
     return __ldcs(R + (size_t(c) * chunk + rin) * kq + (k - c * kq));

@@ -95,8 +95,9 @@ struct arena_fft_plan {
   int quad = 0;             // quadrant formulation (poisson_quad.cuh)
   int sm_count = 148;
   // host-boundary resources (lazily allocated)
-  void* d_in = nullptr;
+  void* d_in = nullptr;   // dft3 host paths: n^3 complex
   void* d_out = nullptr;
+  void* d_real = nullptr;  // Poisson host solve: one n^3 real field, solved in place
   void* d_work = nullptr;  // n^3 complex, dft3 only
   cudaStream_t hstream = nullptr;
   std::mutex host_mu;  // one host-path call in flight per plan
@@ -164,6 +165,7 @@ void free_plan(arena_fft_plan* p) {
   if (p->ctrs) cudaFree(p->ctrs);
   if (p->d_in) cudaFree(p->d_in);
   if (p->d_out) cudaFree(p->d_out);
+  if (p->d_real) cudaFree(p->d_real);
   if (p->d_work) cudaFree(p->d_work);
   if (p->hstream) cudaStreamDestroy(p->hstream);
   for (int b = 0; b < 2; ++b) {
@@ -251,10 +253,29 @@ arena_status enqueue_kernels(arena_fft_plan* p, const void* d_f, void* d_u, cuda
   return ARENA_OK;
 }
 
-arena_status ensure_host_buffers(arena_fft_plan* p, bool work) {
+arena_status ensure_host_stream(arena_fft_plan* p) {
   cudaError_t e;
   if (!p->hstream && (e = cudaStreamCreateWithFlags(&p->hstream, cudaStreamNonBlocking)) != cudaSuccess)
     return cuda_fail(e, "cudaStreamCreate");
+  return ARENA_OK;
+}
+
+// The Poisson host solve moves f in, solves in place (every path reads all of
+// f before it writes u) and moves u out: f + workspace on the device, so a
+// 2048^3 fp64 GridField (68.7 GB) fits one B200 with its 69 GB workspace.
+arena_status ensure_real_buffer(arena_fft_plan* p) {
+  arena_status st = ensure_host_stream(p);
+  if (st != ARENA_OK) return st;
+  cudaError_t e;
+  if (!p->d_real && (e = cudaMalloc(&p->d_real, p->real_bytes())) != cudaSuccess)
+    return fail(ARENA_ENOMEM, "device field buffer: " + std::string(cudaGetErrorString(e)));
+  return ARENA_OK;
+}
+
+arena_status ensure_host_buffers(arena_fft_plan* p, bool work) {
+  cudaError_t e;
+  arena_status st = ensure_host_stream(p);
+  if (st != ARENA_OK) return st;
   const size_t cb = size_t(p->n) * p->n * p->n * 2 * p->elem;  // n^3 complex (covers n^3 real)
   if (!p->d_in && (e = cudaMalloc(&p->d_in, cb)) != cudaSuccess)
     return fail(ARENA_ENOMEM, "device input buffer: " + std::string(cudaGetErrorString(e)));
@@ -436,13 +457,13 @@ arena_status arena_poisson_solve_host(arena_fft_plan* p, const void* f, void* u)
   if (!p || !f || !u) return fail(ARENA_EINVAL, "NULL plan or buffer");
   DeviceGuard g(p->device);
   std::lock_guard<std::mutex> lk(p->host_mu);
-  arena_status st = ensure_host_buffers(p, false);
+  arena_status st = ensure_real_buffer(p);
   if (st != ARENA_OK) return st;
   const size_t bytes = p->real_bytes();
-  cudaError_t e = host_copy(p, p->d_in, f, bytes, false);  // pageable GridField data: staged
+  cudaError_t e = host_copy(p, p->d_real, f, bytes, false);  // pageable GridField data: staged
   if (e != cudaSuccess) return cuda_fail(e, "H2D f");
-  if ((st = enqueue_solve(p, p->d_in, p->d_out, p->hstream)) != ARENA_OK) return st;
-  if ((e = host_copy(p, u, p->d_out, bytes, true)) != cudaSuccess) return cuda_fail(e, "D2H u");
+  if ((st = enqueue_solve(p, p->d_real, p->d_real, p->hstream)) != ARENA_OK) return st;
+  if ((e = host_copy(p, u, p->d_real, bytes, true)) != cudaSuccess) return cuda_fail(e, "D2H u");
   return ARENA_OK;
 }
 
@@ -453,7 +474,7 @@ arena_status arena_poisson_solve_host_batch(arena_fft_plan* p, int count, const 
   if (!p || count < 0 || (count && (!f || !u))) return fail(ARENA_EINVAL, "NULL plan or buffer list");
   DeviceGuard g(p->device);
   std::lock_guard<std::mutex> lk(p->host_mu);
-  arena_status st = ensure_host_buffers(p, false);
+  arena_status st = ensure_host_stream(p);
   if (st != ARENA_OK) return st;
   cudaError_t e;
   const size_t bytes = p->real_bytes();

@@ -238,7 +238,9 @@ __device__ __forceinline__ int smem_idx(int pos, int l) {
 // tables in shared memory measured no faster on B200, and a plain generic
 // load made the classic x kernel 30% slower.)
 #ifndef ARENA_TW_LD
-#define ARENA_TW_LD 1  // 0: ld.global.nc, 1: ld.global.nc.L1::evict_last (B200 A/B: -0.3 ms per solve with ST_MODE 2)
+#define ARENA_TW_LD 0  // 0: ld.global.nc, 1: ld.global.nc.L1::evict_last (B200 A/B: evict_last saved 0.3 ms
+                       // per 1024^3 solve with 8-row j blocks; with 64-row blocks plain loads win:
+                       // 16.38 -> 16.24 ms, y passes 3.20 -> 3.10 ms; 2048^3 +0.5%)
 #endif
 #ifndef ARENA_ST_MODE
 #define ARENA_ST_MODE 2  // data stores: 0 st.global.cs, 1 st.global, 2 st.global.L1::no_allocate

@@ -7,6 +7,13 @@
 namespace arena_fft {
 
 constexpr int kPow2MaxN = 2048;
+
+// Row pitch (complex elements) of the half spectrum for an n-point grid: nc =
+// n/2 + 1 rounded up to 8 (128-byte fp64 rows), plus ARENA_PITCH_PAD extra units.
+#ifndef ARENA_PITCH_PAD
+#define ARENA_PITCH_PAD 0
+#endif
+__host__ __device__ constexpr int spec_pitch(int n) { return (n / 2 + 1 + 7) / 8 * 8 + 8 * ARENA_PITCH_PAD; }
 constexpr int kMaxPeers = 8;  // ranks a slab solve can scatter to directly (peer-mapped workspaces)
 constexpr int kPow2Launches = 5;
 

@@ -343,7 +343,7 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
   p->device = device;
   p->elem = precision_bits == 64 ? 8 : 4;
   p->nc = n / 2 + 1;
-  p->ncp = (p->nc + 7) / 8 * 8;
+  p->ncp = spec_pitch(n);  // poisson_pow2.cuh (the kernels check it)
   p->sm_count = prop.multiProcessorCount;
   {
     const char* gr = std::getenv("ARENA_FFT_GRAPHS");  // "0" disables graph replay

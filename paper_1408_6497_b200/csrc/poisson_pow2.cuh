@@ -30,7 +30,7 @@ __host__ __device__ constexpr int pow2_floor(int x) { return x <= 1 ? 1 : 2 * po
 
 // Row pitch (complex elements) of the half spectrum for an n-point grid; the
 // plan allocates with the same formula (plan.cu).
-__host__ __device__ constexpr int spec_pitch(int n) { return (n / 2 + 1 + 7) / 8 * 8; }
+// spec_pitch(n): launchers.h (shared with the plan's allocation)
 
 // Tuning knobs (compile-time; variants are built side by side for A/B runs).
 #ifndef ARENA_STRIDED_MINB

@@ -373,6 +373,15 @@ def get_plan(n: int, precision: int = 64, device: int = -1) -> Plan:
         return p
 
 
+def clear_plan_cache() -> None:
+    """Destroy the cached plans (their workspaces and host-path buffers)."""
+    with _plans_lock:
+        plans = list(_plans.values())
+        _plans.clear()
+    for p in plans:
+        p.close()
+
+
 def _as_grid(f: np.ndarray, dtype) -> np.ndarray:
     f = np.ascontiguousarray(f, dtype=dtype)
     if f.ndim != 3 or not (f.shape[0] == f.shape[1] == f.shape[2]):

@@ -45,6 +45,11 @@ __host__ __device__ constexpr int pow2_floor(int x) { return x <= 1 ? 1 : 2 * po
 #ifndef ARENA_CONTIG_LARGE_N
 #define ARENA_CONTIG_LARGE_N 2048
 #endif
+#ifndef ARENA_CONTIG_LARGE_E
+#define ARENA_CONTIG_LARGE_E 32  // points per thread of the z kernels for n >= ARENA_CONTIG_LARGE_N: 64-thread
+                                 // CTAs, 4 per SM, 255 registers (B200 2048^3 plain path: z 27.5 -> 24.7 ms;
+                                 // 16 points at 128 registers was the earlier choice)
+#endif
 #ifndef ARENA_CONTIG_SMALL_N
 #define ARENA_CONTIG_SMALL_N 512  // B200: 512^3 z passes 0.50 -> 0.39 ms, 256^3 0.10 -> 0.07 ms
 #endif
@@ -100,10 +105,10 @@ struct ContigCfg {  // z passes: rows of NR reals = M = NR/2 complex
   // resident warps (B200, 256^3: z passes 0.10 -> 0.07 ms; at n = 1024 E = 16
   // with 16 CTAs/SM spills).
   static constexpr bool SMALL = NR <= ARENA_CONTIG_SMALL_N;
-  // n >= ARENA_CONTIG_LARGE_N (2048: M = 1024): E = 32 spills ~1 KB, so 16 points
-  // per thread with half the CTAs per SM (128 registers).
+  // n >= ARENA_CONTIG_LARGE_N (2048: M = 1024): half the CTAs per SM, so E = 32
+  // (ARENA_CONTIG_LARGE_E) has 255 registers and does not spill.
   static constexpr bool LARGE = NR >= ARENA_CONTIG_LARGE_N;
-  static constexpr int E = imin((SMALL || LARGE) ? 16 : ARENA_CONTIG_E, M);
+  static constexpr int E = imin(SMALL ? 16 : LARGE ? ARENA_CONTIG_LARGE_E : ARENA_CONTIG_E, M);
   static constexpr int MINB = SMALL ? 2 * ARENA_CONTIG_MINB : (LARGE ? ARENA_CONTIG_MINB / 2 : ARENA_CONTIG_MINB);
   static constexpr int P = M / E;
   static constexpr int VB = 2 * sizeof(T);

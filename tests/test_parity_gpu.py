@@ -673,3 +673,44 @@ def test_repeat_bitwise_deterministic(cuda, n, precision, quad, monkeypatch):
         p.solve_device(f, u)
         torch.cuda.synchronize()
         assert torch.equal(u, u0)
+
+
+@pytest.mark.parametrize("quad", ["1", "0"])
+def test_2048_in_place_analytic(cuda, quad, monkeypatch):
+    """2048^3 (config 5's source, alpha = 1e5) on one GPU, solved in place (f +
+    workspace = 138 GB), both formulations, against the analytic solution checked
+    block by block of planes (gauge-aligned relative L2, problems.cpp:88-106)."""
+    torch = cuda
+    if torch.cuda.get_device_properties(0).total_memory < 150e9:
+        pytest.skip("needs a 180 GB device")
+    import gc
+
+    arena.clear_plan_cache()  # earlier tests' cached plans hold their workspaces
+    gc.collect()
+    torch.cuda.empty_cache()
+    monkeypatch.setenv("ARENA_FFT_QUAD", quad)
+    n, block = 2048, 64
+    src = problems.config(5, n)
+    f = torch.empty((n, n, n), dtype=torch.float64, device="cuda")
+    problems.fill_device(src, "f", f)
+    f -= f.mean()
+    p = arena.Plan(n)
+    p.solve_device(f, f)
+    torch.cuda.synchronize()
+    del p
+    buf = torch.empty((block, n, n), dtype=torch.float64, device="cuda")
+    su = sa = 0.0
+    for i0 in range(0, n, block):
+        problems.fill_device(src, "u", buf, 64, 0, i0, block)
+        su += f[i0:i0 + block].sum().item()
+        sa += buf.sum().item()
+    shift, mean_e = (sa - su) / n ** 3, sa / n ** 3
+    d2 = e2 = 0.0
+    for i0 in range(0, n, block):
+        problems.fill_device(src, "u", buf, 64, 0, i0, block)
+        d = f[i0:i0 + block] + shift - buf
+        d2 += (d * d).sum().item()
+        e2 += ((buf - mean_e) ** 2).sum().item()
+    del f, buf
+    torch.cuda.empty_cache()
+    assert (d2 / e2) ** 0.5 <= 1e-12

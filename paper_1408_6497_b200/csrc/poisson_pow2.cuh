@@ -469,6 +469,9 @@ namespace arena_fft {
 #ifndef ARENA_TMA_LROW
 #define ARENA_TMA_LROW 128  // bytes of a tile row (L adjacent k) at most
 #endif
+#ifndef ARENA_TMA_Y_TINY
+#define ARENA_TMA_Y_TINY 0  // tile bytes up to which the y passes run four CTAs per SM (0: never)
+#endif
 #ifndef ARENA_TMA_Y_SMALL
 #define ARENA_TMA_Y_SMALL 65536  // tile bytes up to which the y passes run two CTAs per SM (512^3: y 0.53 -> 0.46 ms)
 #endif
@@ -524,7 +527,9 @@ struct TmaCfg {
   static constexpr int MINB0 = WIDEX ? 1
                                : YP ? (F64 ? ARENA_TMA_MINB_Y : ARENA_TMA_MINB_Y32) : (F64 ? ARENA_TMA_MINB : ARENA_TMA_MINB32);
   // y passes with tiles of <= 64 KB (n <= 512): two CTAs per SM
-  static constexpr int MINB = (YP && N * L * VB <= ARENA_TMA_Y_SMALL) ? imax(MINB0, 2) : MINB0;
+  static constexpr int MINB = (YP && N * L * VB <= ARENA_TMA_Y_TINY)    ? imax(MINB0, 4)
+                              : (YP && N * L * VB <= ARENA_TMA_Y_SMALL) ? imax(MINB0, 2)
+                                                                        : MINB0;
   static constexpr int THREADS = L * P;
   static constexpr int NC = N / 2 + 1;
   static constexpr int KT = (NC + L - 1) / L;  // k tiles per line set

@@ -21,3 +21,5 @@ python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > $O/bench_small.json 2>&
 python tools/solve_once.py --n 1024 --reps 1 > $O/solve_once.log 2>&1 && \
   ncu --set full --import-source on --clock-control none -k regex:"k_z|k_strided" -c 5 -o $O/full_1024_fp64 \
       python tools/solve_once.py --n 1024 --reps 1 > $O/ncu_full.log 2>&1; echo "ncu full rc=$?"
+
+python tools/summarize_profiles.py > /dev/null 2>&1 || true  # (run here after copying the lines into profiles/)

@@ -714,3 +714,42 @@ def test_2048_in_place_analytic(cuda, quad, monkeypatch):
     del f, buf
     torch.cuda.empty_cache()
     assert (d2 / e2) ** 0.5 <= 1e-12
+
+
+@pytest.mark.parametrize("n", [12, 30, 48, 96])
+def test_random_generic_fp32_vs_oracle(cuda, n):
+    """Generic (mixed-radix) path in fp32 against the fp64 oracle of the rounded input."""
+    torch = cuda
+    f = torch.from_numpy(np.random.default_rng(n + 11).uniform(-1, 1, (n, n, n))).float().cuda()
+    u = torch.empty_like(f)
+    p = arena.Plan(n, 32)
+    assert p.path == arena.PATH_GENERIC
+    p.solve_device(f, u)
+    torch.cuda.synchronize()
+    assert _rel(u.double().cpu().numpy(), oracle.poisson_solve(f.double().cpu().numpy())) <= TOL32
+
+
+@pytest.mark.parametrize("n", [384, 768])
+def test_generic_large_analytic(cuda, n):
+    """Generic path at 3 * 2^k sizes (radix-8/4/3 plans, the fused x-symbol pass)
+    against the analytic solution of config 4's source (64 modes, |k| <= 32)."""
+    torch = cuda
+    src, f, ua = _config_device(torch, 4, n)
+    u = torch.empty_like(f)
+    p = arena.Plan(n)
+    assert p.path == arena.PATH_GENERIC
+    p.solve_device(f, u)
+    torch.cuda.synchronize()
+    e = (torch.linalg.vector_norm(u - ua) / torch.linalg.vector_norm(ua)).item()
+    assert e <= 1e-12, e
+
+
+@pytest.mark.parametrize("n", [6, 10, 24, 60])
+def test_dft3_round_trip_generic(cuda, n):
+    """dft3_inverse(dft3_forward(g)) == g (fft_solver.cpp:13-49 conventions), and the
+    forward transform against numpy's, at non-power-of-two n."""
+    g = np.random.default_rng(n + 5).uniform(-1, 1, (n, n, n))
+    spec = arena.dft3_forward(g)
+    assert np.abs(spec - np.fft.fftn(g)).max() <= 1e-12 * np.abs(spec).max()
+    back = arena.dft3_inverse(spec, n)
+    assert np.abs(back - g).max() <= 1e-12

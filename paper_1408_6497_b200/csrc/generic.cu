@@ -5,9 +5,10 @@
 // 128-byte rows), Stockham stages with compile-time radix-2/3/4/5/7/8
 // butterflies (constant twiddles) and a direct O(R) sum for larger prime
 // factors; every n >= 2 is handled.  Five sweeps: the x pass runs forward *
-// symbol * backward in one kernel (G_XPOISSON).  B200, fp64: 384^3 in 5.2 ms,
-// 768^3 in 37 ms, 1000^3 in 85 ms (seven sweeps and table twiddles: 6.8 / 83 /
-// 156 ms; the power-of-two path: 1024^3 in 17.4 ms).
+// symbol * backward in one kernel (G_XPOISSON), the z passes transform two real
+// rows per complex line (G_R2C_PAIR / G_C2R_PAIR).  B200, fp64: 384^3 in 3.9 ms,
+// 768^3 in 28 ms, 1000^3 in 61 ms (seven sweeps, table twiddles, one row per
+// line: 6.8 / 83 / 156 ms; the power-of-two path: 1024^3 in 16.4 ms).
 //
 // Same conventions as fft_solver.cpp: r2c along the last axis keeping
 // k in [0, n/2], c2r treating its input as Hermitian (imaginary parts of the
@@ -26,7 +27,12 @@ namespace {
 // G_XPOISSON: the x pass of the solve in one sweep — forward stages, the
 // Poisson symbol of fft_solver.cpp:66-79, backward stages (as K3 of the
 // power-of-two path), so the solve is five sweeps instead of seven.
-enum GenMode { G_R2C = 0, G_C2R = 1, G_C2C = 2, G_R2C_FULL = 3, G_C2C_TO_REAL = 4, G_XPOISSON = 5 };
+// G_R2C_PAIR / G_C2R_PAIR: the solve's z passes with two real rows packed into
+// one complex line (row 2q in the real part, row 2q+1 in the imaginary part), so
+// one n-point complex FFT serves two rows; the Hermitian split / merge happens on
+// the way out / in.
+enum GenMode { G_R2C = 0, G_C2R = 1, G_C2C = 2, G_R2C_FULL = 3, G_C2C_TO_REAL = 4, G_XPOISSON = 5,
+               G_R2C_PAIR = 6, G_C2R_PAIR = 7 };
 
 // cos / sin(2 pi m / R), 0 <= m < R, for the odd radices with compile-time
 // butterflies (literal constants: folded once the loops are unrolled).
@@ -182,8 +188,34 @@ __global__ void k_gen_lines(const void* in, void* out, GenPlan pl, GenGeom g,
     }
   };
 
+  // pair modes: line l packs rows 2q and 2q+1 (q = q0 + l); nlines counts rows, cnt_b == 1
+  auto row_ok = [&](long long r) { return r < nlines; };
+
   // ---- load
-  if (MODE == G_C2R) {
+  if constexpr (MODE == G_R2C_PAIR) {
+    const T* src = static_cast<const T*>(in);
+    for (int idx = threadIdx.x; idx < L * n; idx += blockDim.x) {
+      int l, x;
+      split(idx, n, l, x);
+      const long long ra = 2 * (q0 + l), rb = ra + 1;
+      b0[x * L + l] = V{row_ok(ra) ? src[ra * g.sa + x] : T(0), row_ok(rb) ? src[rb * g.sa + x] : T(0)};
+    }
+  } else if constexpr (MODE == G_C2R_PAIR) {
+    const V* src = static_cast<const V*>(in);
+    for (int idx = threadIdx.x; idx < L * nc; idx += blockDim.x) {
+      int l, k;
+      split(idx, nc, l, k);
+      const long long ra = 2 * (q0 + l), rb = ra + 1;
+      V A = row_ok(ra) ? src[ra * g.sa + k] : V{T(0), T(0)};
+      V B = row_ok(rb) ? src[rb * g.sa + k] : V{T(0), T(0)};
+      if (k == 0 || 2 * k == n) {  // self-conjugate modes: imaginary parts ignored
+        A.y = T(0);
+        B.y = T(0);
+      }
+      b0[k * L + l] = V{A.x - B.y, A.y + B.x};                                  // A + i B
+      if (k > 0 && n - k != k) b0[(n - k) * L + l] = V{A.x + B.y, B.x - A.y};  // conj(A) + i conj(B)
+    }
+  } else if (MODE == G_C2R) {
     const V* src = static_cast<const V*>(in);
     for (int idx = threadIdx.x; idx < L * nc; idx += blockDim.x) {
       int l, k;
@@ -251,6 +283,31 @@ __global__ void k_gen_lines(const void* in, void* out, GenPlan pl, GenGeom g,
   }
 
   // ---- store
+  if constexpr (MODE == G_R2C_PAIR) {
+    V* dst = static_cast<V*>(out);
+    for (int idx = threadIdx.x; idx < L * nc; idx += blockDim.x) {
+      int l, k;
+      split(idx, nc, l, k);
+      const long long ra = 2 * (q0 + l), rb = ra + 1;
+      const V Z = b0[k * L + l], Zm = b0[((n - k) % n) * L + l];
+      // row a: (Z + conj(Zm)) / 2, row b: (Z - conj(Zm)) / 2i
+      if (row_ok(ra)) dst[ra * g.osa + k] = V{T(0.5) * (Z.x + Zm.x), T(0.5) * (Z.y - Zm.y)};
+      if (row_ok(rb)) dst[rb * g.osa + k] = V{T(0.5) * (Z.y + Zm.y), T(0.5) * (Zm.x - Z.x)};
+    }
+    return;
+  }
+  if constexpr (MODE == G_C2R_PAIR) {
+    T* dst = static_cast<T*>(out);
+    for (int idx = threadIdx.x; idx < L * n; idx += blockDim.x) {
+      int l, x;
+      split(idx, n, l, x);
+      const long long ra = 2 * (q0 + l), rb = ra + 1;
+      const V v = b0[x * L + l];
+      if (row_ok(ra)) dst[ra * g.osa + x] = v.x * out_scale;
+      if (row_ok(rb)) dst[rb * g.osa + x] = v.y * out_scale;
+    }
+    return;
+  }
   const int cnt = MODE == G_R2C ? nc : n;
   for (int idx = threadIdx.x; idx < L * cnt; idx += blockDim.x) {
     int l, x;
@@ -288,7 +345,8 @@ cudaError_t run_lines(const GenArgs& a, const void* in, void* out, long long nli
     if (e != cudaSuccess) return e;
     attr_done[dev & 63] = true;
   }
-  const long long blocks = (nlines + L - 1) / L;
+  const long long units = (MODE == G_R2C_PAIR || MODE == G_C2R_PAIR) ? (nlines + 1) / 2 : nlines;  // pairs of rows
+  const long long blocks = (units + L - 1) / L;
   k_gen_lines<T, MODE><<<unsigned(blocks), 256, smem, a.stream>>>(
       in, out, *a.plan, g, static_cast<const vec2_t<T>*>(a.tw), sign, a.nc, out_scale, L, nlines);
   return cudaGetLastError();
@@ -305,7 +363,7 @@ cudaError_t gen_poisson(const GenArgs& a, const void* f, void* u, void* spec) {
   cudaError_t e;
   // z r2c: rows of f -> rows of S
   gmark(a, 0);
-  e = run_lines<T, G_R2C>(a, f, spec, nn, GenGeom{n, 0, 1, ncp, 0, 1, 1, 1}, -1, T(1));
+  e = run_lines<T, G_R2C_PAIR>(a, f, spec, nn, GenGeom{n, 0, 1, ncp, 0, 1, 1, 1}, -1, T(1));
   if (e) return e;
   // y c2c forward: lines (i, k), element j at i*n*ncp + k + j*ncp
   GenGeom gy{(long long)n * ncp, 1, ncp, (long long)n * ncp, 1, ncp, ncp, nc};
@@ -321,7 +379,7 @@ cudaError_t gen_poisson(const GenArgs& a, const void* f, void* u, void* spec) {
   if ((e = run_lines<T, G_C2C>(a, spec, spec, (long long)n * ncp, gy, +1, T(1)))) return e;
   // z c2r: rows of S -> rows of u
   gmark(a, 4);
-  e = run_lines<T, G_C2R>(a, spec, u, nn, GenGeom{ncp, 0, 1, n, 0, 1, 1, 1}, +1, T(1));
+  e = run_lines<T, G_C2R_PAIR>(a, spec, u, nn, GenGeom{ncp, 0, 1, n, 0, 1, 1, 1}, +1, T(1));
   gmark(a, 5);
   return e;
 }

@@ -136,7 +136,9 @@ def algorithmic_bytes(n: int, elem: int):
            "zy_fused_fwd": R + C, "yz_fused_inv": C + R,
            # generic (any n) path: five sweeps (x forward * symbol * x backward fused)
            "gen_z_r2c": R + C, "gen_y_fwd": 2 * C, "gen_xmid_fwd_scale_inv": 2 * C,
-           "gen_y_inv": 2 * C, "gen_z_c2r": C + R}
+           "gen_y_inv": 2 * C, "gen_z_c2r": C + R,
+           # radix-3 split path (n = 3M): two extra spectrum sweeps (split, merge)
+           "split3_fwd": 2 * C, "split3_inv": 2 * C}
     return per, 2 * R + 8 * C
 
 

@@ -434,6 +434,22 @@ bool gen_plan_make(int n, GenPlan* p) {
 size_t gen_smem_bytes(int n, int elem_bytes) { return size_t(2) * n * elem_bytes; }
 int gen_max_n(int elem_bytes) { return (227 * 1024) / (2 * elem_bytes); }
 
+// The solve's z passes alone (the radix-3 split path runs its own y / x passes).
+template <typename T>
+cudaError_t gen_z_r2c(const GenArgs& a, const void* f, void* spec) {
+  const long long nn = (long long)a.n * a.n;
+  return run_lines<T, G_R2C_PAIR>(a, f, spec, nn, GenGeom{a.n, 0, 1, a.ncp, 0, 1, 1, 1}, -1, T(1));
+}
+template <typename T>
+cudaError_t gen_z_c2r(const GenArgs& a, const void* spec, void* u) {
+  const long long nn = (long long)a.n * a.n;
+  return run_lines<T, G_C2R_PAIR>(a, spec, u, nn, GenGeom{a.ncp, 0, 1, a.n, 0, 1, 1, 1}, +1, T(1));
+}
+cudaError_t gen_z_r2c_f64(const GenArgs& a, const void* f, void* spec) { return gen_z_r2c<double>(a, f, spec); }
+cudaError_t gen_z_r2c_f32(const GenArgs& a, const void* f, void* spec) { return gen_z_r2c<float>(a, f, spec); }
+cudaError_t gen_z_c2r_f64(const GenArgs& a, const void* spec, void* u) { return gen_z_c2r<double>(a, spec, u); }
+cudaError_t gen_z_c2r_f32(const GenArgs& a, const void* spec, void* u) { return gen_z_c2r<float>(a, spec, u); }
+
 cudaError_t gen_poisson_f64(const GenArgs& a, const void* f, void* u, void* spec) {
   return gen_poisson<double>(a, f, u, spec);
 }

@@ -143,6 +143,35 @@ struct GenArgs {
 cudaError_t gen_poisson_f64(const GenArgs& a, const void* f, void* u, void* spec);
 cudaError_t gen_poisson_f32(const GenArgs& a, const void* f, void* u, void* spec);
 constexpr int kGenLaunches = 5;
+// The generic z passes alone (rows' r2c into the generic layout / c2r back).
+cudaError_t gen_z_r2c_f64(const GenArgs& a, const void* f, void* spec);
+cudaError_t gen_z_r2c_f32(const GenArgs& a, const void* f, void* spec);
+cudaError_t gen_z_c2r_f64(const GenArgs& a, const void* spec, void* u);
+cudaError_t gen_z_c2r_f32(const GenArgs& a, const void* spec, void* u);
+
+// Radix-3 split path for n = 3M, M a power of two in [16, 512] (poisson_split3.cuh).
+constexpr int kSplit3Launches = 7;
+struct Split3Args {
+  const void* f;
+  void* u;
+  void* S;          // generic-layout half spectrum (n*n rows of ncp)
+  void* Q;          // nine chunks of Layout(M, M) rows of ncp
+  const void* tw;   // W_n^m
+  const void* stw;  // stage-twiddle tables of an n' = 2M plan (M-point lines: which = 0)
+  int n, M, nc, ncp;
+  cudaStream_t stream;
+  cudaEvent_t* ev;  // nullable; kSplit3Launches + 1 events
+  TmaCache* tma;
+  int sm_count;
+  const GenPlan* gplan;
+};
+inline bool split3_ok(int n) {
+  if (n % 3) return false;
+  const int M = n / 3;
+  return M >= 16 && M <= 512 && (M & (M - 1)) == 0;
+}
+cudaError_t launch_split3_f64(const Split3Args& a);
+cudaError_t launch_split3_f32(const Split3Args& a);
 // dft3_forward: real g (n^3) -> complex spec (n^3, interleaved).  dft3_inverse:
 // complex spec -> real g = Re(backward)/n^3 using `work` (n^3 complex) as scratch.
 cudaError_t gen_dft3_forward_f64(const GenArgs& a, const void* g, void* spec);

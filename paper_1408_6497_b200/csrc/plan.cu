@@ -53,6 +53,8 @@ const char* kStageNames[4][kPow2Launches] = {
     {"zy_fused_fwd", "xmid_fwd_scale_inv", "yinv", "zinv_c2r", nullptr},
     {"zfwd_r2c", "yfwd", "xmid_fwd_scale_inv", "yz_fused_inv", nullptr},
     {"zy_fused_fwd", "xmid_fwd_scale_inv", "yz_fused_inv", nullptr, nullptr}};
+const char* kSplit3Names[kSplit3Launches] = {"gen_z_r2c", "split3_fwd", "yfwd", "xmid_fwd_scale_inv", "yinv",
+                                             "split3_inv", "gen_z_c2r"};
 const char* kGenNames[kGenLaunches] = {"gen_z_r2c", "gen_y_fwd", "gen_xmid_fwd_scale_inv", "gen_y_inv",
                                        "gen_z_c2r"};
 
@@ -93,6 +95,8 @@ struct arena_fft_plan {
   int lag = 2;
   int fuse = 0;             // kFuseFwd | kFuseInv
   int quad = 0;             // quadrant formulation (poisson_quad.cuh)
+  bool split3 = false;      // generic n = 3M: radix-3 split onto the power-of-two passes (poisson_split3.cuh)
+  void* Q = nullptr;        // split3: nine-chunk workspace
   int sm_count = 148;
   // host-boundary resources (lazily allocated)
   void* d_in = nullptr;   // dft3 host paths: n^3 complex
@@ -115,7 +119,7 @@ struct arena_fft_plan {
   std::mutex ev_mu;
 
   int launches() const {
-    if (path != ARENA_PATH_POW2) return kGenLaunches;
+    if (path != ARENA_PATH_POW2) return split3 ? kSplit3Launches : kGenLaunches;
     return kPow2Launches - ((ctrs && (fuse & kFuseFwd)) ? 1 : 0) - ((ctrs && (fuse & kFuseInv)) ? 1 : 0);
   }
   size_t real_bytes() const { return size_t(n) * n * n * elem; }
@@ -145,10 +149,11 @@ arena_status make_twiddles(arena_fft_plan* p) {
   if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? fail(ARENA_ENOMEM, "twiddle table") : cuda_fail(e, "cudaMalloc");
   e = cudaMemcpy(p->tw, host.data(), host.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "twiddle upload");
-  if (p->path == ARENA_PATH_POW2) {
-    const size_t ns = stw_entries(n);
+  if (p->path == ARENA_PATH_POW2 || p->split3) {
+    const int nt = p->split3 ? 2 * (n / 3) : n;  // split3: M-point lines = the n/2 tables of n' = 2M
+    const size_t ns = stw_entries(nt);
     std::vector<unsigned char> st(std::max<size_t>(ns, 1) * vb);
-    stw_fill_host(n, p->prec, st.data());
+    stw_fill_host(nt, p->prec, st.data());
     if ((e = cudaMalloc(&p->stw, st.size())) != cudaSuccess) return fail(ARENA_ENOMEM, "stage twiddle tables");
     if ((e = cudaMemcpy(p->stw, st.data(), st.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
       return cuda_fail(e, "stage twiddle upload");
@@ -160,6 +165,7 @@ void free_plan(arena_fft_plan* p) {
   if (!p) return;
   DeviceGuard g(p->device);
   if (p->spec) cudaFree(p->spec);
+  if (p->Q) cudaFree(p->Q);
   if (p->tw) cudaFree(p->tw);
   if (p->stw) cudaFree(p->stw);
   if (p->ctrs) cudaFree(p->ctrs);
@@ -245,6 +251,10 @@ arena_status enqueue_kernels(arena_fft_plan* p, const void* d_f, void* d_u, cuda
                /*ni*/ p->n, /*nj*/ p->n, /*nchunks*/ 1, /*j0*/ 0, /*specC*/ p->spec, kPhaseAll, p->ctrs, p->lag, p->fuse};
     a.quad = p->quad;
     e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
+  } else if (p->split3) {
+    Split3Args a{d_f, d_u, p->spec, p->Q, p->tw, p->stw, p->n, p->n / 3, p->nc, p->ncp, s, ev, p->tma, p->sm_count,
+                 &p->gplan};
+    e = p->prec == 64 ? launch_split3_f64(a) : launch_split3_f32(a);
   } else {
     GenArgs a{&p->gplan, p->tw, p->n, p->nc, p->ncp, s, ev};
     e = p->prec == 64 ? gen_poisson_f64(a, d_f, d_u, p->spec) : gen_poisson_f32(a, d_f, d_u, p->spec);
@@ -392,6 +402,20 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
       free_plan(p);
       return fail(ARENA_EUNSUPPORTED, "n = " + std::to_string(n) + " exceeds the generic path's shared-memory line limit");
     }
+    // n = 3M, M a power of two in [16, 512]: y / x passes on the power-of-two TMA kernels
+    // (poisson_split3.cuh).  ARENA_FFT_SPLIT3 = 0 keeps the generic stages.
+    {
+      const char* sz = std::getenv("ARENA_FFT_SPLIT3");
+      const char* kern = std::getenv("ARENA_FFT_KERNELS");
+      if (split3_ok(n) && !(sz && std::string(sz) == "0") && !(kern && std::string(kern) == "classic")) {
+        p->split3 = true;
+        p->tma = new (std::nothrow) TmaCache;
+        if (!p->tma) {
+          free_plan(p);
+          return fail(ARENA_ENOMEM, "TMA cache");
+        }
+      }
+    }
   }
   arena_status st = make_twiddles(p);
   if (st != ARENA_OK) {
@@ -404,6 +428,10 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
       free_plan(p);
       return fail(ARENA_ENOMEM,
                   "half-spectrum workspace (" + std::to_string(p->spec_bytes) + " B): " + cudaGetErrorString(e));
+    }
+    if (p->split3 && (e = cudaMalloc(&p->Q, p->spec_bytes)) != cudaSuccess) {
+      free_plan(p);
+      return fail(ARENA_ENOMEM, "split3 workspace: " + std::string(cudaGetErrorString(e)));
     }
   }
   *out = p;
@@ -622,7 +650,7 @@ arena_status arena_fft_stage_times(arena_fft_plan* p, double* ms, const char** n
     ++p->solves;
   }
   p->ev_sets_used = 0;
-  const char** nm = p->path == ARENA_PATH_POW2 ? kStageNames[p->ctrs ? p->fuse : 0] : kGenNames;
+  const char** nm = p->path == ARENA_PATH_POW2 ? kStageNames[p->ctrs ? p->fuse : 0] : p->split3 ? kSplit3Names : kGenNames;
   for (int k = 0; k < L && k < max_stages; ++k) {
     if (ms) ms[k] = p->stage_ms[k];
     if (names) names[k] = nm[k];

@@ -572,34 +572,37 @@ struct PeerOut {
   int shift;
 };
 
-// QUAD: the quadrant layout of an n = 2N grid (poisson_quad.cuh): four chunks of
-// N x N rows, one per (i parity, j parity) of the frequency; lines stay inside a
-// chunk, tile index gt = (chunk * lines + outer) * KT + k-tile, and the symbol
-// reads ki = 2 i' + ci, kj = 2 j' + cj of the n-point transform.
-template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false, bool QUAD = false>
-__global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, QUAD>()>::THREADS,
-                                  TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, QUAD>()>::MINB)
+// SPL = 2: the quadrant layout of an n = 2N grid (poisson_quad.cuh): four chunks
+// of N x N rows, one per (i parity, j parity) of the frequency; SPL = 3: nine
+// chunks of an n = 3N grid (poisson_split3.cuh).  Lines stay inside a chunk,
+// tile index gt = (chunk * lines + outer) * KT + k-tile, and the symbol reads
+// ki = SPL i' + ci, kj = SPL j' + cj of the n-point transform (chunk = SPL ci + cj).
+template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false, int SPL = 0>
+__global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, (SPL > 0)>()>::THREADS,
+                                  TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, (SPL > 0)>()>::MINB)
     k_strided_tma(const __grid_constant__ CUtensorMap tmap, vec2_t<T>* __restrict__ spec,
                   const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g_, int nchunks_, int j0_, KSpan ks_,
                   vec2_t<T>* __restrict__ out_, Layout gout_, const __grid_constant__ PeerOut<vec2_t<T>> po) {
   static_assert(!(FIXED && PEER), "the fixed geometry is the single-GPU one");
+  constexpr bool QUAD = SPL > 0;
   static_assert(!(QUAD && PEER), "the quadrant layout is single-GPU");
   const Layout g = FIXED ? fixed_layout<N>() : g_;
   const Layout gout = FIXED ? fixed_layout<N>() : gout_;
   const int nchunks = FIXED ? 1 : nchunks_;
   const int j0 = FIXED ? 0 : j0_;
   // FIXED: the single-GPU geometry (QUAD: a chunk of the 2N grid's quadrant layout)
-  const KSpan ks = FIXED ? (QUAD ? KSpan{N + 1, spec_pitch(2 * N), 0} : KSpan{N / 2 + 1, spec_pitch(N), 0}) : ks_;
+  const KSpan ks = FIXED ? (QUAD ? KSpan{SPL * N / 2 + 1, spec_pitch(SPL * N), 0} : KSpan{N / 2 + 1, spec_pitch(N), 0})
+                         : ks_;
   vec2_t<T>* __restrict__ out = FIXED ? spec : out_;
   using V = vec2_t<T>;
-  using C = TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, QUAD>()>;
+  using C = TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, (SPL > 0)>()>;
   constexpr int E = C::E, P = C::P, L = C::L, TILE = C::TILE;
   constexpr uint32_t TILE_BYTES = TILE * sizeof(V);
   constexpr int NBUF = C::NBUF;
   const int KT = (ks.kc + L - 1) / L;
   const size_t kq = size_t(ks.kq);
   const int NL = (PASS < 2 ? g.ni : g.nj) * KT;  // tiles per chunk (QUAD) / in all
-  const int NT = NL * (QUAD ? 4 : 1);
+  const int NT = NL * (QUAD ? SPL * SPL : 1);
   constexpr bool TWS = PASS == 2 ? bool(ARENA_TMA_TWSMEM_X) : bool(ARENA_TMA_TWSMEM_Y);
   V* bufs = smem_base<V>();
   V* tws = bufs + NBUF * TILE;
@@ -719,12 +722,12 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
       line_fft_tail<N, E, L, +1>(v, cur, twp, t, l);
     } else {
       line_fft<N, E, L, -1>(v, cur, twp, t, l);
-      const T kj = QUAD ? T(signed_freq(2 * outer + (qd & 1), 2 * N)) : T(signed_freq(j0 + outer, N));
+      const T kj = QUAD ? T(signed_freq(SPL * outer + qd % imax(SPL, 1), SPL * N)) : T(signed_freq(j0 + outer, N));
       const T kk = T(ks.k0 + k);
       const T c = kj * kj + kk * kk;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const T ki = QUAD ? T(signed_freq(2 * (t + P * e) + (qd >> 1), 2 * N)) : T(signed_freq(t + P * e, N));
+        const T ki = QUAD ? T(signed_freq(SPL * (t + P * e) + qd / imax(SPL, 1), SPL * N)) : T(signed_freq(t + P * e, N));
         const T k2 = ki * ki + c;
         const T m = poisson_symbol(k2, scale, four_pi2);
         v[e].x *= m;

@@ -3,6 +3,7 @@
 
 namespace arena_fft {
 cudaError_t launch_pow2_f32(const Pow2Args& a) { return launch_pow2<float>(a); }
+cudaError_t launch_split3_f32(const Split3Args& a) { return launch_split3<float>(a); }
 bool pow2_config_f32(int n, KernelGeom* g) { return pow2_config<float>(n, g); }
 bool pow2_fused_ok_f32(int n) {
   switch (n) {

@@ -3,6 +3,7 @@
 
 namespace arena_fft {
 cudaError_t launch_pow2_f64(const Pow2Args& a) { return launch_pow2<double>(a); }
+cudaError_t launch_split3_f64(const Split3Args& a) { return launch_split3<double>(a); }
 bool pow2_config_f64(int n, KernelGeom* g) { return pow2_config<double>(n, g); }
 bool pow2_fused_ok_f64(int n) {
   switch (n) {

@@ -10,6 +10,7 @@
 #include "launchers.h"
 #include "poisson_fused.cuh"
 #include "poisson_quad.cuh"
+#include "poisson_split3.cuh"
 #include "poisson_ystream.cuh"
 
 namespace arena_fft {
@@ -95,25 +96,25 @@ inline const vec2_t<T>* stw_ptr(const Pow2Args& a, int which, int E) {
   return static_cast<const vec2_t<T>*>(a.stw) + stw_offset(a.n, which, E);
 }
 
-template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false, bool QUAD = false>
+template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false, int SPL = 0>
 cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* spec, const Layout& g, T scale,
                                T four_pi2, KSpan ks = KSpan{N / 2 + 1, spec_pitch(N), 0}, void* out = nullptr,
                                const Layout* gout = nullptr, const PeerOut<vec2_t<T>>* po = nullptr) {
-  using C = TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, QUAD>()>;
+  using C = TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, (SPL > 0)>()>;
   using V = vec2_t<T>;
-  auto kern = k_strided_tma<T, N, PASS, PEER, FIXED, QUAD>;
+  auto kern = k_strided_tma<T, N, PASS, PEER, FIXED, SPL>;
   constexpr int SMEM = PASS == 2 ? C::SMEM_X : C::SMEM_Y;
-  cudaError_t e = ensure_smem<k_strided_tma<T, N, PASS, PEER, FIXED, QUAD>>(SMEM, C::THREADS);
+  cudaError_t e = ensure_smem<k_strided_tma<T, N, PASS, PEER, FIXED, SPL>>(SMEM, C::THREADS);
   if (e) return e;
   PeerOut<V> pov{};
   if (po) pov = *po;
   int per_sm = 1;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, SMEM))) return e;
-  const int tiles = (PASS < 2 ? g.ni : g.nj) * ((ks.kc + C::L - 1) / C::L) * (QUAD ? 4 : 1);
+  const int tiles = (PASS < 2 ? g.ni : g.nj) * ((ks.kc + C::L - 1) / C::L) * (SPL ? SPL * SPL : 1);
   int grid = a.sm_count * (per_sm > 0 ? per_sm : 1);
   if (grid > tiles) grid = tiles;
   // stage twiddles of N-point lines: table `which` 1 (N = n), 0 (N = n/2, quadrant lines)
-  kern<<<grid, C::THREADS, SMEM, a.stream>>>(map, static_cast<V*>(spec), stw_ptr<T>(a, QUAD ? 0 : 1, C::E), scale, four_pi2, g,
+  kern<<<grid, C::THREADS, SMEM, a.stream>>>(map, static_cast<V*>(spec), stw_ptr<T>(a, SPL ? 0 : 1, C::E), scale, four_pi2, g,
                                                a.nchunks, a.j0, ks, static_cast<V*>(out ? out : spec),
                                                gout ? *gout : g, pov);
   return cudaGetLastError();
@@ -220,22 +221,93 @@ cudaError_t launch_quad(const Pow2Args& a) {
       k_zfwd_quad<T, NR><<<qgrid, QC::THREADS, QC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw,
                                                                      stw_ptr<T>(a, 0, QC::E), gq);
       mark(a, mk++);
-      if ((e = launch_strided_tma<T, H, 0, false, false, true>(a, *my, a.spec, gq, scale, four_pi2, ks))) return e;
+      if ((e = launch_strided_tma<T, H, 0, false, false, 2>(a, *my, a.spec, gq, scale, four_pi2, ks))) return e;
     }
     if (a.phases & kPhaseX) {
       mark(a, mk++);
       // compile-time quadrant geometry for the x pass, as the single-GPU x pass (FIXED)
-      if ((e = launch_strided_tma<T, H, 2, false, true, true>(a, *mx, a.spec, gq, scale, four_pi2, ks))) return e;
+      if ((e = launch_strided_tma<T, H, 2, false, true, 2>(a, *mx, a.spec, gq, scale, four_pi2, ks))) return e;
     }
     if (a.phases & kPhaseYZ) {
       mark(a, mk++);
-      if ((e = launch_strided_tma<T, H, 1, false, false, true>(a, *my, a.spec, gq, scale, four_pi2, ks))) return e;
+      if ((e = launch_strided_tma<T, H, 1, false, false, 2>(a, *my, a.spec, gq, scale, four_pi2, ks))) return e;
       mark(a, mk++);
       k_zinv_quad<T, NR><<<qgrid, QC::THREADS, QC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw,
                                                                      stw_ptr<T>(a, 0, QC::E), gq);
       mark(a, mk++);
     }
     return cudaGetLastError();
+  }
+}
+
+// Radix-3 split path (poisson_split3.cuh): generic z r2c, split, M-point y / x / y
+// TMA passes on the nine chunks, merge, generic z c2r.
+template <typename T, int M>
+cudaError_t launch_split3_m(const Split3Args& s) {
+  using V = vec2_t<T>;
+  cudaError_t e;
+  const int n = s.n;
+  if (n != 3 * M || !s.tma) return cudaErrorInvalidValue;
+  const Layout gq = make_layout(M, M);
+  const KSpan ks{s.nc, s.ncp, 0};
+  TmaCache* c = s.tma;
+  if (c->specB != s.Q || c->n != n || c->nchunks != 9) {
+    if ((e = encode_map<T, M>(c->maps[0], s.Q, gq, 9, true, ks.kc, ks.kq, TmaCfg<T, M, true>::L, true))) return e;
+    if ((e = encode_map<T, M>(c->maps[1], s.Q, gq, 9, false, ks.kc, ks.kq, TmaCfg<T, M, true>::L, false,
+                              TmaCfg<T, M, false, x_wide<T, true>()>::L)))
+      return e;
+    c->specB = c->specC = s.Q;
+    c->n = n;
+    c->ni = c->nj = M;
+    c->nchunks = 9;
+    c->quad = 3;
+  }
+  const CUtensorMap* my = reinterpret_cast<const CUtensorMap*>(c->maps[0]);
+  const CUtensorMap* mx = reinterpret_cast<const CUtensorMap*>(c->maps[1]);
+  const T scale = T(1.0 / (double(n) * n * n));  // fft_solver.cpp:67
+  const T four_pi2 = T(4.0 * M_PI * M_PI);       // fft_solver.cpp:66
+  // the strided kernels read the M-point stage tables through a (n' = 2M) plan's offsets
+  Pow2Args a{};
+  a.stw = s.stw;
+  a.n = 2 * M;
+  a.stream = s.stream;
+  a.sm_count = s.sm_count;
+  a.nchunks = 1;
+  const GenArgs ga{s.gplan, s.tw, n, s.nc, s.ncp, s.stream, nullptr};
+  auto mk = [&](int i) {
+    if (s.ev) cudaEventRecord(s.ev[i], s.stream);
+  };
+  const unsigned grid = unsigned(M) * M;
+  mk(0);
+  if ((e = sizeof(T) == 8 ? gen_z_r2c_f64(ga, s.f, s.S) : gen_z_r2c_f32(ga, s.f, s.S))) return e;
+  mk(1);
+  k_split3_fwd<T><<<grid, 128, 0, s.stream>>>(static_cast<const V*>(s.S), static_cast<V*>(s.Q),
+                                               static_cast<const V*>(s.tw), n, M, s.nc, s.ncp, gq);
+  mk(2);
+  if ((e = launch_strided_tma<T, M, 0, false, false, 3>(a, *my, s.Q, gq, scale, four_pi2, ks))) return e;
+  mk(3);
+  if ((e = launch_strided_tma<T, M, 2, false, false, 3>(a, *mx, s.Q, gq, scale, four_pi2, ks))) return e;
+  mk(4);
+  if ((e = launch_strided_tma<T, M, 1, false, false, 3>(a, *my, s.Q, gq, scale, four_pi2, ks))) return e;
+  mk(5);
+  k_split3_inv<T><<<grid, 128, 0, s.stream>>>(static_cast<const V*>(s.Q), static_cast<V*>(s.S),
+                                               static_cast<const V*>(s.tw), n, M, s.nc, s.ncp, gq);
+  mk(6);
+  if ((e = sizeof(T) == 8 ? gen_z_c2r_f64(ga, s.S, s.u) : gen_z_c2r_f32(ga, s.S, s.u))) return e;
+  mk(7);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_split3(const Split3Args& s) {
+  switch (s.M) {
+    case 16: return launch_split3_m<T, 16>(s);
+    case 32: return launch_split3_m<T, 32>(s);
+    case 64: return launch_split3_m<T, 64>(s);
+    case 128: return launch_split3_m<T, 128>(s);
+    case 256: return launch_split3_m<T, 256>(s);
+    case 512: return launch_split3_m<T, 512>(s);
+    default: return cudaErrorInvalidValue;
   }
 }
 

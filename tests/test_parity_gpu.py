@@ -753,3 +753,27 @@ def test_dft3_round_trip_generic(cuda, n):
     assert np.abs(spec - np.fft.fftn(g)).max() <= 1e-12 * np.abs(spec).max()
     back = arena.dft3_inverse(spec, n)
     assert np.abs(back - g).max() <= 1e-12
+
+
+@pytest.mark.parametrize("n", [48, 96, 192])
+@pytest.mark.parametrize("precision", [64, 32])
+def test_split3_path_vs_oracle(cuda, n, precision, monkeypatch):
+    """Radix-3 split path (poisson_split3.cuh) for n = 3 * 2^k against the oracle, and
+    against the plain generic stages of the same plan type (ARENA_FFT_SPLIT3=0)."""
+    torch = cuda
+    dt = torch.float64 if precision == 64 else torch.float32
+    f = torch.from_numpy(np.random.default_rng(n + 17).uniform(-1, 1, (n, n, n))).to(dtype=dt, device="cuda")
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ARENA_FFT_SPLIT3", mode)
+        u = torch.empty_like(f)
+        p = arena.Plan(n, precision)
+        p.set_stage_timing(True)
+        p.solve_device(f, u)
+        torch.cuda.synchronize()
+        times, _ = p.stage_times()
+        assert len(times) == (7 if mode == "1" else 5), times
+        out[mode] = u.double().cpu().numpy()
+    ref = oracle.poisson_solve(f.double().cpu().numpy())
+    tol = TOL64 if precision == 64 else TOL32
+    assert _rel(out["1"], ref) <= tol and _rel(out["0"], ref) <= tol

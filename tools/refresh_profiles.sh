@@ -14,6 +14,8 @@ python bench.py --n 256 --config 2 --no-cpu > $O/bench_256_fp64_config2.json 2>&
 python bench.py --n 64 --config 1 --no-cpu > $O/bench_64_fp64_config1.json 2>&1; echo "bench 64 rc=$?"
 python bench.py --n 2048 --config 5 --steps 5 --no-cpu > $O/bench_2048_fp64_config5.json 2>&1; echo "bench 2048 rc=$?"
 python bench.py --n 2048 --config 5 --precision 32 --steps 5 --no-cpu > $O/bench_2048_fp32_config5.json 2>&1; echo "bench 2048 fp32 rc=$?"
+python bench.py --n 768 --config 4 --steps 10 --no-cpu --no-e2e > $O/bench_768_fp64_split3.json 2>&1; echo "bench 768 rc=$?"
+python bench.py --n 384 --config 4 --steps 20 --no-cpu --no-e2e > $O/bench_384_fp64_split3.json 2>&1; echo "bench 384 rc=$?"
 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference_arm.json 2>&1; echo "reference rc=$?"
 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > $O/bench_small.json 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_bench_1024_fp64.csv \

@@ -324,9 +324,14 @@ __global__ void k_gen_lines(const void* in, void* out, GenPlan pl, GenGeom g,
 // rows) within ~100 KB so two CTAs share an SM, else fewer; contiguous passes:
 // rows are contiguous anyway, so at most 2 lines within ~48 KB (four CTAs per
 // SM hide the load latency).  B200, 768^3: 83 ms with 8 lines everywhere.
+#ifndef ARENA_GEN_ZCAP
+#define ARENA_GEN_ZCAP (96 * 1024)  // shared-memory budget of a contiguous-axis CTA (B200 1000^3:
+#endif                              // z passes 10.6 -> 8.5 ms with 96 KB instead of 48 KB)
 inline int gen_lines_per_cta(int n, int vb, bool strided) {
-  int L = strided ? 8 : 2;
-  const size_t cap = strided ? 100 * 1024 : 48 * 1024;
+  // contiguous axis: 4 lines (row pairs) up to n = 512, else 2 (B200: 384^3 z 0.56 -> 0.46 ms
+  // with 4; 768^3 z 3.7 -> 4.5 ms with 4)
+  int L = strided ? 8 : (n <= 512 ? 4 : 2);
+  const size_t cap = strided ? 100 * 1024 : ARENA_GEN_ZCAP;
   while (L > 1 && size_t(2) * n * L * vb > cap) L /= 2;
   return L;
 }

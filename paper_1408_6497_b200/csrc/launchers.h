@@ -149,7 +149,8 @@ cudaError_t gen_z_r2c_f32(const GenArgs& a, const void* f, void* spec);
 cudaError_t gen_z_c2r_f64(const GenArgs& a, const void* spec, void* u);
 cudaError_t gen_z_c2r_f32(const GenArgs& a, const void* spec, void* u);
 
-// Radix-3 split path for n = 3M, M a power of two in [16, 512] (poisson_split3.cuh).
+// Radix-R split path (R = 3: n = 3M, M a power of two in [16, 512]; R = 5: n = 5M,
+// M in [16, 256]) onto the power-of-two passes (poisson_split3.cuh).
 constexpr int kSplit3Launches = 7;
 struct Split3Args {
   const void* f;
@@ -158,17 +159,21 @@ struct Split3Args {
   void* Q;          // nine chunks of Layout(M, M) rows of ncp
   const void* tw;   // W_n^m
   const void* stw;  // stage-twiddle tables of an n' = 2M plan (M-point lines: which = 0)
-  int n, M, nc, ncp;
+  int n, R, M, nc, ncp;
   cudaStream_t stream;
   cudaEvent_t* ev;  // nullable; kSplit3Launches + 1 events
   TmaCache* tma;
   int sm_count;
   const GenPlan* gplan;
 };
-inline bool split3_ok(int n) {
-  if (n % 3) return false;
-  const int M = n / 3;
-  return M >= 16 && M <= 512 && (M & (M - 1)) == 0;
+// The split radix for n (3 or 5), or 0 when n is not R * 2^k in range.
+inline int split_radix(int n) {
+  for (int R : {3, 5}) {
+    if (n % R) continue;
+    const int M = n / R;
+    if (M >= 16 && M <= (R == 3 ? 512 : 256) && (M & (M - 1)) == 0) return R;
+  }
+  return 0;
 }
 cudaError_t launch_split3_f64(const Split3Args& a);
 cudaError_t launch_split3_f32(const Split3Args& a);

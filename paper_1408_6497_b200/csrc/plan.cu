@@ -150,7 +150,7 @@ arena_status make_twiddles(arena_fft_plan* p) {
   e = cudaMemcpy(p->tw, host.data(), host.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "twiddle upload");
   if (p->path == ARENA_PATH_POW2 || p->split3) {
-    const int nt = p->split3 ? 2 * (n / 3) : n;  // split3: M-point lines = the n/2 tables of n' = 2M
+    const int nt = p->split3 ? 2 * (n / split_radix(n)) : n;  // split: M-point lines = the n/2 tables of n' = 2M
     const size_t ns = stw_entries(nt);
     std::vector<unsigned char> st(std::max<size_t>(ns, 1) * vb);
     stw_fill_host(nt, p->prec, st.data());
@@ -252,7 +252,8 @@ arena_status enqueue_kernels(arena_fft_plan* p, const void* d_f, void* d_u, cuda
     a.quad = p->quad;
     e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
   } else if (p->split3) {
-    Split3Args a{d_f, d_u, p->spec, p->Q, p->tw, p->stw, p->n, p->n / 3, p->nc, p->ncp, s, ev, p->tma, p->sm_count,
+    const int R = split_radix(p->n);
+    Split3Args a{d_f, d_u, p->spec, p->Q, p->tw, p->stw, p->n, R, p->n / R, p->nc, p->ncp, s, ev, p->tma, p->sm_count,
                  &p->gplan};
     e = p->prec == 64 ? launch_split3_f64(a) : launch_split3_f32(a);
   } else {
@@ -407,7 +408,7 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
     {
       const char* sz = std::getenv("ARENA_FFT_SPLIT3");
       const char* kern = std::getenv("ARENA_FFT_KERNELS");
-      if (split3_ok(n) && !(sz && std::string(sz) == "0") && !(kern && std::string(kern) == "classic")) {
+      if (split_radix(n) && !(sz && std::string(sz) == "0") && !(kern && std::string(kern) == "classic")) {
         p->split3 = true;
         p->tma = new (std::nothrow) TmaCache;
         if (!p->tma) {

@@ -1,6 +1,7 @@
-// poisson_split3.cuh — the radix-3 split of the i and j transforms for
-// n = 3M (M a power of two): the mixed-radix sizes 48 ... 1536 run their y / x
-// passes on the power-of-two TMA kernels.
+// poisson_split3.cuh — the radix-R split (R = 3 or 5) of the i and j
+// transforms for n = RM (M a power of two): the mixed-radix sizes 48 ... 1536
+// (R = 3) and 80 ... 1280 (R = 5) run their y / x passes on the power-of-two
+// TMA kernels.  Written below for R = 3; R = 5 is the same with 25 chunks.
 //
 // As the quadrant formulation (poisson_quad.cuh) with radix 3: after the rows'
 // r2c (the generic path's z pass, two rows per complex line), for the nine rows
@@ -36,77 +37,112 @@ __device__ __forceinline__ void dft3(V& x0, V& x1, V& x2) {
   x2 = csub(m, r);
 }
 
-// 3x3 DFT y[ci][cj] = sum_{a,b} W_3^{S(a ci + b cj)} x[a][b] in place.
-template <int S, typename V>
-__device__ __forceinline__ void dft3x3(V (&x)[3][3]) {
+// cos / sin(2 pi m / 5)
+__host__ __device__ constexpr double cos5(int m) {
+  return m == 0 ? 1.0 : (m == 1 || m == 4) ? 0.30901699437494745 : -0.8090169943749475;
+}
+__host__ __device__ constexpr double sin5(int m) {
+  return m == 0 ? 0.0 : m == 1 ? 0.9510565162951535 : m == 2 ? 0.5877852522924731 : m == 3 ? -0.5877852522924731
+                                                                                         : -0.9510565162951535;
+}
+
+// R-point DFT (R = 3 or 5) of x[0], x[s], ..., x[(R-1) s], sign S, in place.
+template <int R, int S, typename V>
+__device__ __forceinline__ void dftR(V* x, int s) {
+  using T = decltype(x->x);
+  if constexpr (R == 3) {
+    dft3<S>(x[0], x[s], x[2 * s]);
+  } else {
+    V in[R], out[R];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) dft3<S>(x[a][0], x[a][1], x[a][2]);  // over b -> cj
+    for (int r = 0; r < R; ++r) in[r] = x[r * s];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) dft3<S>(x[0][c], x[1][c], x[2][c]);  // over a -> ci
+    for (int q = 0; q < R; ++q) {
+      T re = in[0].x, im = in[0].y;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const T c = T(cos5((r * q) % R)), sn = T(S * sin5((r * q) % R));  // exp(S 2 pi i rq / 5) = c + i sn
+        re = fma(in[r].x, c, fma(-in[r].y, sn, re));
+        im = fma(in[r].y, c, fma(in[r].x, sn, im));
+      }
+      out[q] = V{re, im};
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r * s] = out[r];
+  }
+}
+
+// RxR DFT y[ci][cj] = sum_{a,b} W_R^{S(a ci + b cj)} x[a][b] in place.
+template <int R, int S, typename V>
+__device__ __forceinline__ void dftRxR(V (&x)[R][R]) {
+#pragma unroll
+  for (int a = 0; a < R; ++a) dftR<R, S>(&x[a][0], 1);  // over b -> cj
+#pragma unroll
+  for (int c = 0; c < R; ++c) dftR<R, S>(&x[0][c], R);  // over a -> ci
 }
 
 // Forward split: S (generic layout) -> Q (nine chunks).  One CTA per (i', j'),
 // threads over k (coalesced rows).
-template <typename T>
+template <typename T, int R>
 __global__ void __launch_bounds__(128) k_split3_fwd(const vec2_t<T>* __restrict__ S, vec2_t<T>* __restrict__ Q,
                                                   const vec2_t<T>* __restrict__ tw, int n, int M, int nc, int ncp,
                                                   Layout gq) {
   using V = vec2_t<T>;
   const int ip = blockIdx.x / M, jp = blockIdx.x % M;
-  const V* src[3][3];
-  V* dst[3][3];
-  V w[3][3];
+  const V* src[R][R];
+  V* dst[R][R];
+  V w[R][R];
 #pragma unroll
-  for (int a = 0; a < 3; ++a)
+  for (int a = 0; a < R; ++a)
 #pragma unroll
-    for (int b = 0; b < 3; ++b) {
+    for (int b = 0; b < R; ++b) {
       src[a][b] = S + (size_t(ip + a * M) * n + (jp + b * M)) * ncp;
-      dst[a][b] = Q + lrow(gq, 3 * a + b, ip, jp) * ncp;
+      dst[a][b] = Q + lrow(gq, R * a + b, ip, jp) * ncp;
       w[a][b] = tw_load(tw, (a * ip + b * jp) % n);  // W_n^{ci i' + cj j'}, (ci, cj) = (a, b)
     }
   for (int k = threadIdx.x; k < nc; k += blockDim.x) {
-    V x[3][3];
+    V x[R][R];
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+    for (int a = 0; a < R; ++a)
 #pragma unroll
-      for (int b = 0; b < 3; ++b) x[a][b] = __ldcs(src[a][b] + k);
-    dft3x3<-1>(x);
+      for (int b = 0; b < R; ++b) x[a][b] = __ldcs(src[a][b] + k);
+    dftRxR<R, -1>(x);
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+    for (int a = 0; a < R; ++a)
 #pragma unroll
-      for (int b = 0; b < 3; ++b) st_out(dst[a][b] + k, cmul(x[a][b], w[a][b]));
+      for (int b = 0; b < R; ++b) st_out(dst[a][b] + k, cmul(x[a][b], w[a][b]));
   }
 }
 
 // Inverse merge: Q -> S, x_{a,b} = sum_{ci,cj} W_3^{-(a ci + b cj)} W_n^{-(ci i' + cj j')} Y'_{ci,cj}.
-template <typename T>
+template <typename T, int R>
 __global__ void __launch_bounds__(128) k_split3_inv(const vec2_t<T>* __restrict__ Q, vec2_t<T>* __restrict__ S,
                                                   const vec2_t<T>* __restrict__ tw, int n, int M, int nc, int ncp,
                                                   Layout gq) {
   using V = vec2_t<T>;
   const int ip = blockIdx.x / M, jp = blockIdx.x % M;
-  const V* src[3][3];
-  V* dst[3][3];
-  V w[3][3];
+  const V* src[R][R];
+  V* dst[R][R];
+  V w[R][R];
 #pragma unroll
-  for (int a = 0; a < 3; ++a)
+  for (int a = 0; a < R; ++a)
 #pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      src[a][b] = Q + lrow(gq, 3 * a + b, ip, jp) * ncp;
+    for (int b = 0; b < R; ++b) {
+      src[a][b] = Q + lrow(gq, R * a + b, ip, jp) * ncp;
       dst[a][b] = S + (size_t(ip + a * M) * n + (jp + b * M)) * ncp;
       w[a][b] = tw_load(tw, (a * ip + b * jp) % n);
     }
   for (int k = threadIdx.x; k < nc; k += blockDim.x) {
-    V x[3][3];
+    V x[R][R];
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+    for (int a = 0; a < R; ++a)
 #pragma unroll
-      for (int b = 0; b < 3; ++b) x[a][b] = cmulc(__ldcs(src[a][b] + k), w[a][b]);
-    dft3x3<+1>(x);
+      for (int b = 0; b < R; ++b) x[a][b] = cmulc(__ldcs(src[a][b] + k), w[a][b]);
+    dftRxR<R, +1>(x);
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+    for (int a = 0; a < R; ++a)
 #pragma unroll
-      for (int b = 0; b < 3; ++b) st_out(dst[a][b] + k, x[a][b]);
+      for (int b = 0; b < R; ++b) st_out(dst[a][b] + k, x[a][b]);
   }
 }
 

@@ -242,25 +242,26 @@ cudaError_t launch_quad(const Pow2Args& a) {
 
 // Radix-3 split path (poisson_split3.cuh): generic z r2c, split, M-point y / x / y
 // TMA passes on the nine chunks, merge, generic z c2r.
-template <typename T, int M>
+template <typename T, int R, int M>
 cudaError_t launch_split3_m(const Split3Args& s) {
   using V = vec2_t<T>;
+  constexpr int CH = R * R;  // chunks
   cudaError_t e;
   const int n = s.n;
-  if (n != 3 * M || !s.tma) return cudaErrorInvalidValue;
+  if (n != R * M || !s.tma) return cudaErrorInvalidValue;
   const Layout gq = make_layout(M, M);
   const KSpan ks{s.nc, s.ncp, 0};
   TmaCache* c = s.tma;
-  if (c->specB != s.Q || c->n != n || c->nchunks != 9) {
-    if ((e = encode_map<T, M>(c->maps[0], s.Q, gq, 9, true, ks.kc, ks.kq, TmaCfg<T, M, true>::L, true))) return e;
-    if ((e = encode_map<T, M>(c->maps[1], s.Q, gq, 9, false, ks.kc, ks.kq, TmaCfg<T, M, true>::L, false,
+  if (c->specB != s.Q || c->n != n || c->nchunks != CH) {
+    if ((e = encode_map<T, M>(c->maps[0], s.Q, gq, CH, true, ks.kc, ks.kq, TmaCfg<T, M, true>::L, true))) return e;
+    if ((e = encode_map<T, M>(c->maps[1], s.Q, gq, CH, false, ks.kc, ks.kq, TmaCfg<T, M, true>::L, false,
                               TmaCfg<T, M, false, x_wide<T, true>()>::L)))
       return e;
     c->specB = c->specC = s.Q;
     c->n = n;
     c->ni = c->nj = M;
-    c->nchunks = 9;
-    c->quad = 3;
+    c->nchunks = CH;
+    c->quad = R;
   }
   const CUtensorMap* my = reinterpret_cast<const CUtensorMap*>(c->maps[0]);
   const CUtensorMap* mx = reinterpret_cast<const CUtensorMap*>(c->maps[1]);
@@ -281,16 +282,16 @@ cudaError_t launch_split3_m(const Split3Args& s) {
   mk(0);
   if ((e = sizeof(T) == 8 ? gen_z_r2c_f64(ga, s.f, s.S) : gen_z_r2c_f32(ga, s.f, s.S))) return e;
   mk(1);
-  k_split3_fwd<T><<<grid, 128, 0, s.stream>>>(static_cast<const V*>(s.S), static_cast<V*>(s.Q),
+  k_split3_fwd<T, R><<<grid, 128, 0, s.stream>>>(static_cast<const V*>(s.S), static_cast<V*>(s.Q),
                                                static_cast<const V*>(s.tw), n, M, s.nc, s.ncp, gq);
   mk(2);
-  if ((e = launch_strided_tma<T, M, 0, false, false, 3>(a, *my, s.Q, gq, scale, four_pi2, ks))) return e;
+  if ((e = launch_strided_tma<T, M, 0, false, false, R>(a, *my, s.Q, gq, scale, four_pi2, ks))) return e;
   mk(3);
-  if ((e = launch_strided_tma<T, M, 2, false, false, 3>(a, *mx, s.Q, gq, scale, four_pi2, ks))) return e;
+  if ((e = launch_strided_tma<T, M, 2, false, false, R>(a, *mx, s.Q, gq, scale, four_pi2, ks))) return e;
   mk(4);
-  if ((e = launch_strided_tma<T, M, 1, false, false, 3>(a, *my, s.Q, gq, scale, four_pi2, ks))) return e;
+  if ((e = launch_strided_tma<T, M, 1, false, false, R>(a, *my, s.Q, gq, scale, four_pi2, ks))) return e;
   mk(5);
-  k_split3_inv<T><<<grid, 128, 0, s.stream>>>(static_cast<const V*>(s.Q), static_cast<V*>(s.S),
+  k_split3_inv<T, R><<<grid, 128, 0, s.stream>>>(static_cast<const V*>(s.Q), static_cast<V*>(s.S),
                                                static_cast<const V*>(s.tw), n, M, s.nc, s.ncp, gq);
   mk(6);
   if ((e = sizeof(T) == 8 ? gen_z_c2r_f64(ga, s.S, s.u) : gen_z_c2r_f32(ga, s.S, s.u))) return e;
@@ -300,15 +301,28 @@ cudaError_t launch_split3_m(const Split3Args& s) {
 
 template <typename T>
 cudaError_t launch_split3(const Split3Args& s) {
-  switch (s.M) {
-    case 16: return launch_split3_m<T, 16>(s);
-    case 32: return launch_split3_m<T, 32>(s);
-    case 64: return launch_split3_m<T, 64>(s);
-    case 128: return launch_split3_m<T, 128>(s);
-    case 256: return launch_split3_m<T, 256>(s);
-    case 512: return launch_split3_m<T, 512>(s);
-    default: return cudaErrorInvalidValue;
+  if (s.R == 3) {
+    switch (s.M) {
+      case 16: return launch_split3_m<T, 3, 16>(s);
+      case 32: return launch_split3_m<T, 3, 32>(s);
+      case 64: return launch_split3_m<T, 3, 64>(s);
+      case 128: return launch_split3_m<T, 3, 128>(s);
+      case 256: return launch_split3_m<T, 3, 256>(s);
+      case 512: return launch_split3_m<T, 3, 512>(s);
+      default: return cudaErrorInvalidValue;
+    }
   }
+  if (s.R == 5) {
+    switch (s.M) {
+      case 16: return launch_split3_m<T, 5, 16>(s);
+      case 32: return launch_split3_m<T, 5, 32>(s);
+      case 64: return launch_split3_m<T, 5, 64>(s);
+      case 128: return launch_split3_m<T, 5, 128>(s);
+      case 256: return launch_split3_m<T, 5, 256>(s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <typename T, int NR>

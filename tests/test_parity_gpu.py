@@ -729,7 +729,7 @@ def test_random_generic_fp32_vs_oracle(cuda, n):
     assert _rel(u.double().cpu().numpy(), oracle.poisson_solve(f.double().cpu().numpy())) <= TOL32
 
 
-@pytest.mark.parametrize("n", [384, 768])
+@pytest.mark.parametrize("n", [384, 768, 640, 1000])
 def test_generic_large_analytic(cuda, n):
     """Generic path at 3 * 2^k sizes (radix-8/4/3 plans, the fused x-symbol pass)
     against the analytic solution of config 4's source (64 modes, |k| <= 32)."""
@@ -755,10 +755,10 @@ def test_dft3_round_trip_generic(cuda, n):
     assert np.abs(back - g).max() <= 1e-12
 
 
-@pytest.mark.parametrize("n", [48, 96, 192])
+@pytest.mark.parametrize("n", [48, 96, 192, 80, 160, 320])
 @pytest.mark.parametrize("precision", [64, 32])
 def test_split3_path_vs_oracle(cuda, n, precision, monkeypatch):
-    """Radix-3 split path (poisson_split3.cuh) for n = 3 * 2^k against the oracle, and
+    """Radix-3 / radix-5 split path (poisson_split3.cuh) for n = 3 * 2^k, 5 * 2^k against the oracle, and
     against the plain generic stages of the same plan type (ARENA_FFT_SPLIT3=0)."""
     torch = cuda
     dt = torch.float64 if precision == 64 else torch.float32

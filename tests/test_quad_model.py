@@ -76,21 +76,21 @@ def test_quadrant_solve_matches_oracle(n):
     assert np.linalg.norm(u - ref) <= 1e-12 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("M", [2, 4, 8])
-def test_radix3_split_reproduces_spectrum(M):
+@pytest.mark.parametrize("R,M", [(3, 2), (3, 4), (3, 8), (5, 2), (5, 4)])
+def test_radix3_split_reproduces_spectrum(R, M):
     """The radix-3 split of poisson_split3.cuh: Y_{ci,cj} = W_n^{ci i' + cj j'}
     sum_{a,b} W_3^{a ci + b cj} X[i' + aM, j' + bM]; its M x M DFT is the spectrum
     at (3 i'' + ci, 3 j'' + cj)."""
-    n = 3 * M
-    f = np.random.default_rng(M).uniform(-1, 1, (n, n, n))
-    X = np.fft.rfft(f, axis=2).reshape(3, M, 3, M, -1).transpose(0, 2, 1, 3, 4)  # [a, b, i', j', k]
-    W3 = np.exp(-2j * np.pi / 3)
+    n = R * M
+    f = np.random.default_rng(M + R).uniform(-1, 1, (n, n, n))
+    X = np.fft.rfft(f, axis=2).reshape(R, M, R, M, -1).transpose(0, 2, 1, 3, 4)  # [a, b, i', j', k]
+    WR = np.exp(-2j * np.pi / R)
     full = np.fft.rfftn(f)
     ip = np.arange(M)[:, None]
     jp = np.arange(M)[None, :]
-    for ci in range(3):
-        for cj in range(3):
-            Y = sum(W3 ** (a * ci + b * cj) * X[a, b] for a in range(3) for b in range(3))
+    for ci in range(R):
+        for cj in range(R):
+            Y = sum(WR ** (a * ci + b * cj) * X[a, b] for a in range(R) for b in range(R))
             Y = Y * np.exp(-2j * np.pi * (ci * ip + cj * jp) / n)[..., None]
             sub = np.fft.fft2(Y, axes=(0, 1))
-            assert np.allclose(sub, full[ci::3, cj::3], rtol=0, atol=1e-10 * np.abs(full).max())
+            assert np.allclose(sub, full[ci::R, cj::R], rtol=0, atol=1e-10 * np.abs(full).max())

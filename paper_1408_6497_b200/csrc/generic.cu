@@ -8,7 +8,9 @@
 // symbol * backward in one kernel (G_XPOISSON), the z passes transform two real
 // rows per complex line (G_R2C_PAIR / G_C2R_PAIR).  B200, fp64: 384^3 in 3.9 ms,
 // 768^3 in 28 ms, 1000^3 in 61 ms (seven sweeps, table twiddles, one row per
-// line: 6.8 / 83 / 156 ms; the power-of-two path: 1024^3 in 16.4 ms).
+// line: 6.8 / 83 / 156 ms; the power-of-two path: 1024^3 in 16.4 ms).  Sizes
+// n = 3 * 2^k and 5 * 2^k only use the z passes here: their y / x passes run on
+// the power-of-two kernels through the radix-3 / radix-5 split (poisson_split3.cuh).
 //
 // Same conventions as fft_solver.cpp: r2c along the last axis keeping
 // k in [0, n/2], c2r treating its input as Hermitian (imaginary parts of the

@@ -138,7 +138,7 @@ def algorithmic_bytes(n: int, elem: int):
            "gen_z_r2c": R + C, "gen_y_fwd": 2 * C, "gen_xmid_fwd_scale_inv": 2 * C,
            "gen_y_inv": 2 * C, "gen_z_c2r": C + R,
            # radix-3 split path (n = 3M): two extra spectrum sweeps (split, merge)
-           "split3_fwd": 2 * C, "split3_inv": 2 * C}
+           "split3_fwd": 2 * C, "split3_inv": 2 * C, "zsplit_r2c": R + C, "zsplit_c2r": C + R}
     return per, 2 * R + 8 * C
 
 

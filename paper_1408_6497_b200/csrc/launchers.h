@@ -159,6 +159,7 @@ struct Split3Args {
   void* Q;          // nine chunks of Layout(M, M) rows of ncp
   const void* tw;   // W_n^m
   const void* stw;  // stage-twiddle tables of an n' = 2M plan (M-point lines: which = 0)
+  const void* stwz; // stage-twiddle tables of an n' = M plan (M/2-point lines: the split z passes)
   int n, R, M, nc, ncp;
   cudaStream_t stream;
   cudaEvent_t* ev;  // nullable; kSplit3Launches + 1 events

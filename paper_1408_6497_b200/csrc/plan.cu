@@ -53,8 +53,8 @@ const char* kStageNames[4][kPow2Launches] = {
     {"zy_fused_fwd", "xmid_fwd_scale_inv", "yinv", "zinv_c2r", nullptr},
     {"zfwd_r2c", "yfwd", "xmid_fwd_scale_inv", "yz_fused_inv", nullptr},
     {"zy_fused_fwd", "xmid_fwd_scale_inv", "yz_fused_inv", nullptr, nullptr}};
-const char* kSplit3Names[kSplit3Launches] = {"gen_z_r2c", "split3_fwd", "yfwd", "xmid_fwd_scale_inv", "yinv",
-                                             "split3_inv", "gen_z_c2r"};
+const char* kSplit3Names[kSplit3Launches] = {"zsplit_r2c", "split3_fwd", "yfwd", "xmid_fwd_scale_inv", "yinv",
+                                             "split3_inv", "zsplit_c2r"};
 const char* kGenNames[kGenLaunches] = {"gen_z_r2c", "gen_y_fwd", "gen_xmid_fwd_scale_inv", "gen_y_inv",
                                        "gen_z_c2r"};
 
@@ -97,6 +97,7 @@ struct arena_fft_plan {
   int quad = 0;             // quadrant formulation (poisson_quad.cuh)
   bool split3 = false;      // generic n = 3M: radix-3 split onto the power-of-two passes (poisson_split3.cuh)
   void* Q = nullptr;        // split3: nine-chunk workspace
+  void* stwz = nullptr;     // split3: stage tables of the M/2-point z sub-FFTs (nullptr: generic z passes)
   int sm_count = 148;
   // host-boundary resources (lazily allocated)
   void* d_in = nullptr;   // dft3 host paths: n^3 complex
@@ -158,6 +159,15 @@ arena_status make_twiddles(arena_fft_plan* p) {
     if ((e = cudaMemcpy(p->stw, st.data(), st.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
       return cuda_fail(e, "stage twiddle upload");
   }
+  const char* zk = std::getenv("ARENA_FFT_SPLITZ");  // "0": the generic z passes on the split path
+  if (p->split3 && !(zk && std::string(zk) == "0")) {
+    const int nz = n / split_radix(n);  // tables of an n'' = M plan: M/2-point lines (which = 0)
+    std::vector<unsigned char> st(std::max<size_t>(stw_entries(nz), 1) * vb);
+    stw_fill_host(nz, p->prec, st.data());
+    if ((e = cudaMalloc(&p->stwz, st.size())) != cudaSuccess) return fail(ARENA_ENOMEM, "z stage twiddle tables");
+    if ((e = cudaMemcpy(p->stwz, st.data(), st.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cuda_fail(e, "z stage twiddle upload");
+  }
   return ARENA_OK;
 }
 
@@ -166,6 +176,7 @@ void free_plan(arena_fft_plan* p) {
   DeviceGuard g(p->device);
   if (p->spec) cudaFree(p->spec);
   if (p->Q) cudaFree(p->Q);
+  if (p->stwz) cudaFree(p->stwz);
   if (p->tw) cudaFree(p->tw);
   if (p->stw) cudaFree(p->stw);
   if (p->ctrs) cudaFree(p->ctrs);
@@ -253,8 +264,8 @@ arena_status enqueue_kernels(arena_fft_plan* p, const void* d_f, void* d_u, cuda
     e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
   } else if (p->split3) {
     const int R = split_radix(p->n);
-    Split3Args a{d_f, d_u, p->spec, p->Q, p->tw, p->stw, p->n, R, p->n / R, p->nc, p->ncp, s, ev, p->tma, p->sm_count,
-                 &p->gplan};
+    Split3Args a{d_f, d_u, p->spec, p->Q, p->tw, p->stw, p->stwz, p->n, R, p->n / R, p->nc, p->ncp, s, ev, p->tma,
+                 p->sm_count, &p->gplan};
     e = p->prec == 64 ? launch_split3_f64(a) : launch_split3_f32(a);
   } else {
     GenArgs a{&p->gplan, p->tw, p->n, p->nc, p->ncp, s, ev};

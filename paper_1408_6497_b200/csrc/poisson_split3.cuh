@@ -146,4 +146,141 @@ __global__ void __launch_bounds__(128) k_split3_inv(const vec2_t<T>* __restrict_
   }
 }
 
+// ------------------------------------------------ z passes for n = R * M rows
+// A row of n reals is packed into NZ = n/2 = R * MH complex points (MH = M/2, a
+// power of two).  Its NZ-point FFT is a radix-R step in registers (decimation in
+// frequency: y_d[m] = W_NZ^{d m} sum_c W_R^{c d} z[m + MH c]) followed by R
+// MH-point FFTs on the line engine, Z[R q + d] = FFT(y_d)[q]; the spectrum is
+// staged in shared memory in natural order for the r2c split (as zfwd_rows).
+// The inverse mirrors it.  Replaces the generic stages' z passes of the split
+// path.
+template <typename T, int R, int MH>
+struct SplitZCfg {
+  static constexpr int NZ = R * MH;
+  static constexpr int E = imin(R == 3 ? 8 : 4, MH);  // points per thread per sub-FFT (R * E live values)
+  static constexpr int P = MH / E;
+  static constexpr int L = imax(1, 64 / P);  // rows per CTA: 64+ threads
+  static constexpr int THREADS = L * P;
+  static constexpr int SMEM = (NZ * L + L) * 2 * int(sizeof(T));
+};
+
+template <typename T, int R, int MH>
+__global__ void __launch_bounds__(SplitZCfg<T, R, MH>::THREADS) k_zfwd_split(const T* __restrict__ f,
+                                                                            vec2_t<T>* __restrict__ S,
+                                                                            const vec2_t<T>* __restrict__ tw,
+                                                                            const vec2_t<T>* __restrict__ stw,
+                                                                            int ncp, long long nrows) {
+  using V = vec2_t<T>;
+  using C = SplitZCfg<T, R, MH>;
+  constexpr int NZ = C::NZ, E = C::E, P = C::P, L = C::L, n = 2 * NZ;
+  V* sm = smem_base<V>();
+  const int l = threadIdx.x % L, t = threadIdx.x / L;
+  const long long row = (long long)blockIdx.x * L + l;
+  const bool ok = row < nrows;
+  const V* src = reinterpret_cast<const V*>(f + (ok ? row : 0) * n);
+  V v[R][E];
+#pragma unroll
+  for (int c = 0; c < R; ++c)
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[c][e] = ok ? __ldcs(src + t + P * e + MH * c) : V{T(0), T(0)};
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    V x[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) x[c] = v[c][e];
+    dftR<R, -1>(x, 1);
+    const int m = t + P * e;
+#pragma unroll
+    for (int d = 0; d < R; ++d) v[d][e] = d ? cmul(x[d], tw_load(tw, (2 * d * m) % n)) : x[0];  // W_NZ^{d m}
+  }
+#pragma unroll
+  for (int d = 0; d < R; ++d) line_fft<MH, E, L, -1, kSyncCta>(v[d], sm, stw, t, l);
+#pragma unroll
+  for (int d = 0; d < R; ++d)
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[(R * (t + P * e) + d) * L + l] = v[d][e];  // Z[R q + d]
+  __syncthreads();
+  if (!ok) return;
+  V* dst = S + row * ncp;
+#pragma unroll
+  for (int e = 0; e < R * E; ++e) {
+    const int k = t + P * e;
+    const V A = sm[k * L + l];
+    const V Bc = sm[((NZ - k) % NZ) * L + l];
+    const V B{Bc.x, -Bc.y};
+    const V W = tw_load(tw, k);  // W_n^k
+    const V WD = cmul(W, csub(A, B));
+    st_out(dst + k, V{T(0.5) * (A.x + B.x + WD.y), T(0.5) * (A.y + B.y - WD.x)});
+    if (k == 0) st_out(dst + NZ, V{A.x - A.y, T(0)});
+  }
+}
+
+template <typename T, int R, int MH>
+__global__ void __launch_bounds__(SplitZCfg<T, R, MH>::THREADS) k_zinv_split(const vec2_t<T>* __restrict__ S,
+                                                                            T* __restrict__ u,
+                                                                            const vec2_t<T>* __restrict__ tw,
+                                                                            const vec2_t<T>* __restrict__ stw,
+                                                                            int ncp, long long nrows) {
+  using V = vec2_t<T>;
+  using C = SplitZCfg<T, R, MH>;
+  constexpr int NZ = C::NZ, E = C::E, P = C::P, L = C::L, n = 2 * NZ;
+  V* sm = smem_base<V>();
+  V* xm = sm + NZ * L;
+  const int l = threadIdx.x % L, t = threadIdx.x / L;
+  const long long row = (long long)blockIdx.x * L + l;
+  const bool ok = row < nrows;
+  const V* src = S + (ok ? row : 0) * ncp;
+  V z[R * E];
+#pragma unroll
+  for (int e = 0; e < R * E; ++e) {
+    z[e] = ok ? __ldcs(src + t + P * e) : V{T(0), T(0)};
+    sm[(t + P * e) * L + l] = z[e];
+  }
+  if (t == 0) xm[l] = ok ? __ldcs(src + NZ) : V{T(0), T(0)};
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < R * E; ++e) {  // Hermitian merge into the packed spectrum (as zinv_rows)
+    const int k = t + P * e;
+    V A = z[e];
+    V Bs = (k == 0) ? xm[l] : sm[(NZ - k) * L + l];
+    if (k == 0) {
+      A.y = T(0);
+      Bs.y = T(0);
+    }
+    const V B{Bs.x, -Bs.y};
+    const V W = tw_load(tw, k);
+    const V Ep = cadd(A, B);
+    const V Op = cmulc(csub(A, B), W);
+    z[e] = V{Ep.x - Op.y, Ep.y + Op.x};
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < R * E; ++e) sm[(t + P * e) * L + l] = z[e];
+  __syncthreads();
+  V v[R][E];
+#pragma unroll
+  for (int d = 0; d < R; ++d)
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[d][e] = sm[(R * (t + P * e) + d) * L + l];  // Z[R q + d]
+  __syncthreads();
+#pragma unroll
+  for (int d = 0; d < R; ++d) line_fft<MH, E, L, +1, kSyncCta>(v[d], sm, stw, t, l);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int m = t + P * e;
+    V x[R];
+#pragma unroll
+    for (int d = 0; d < R; ++d) x[d] = d ? cmulc(v[d][e], tw_load(tw, (2 * d * m) % n)) : v[0][e];
+    dftR<R, +1>(x, 1);
+#pragma unroll
+    for (int c = 0; c < R; ++c) v[c][e] = x[c];
+  }
+  if (!ok) return;
+  V* dst = reinterpret_cast<V*>(u + row * n);
+#pragma unroll
+  for (int c = 0; c < R; ++c)
+#pragma unroll
+    for (int e = 0; e < E; ++e) st_out(dst + t + P * e + MH * c, v[c][e]);
+}
+
 }  // namespace arena_fft

@@ -279,8 +279,20 @@ cudaError_t launch_split3_m(const Split3Args& s) {
     if (s.ev) cudaEventRecord(s.ev[i], s.stream);
   };
   const unsigned grid = unsigned(M) * M;
+  constexpr int MH = M / 2;
+  using ZC = SplitZCfg<T, R, MH>;
+  const long long nrows = (long long)n * n;
+  const unsigned zgrid = unsigned((nrows + ZC::L - 1) / ZC::L);
+  const V* stwz = static_cast<const V*>(s.stwz) + stw_offset(M, 0, ZC::E);
+  if ((e = ensure_smem<k_zfwd_split<T, R, MH>>(ZC::SMEM, ZC::THREADS))) return e;
+  if ((e = ensure_smem<k_zinv_split<T, R, MH>>(ZC::SMEM, ZC::THREADS))) return e;
   mk(0);
-  if ((e = sizeof(T) == 8 ? gen_z_r2c_f64(ga, s.f, s.S) : gen_z_r2c_f32(ga, s.f, s.S))) return e;
+  if (s.stwz) {
+    k_zfwd_split<T, R, MH><<<zgrid, ZC::THREADS, ZC::SMEM, s.stream>>>(static_cast<const T*>(s.f), static_cast<V*>(s.S),
+                                                                       static_cast<const V*>(s.tw), stwz, s.ncp, nrows);
+  } else if ((e = sizeof(T) == 8 ? gen_z_r2c_f64(ga, s.f, s.S) : gen_z_r2c_f32(ga, s.f, s.S))) {
+    return e;
+  }
   mk(1);
   k_split3_fwd<T, R><<<grid, 128, 0, s.stream>>>(static_cast<const V*>(s.S), static_cast<V*>(s.Q),
                                                static_cast<const V*>(s.tw), n, M, s.nc, s.ncp, gq);
@@ -294,7 +306,12 @@ cudaError_t launch_split3_m(const Split3Args& s) {
   k_split3_inv<T, R><<<grid, 128, 0, s.stream>>>(static_cast<const V*>(s.Q), static_cast<V*>(s.S),
                                                static_cast<const V*>(s.tw), n, M, s.nc, s.ncp, gq);
   mk(6);
-  if ((e = sizeof(T) == 8 ? gen_z_c2r_f64(ga, s.S, s.u) : gen_z_c2r_f32(ga, s.S, s.u))) return e;
+  if (s.stwz) {
+    k_zinv_split<T, R, MH><<<zgrid, ZC::THREADS, ZC::SMEM, s.stream>>>(static_cast<const V*>(s.S), static_cast<T*>(s.u),
+                                                                       static_cast<const V*>(s.tw), stwz, s.ncp, nrows);
+  } else if ((e = sizeof(T) == 8 ? gen_z_c2r_f64(ga, s.S, s.u) : gen_z_c2r_f32(ga, s.S, s.u))) {
+    return e;
+  }
   mk(7);
   return cudaGetLastError();
 }

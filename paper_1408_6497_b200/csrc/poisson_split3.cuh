@@ -154,12 +154,22 @@ __global__ void __launch_bounds__(128) k_split3_inv(const vec2_t<T>* __restrict_
 // staged in shared memory in natural order for the r2c split (as zfwd_rows).
 // The inverse mirrors it.  Replaces the generic stages' z passes of the split
 // path.
+#ifndef ARENA_SPLITZ_E3
+#define ARENA_SPLITZ_E3 8  // points per thread per sub-FFT, R = 3 (R * E values live)
+#endif
+#ifndef ARENA_SPLITZ_E5
+#define ARENA_SPLITZ_E5 4
+#endif
+#ifndef ARENA_SPLITZ_THREADS
+#define ARENA_SPLITZ_THREADS 32  // threads per CTA (at least: one row's P threads).  B200, 768^3: z passes
+                                 // 1.85 / 2.16 ms at 64 threads, 1.52 / 1.82 at 32 (one warp: cheap barriers)
+#endif
 template <typename T, int R, int MH>
 struct SplitZCfg {
   static constexpr int NZ = R * MH;
-  static constexpr int E = imin(R == 3 ? 8 : 4, MH);  // points per thread per sub-FFT (R * E live values)
+  static constexpr int E = imin(R == 3 ? ARENA_SPLITZ_E3 : ARENA_SPLITZ_E5, MH);
   static constexpr int P = MH / E;
-  static constexpr int L = imax(1, 64 / P);  // rows per CTA: 64+ threads
+  static constexpr int L = imax(1, ARENA_SPLITZ_THREADS / P);  // rows per CTA
   static constexpr int THREADS = L * P;
   static constexpr int SMEM = (NZ * L + L) * 2 * int(sizeof(T));
 };

@@ -52,6 +52,25 @@ __device__ __forceinline__ void dftR(V* x, int s) {
   using T = decltype(x->x);
   if constexpr (R == 3) {
     dft3<S>(x[0], x[s], x[2 * s]);
+  } else if constexpr (R == 5) {
+    // X1,4 = a1 -/+ S' i b1, X2,3 = a2 -/+ S' i b2 with t1 = x1 + x4, t2 = x2 + x3,
+    // t3 = x1 - x4, t4 = x2 - x3, a1 = x0 + c1 t1 + c2 t2, a2 = x0 + c2 t1 + c1 t2,
+    // b1 = s1 t3 + s2 t4, b2 = s2 t3 - s1 t4 (c_k, s_k = cos, sin(2 pi k / 5))
+    constexpr T c1 = T(cos5(1)), c2 = T(cos5(2)), s1 = T(sin5(1)), s2 = T(sin5(2));
+    const V x0 = x[0];
+    const V t1 = cadd(x[s], x[4 * s]), t2 = cadd(x[2 * s], x[3 * s]);
+    const V t3 = csub(x[s], x[4 * s]), t4 = csub(x[2 * s], x[3 * s]);
+    const V a1{fma(c2, t2.x, fma(c1, t1.x, x0.x)), fma(c2, t2.y, fma(c1, t1.y, x0.y))};
+    const V a2{fma(c1, t2.x, fma(c2, t1.x, x0.x)), fma(c1, t2.y, fma(c2, t1.y, x0.y))};
+    const V b1{fma(s2, t4.x, s1 * t3.x), fma(s2, t4.y, s1 * t3.y)};
+    const V b2{fma(-s1, t4.x, s2 * t3.x), fma(-s1, t4.y, s2 * t3.y)};
+    // i b = (-b.y, b.x); forward (S = -1): X1 = a1 - i b1
+    const V ib1{-b1.y, b1.x}, ib2{-b2.y, b2.x};
+    x[0] = cadd(x0, cadd(t1, t2));
+    x[s] = S < 0 ? csub(a1, ib1) : cadd(a1, ib1);
+    x[4 * s] = S < 0 ? cadd(a1, ib1) : csub(a1, ib1);
+    x[2 * s] = S < 0 ? csub(a2, ib2) : cadd(a2, ib2);
+    x[3 * s] = S < 0 ? cadd(a2, ib2) : csub(a2, ib2);
   } else {
     V in[R], out[R];
 #pragma unroll

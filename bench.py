@@ -9,9 +9,15 @@ BASELINE config-4 source (1024^3 fp64, 64 random Fourier modes, seed 4),
 inputs resident in HBM.  The field (8.6 GB) is far larger than L2 (126 MB),
 so no L2 flush is needed between steps.  Prints ONE JSON line on rank 0.
 
---impl reference times the reference's own CPU solver (fft_solver.cpp:51-87
-over the FFTW3-API shim, oracle/_ref; the C restatement oracle/lib when that
-was not built) on the host cores, on a bounded 512^3 sample of the same source.
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+(one rank per GPU, 127.0.0.1) and runs the slab decomposition (strong scaling).
+
+--impl reference times the reference's own CPU solver (fft_solver.cpp:51-87,
+compiled unmodified over the FFTW3-API shim: oracle/_ref) on all host cores,
+each step one full solve of the SAME n^3 config source (same_config), plus one
+1-core solve (the reference's FFTW is single-threaded) and a scipy pocketfft
+all-core restatement ("B-all").  That arm never loads this
+repo's CUDA library (checked against /proc/self/maps).
 """
 from __future__ import annotations
 
@@ -45,7 +51,10 @@ def _args():
     ap.add_argument("--inplace", action="store_true",
                     help="solve in place (u aliases f): f + workspace only, so 2048^3 fp64 fits one GPU "
                          "(default for n >= 2048); parity then from one solve of a fresh f, checked in plane blocks")
-    ap.add_argument("--cpu-n", type=int, default=512, help="grid of the bounded CPU sample")
+    ap.add_argument("--cpu-runs", type=int, default=3, help="CPU baseline: median of this many full solves")
+    ap.add_argument("--no-one-core", action="store_true", help="reference arm: skip the 1-core solve")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check without a GPU: gloo ranks, no solve, one JSON line")
     ap.add_argument("--slab", action="store_true", help="use the slab (NCCL) path even with one rank")
     ap.add_argument("--decomp", default="slab", choices=("slab", "pencil"), help="multi-GPU decomposition")
     ap.add_argument("--pgrid", default=None, help="pencil process grid RxC (default: near-square, R <= C)")
@@ -142,85 +151,136 @@ def algorithmic_bytes(n: int, elem: int):
     return per, 2 * R + 8 * C
 
 
-def cpu_sample(n: int, config: int, kind=None, min_seconds: float = 10.0, max_runs: int = 3):
-    """Time the oracle on a bounded sample: solve the config source at n^3 until
-    min_seconds elapsed or max_runs done; returns (unknowns/s, kind, threads, runs)."""
-    import numpy as np
+def _workload(config: int, n: int, prec: int) -> str:
+    """config.workload text; fp32 runs solve the fp64 source rounded to fp32."""
+    from paper_1408_6497_b200 import problems
 
+    txt = problems.CONFIG_TEXT[config]
+    base_n = {1: 64, 2: 256, 3: 512, 4: 1024, 5: 2048}[config]
+    if n != base_n:
+        txt = txt.replace(f"N={base_n}^3", f"N={n}^3")
+    if prec == 32:
+        txt = txt.replace("fp64", "fp32 (f rounded from the fp64 source)")
+    return f"C{config}: {txt}"
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _median(xs):
+    xs = sorted(xs)
+    m = len(xs) // 2
+    return xs[m] if len(xs) % 2 else 0.5 * (xs[m - 1] + xs[m])
+
+
+def _repo_libs_mapped():
+    """This repo's shared objects mapped into the process (the reference arm must map
+    none of paper_1408_6497_b200/lib; oracle/ libraries are the reference's own code)."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for ln in fh:
+                path = ln.split()[-1] if len(ln.split()) >= 6 else ""
+                if path.startswith(REPO) and ".so" in path:
+                    out.add(os.path.relpath(path, REPO))
+    except OSError:
+        pass
+    return sorted(out)
+
+
+def cpu_reference_solves(f, runs: int, threads: int):
+    """Time `runs` full solves of the host field f by the reference's own solver
+    (fft_solver.cpp:51-87 over the FFTW3-API shim; the C restatement where the
+    reference was not built).  Returns (per-run seconds, kind, the last u)."""
     import oracle
-    from paper_1408_6497_b200 import problems
 
-    kind = kind or oracle.best_kind()
-    threads = len(os.sched_getaffinity(0))
+    kind = oracle.best_kind()
     oracle.set_threads(threads, kind)
-    src = problems.config(config, n)
-    f = _host_source(src)
-    oracle.poisson_solve(f[:8, :8, :8].copy(), kind)  # warm the library
-    runs, t0 = 0, time.perf_counter()
-    while True:
-        oracle.poisson_solve(f, kind)
-        runs += 1
-        el = time.perf_counter() - t0
-        if el >= min_seconds or runs >= max_runs:
-            break
-    return n ** 3 * runs / el, kind, threads, runs
-
-
-def _host_source(src):
-    """Config source on the host without the GPU: separable per-mode evaluation."""
-    import numpy as np
-
-    from paper_1408_6497_b200 import problems
-
-    n = src.n
-    if isinstance(src, problems.ModeSource):
-        # Re sum a e^{2 pi i k.x} = inverse DFT of a sparse Hermitian spectrum (scipy pocketfft).
-        import scipy.fft as sf
-
-        F = np.zeros((n, n, n), dtype=np.complex128)
-        for (kx, ky, kz), c in zip(src.k, src.f_coef()):
-            F[kx % n, ky % n, kz % n] += 0.5 * c
-            F[-kx % n, -ky % n, -kz % n] += 0.5 * np.conj(c)
-        out = sf.ifftn(F, workers=len(os.sched_getaffinity(0)), overwrite_x=True).real * float(n) ** 3
-        del F
-        return np.ascontiguousarray(out)
-    return problems.eval_host(src, "f")
+    ts, u = [], None
+    for _ in range(runs):
+        u = None
+        t0 = time.perf_counter()
+        u = oracle.poisson_solve(f, kind)
+        ts.append(time.perf_counter() - t0)
+    return ts, kind, u
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU solver on the host cores, rank 0 only."""
+    """--impl reference: the reference's CPU solver on the host cores, rank 0 only,
+    each step one full solve of the same n^3 source the GPU arm solves."""
     if rank != 0:
         return
     import numpy as np
 
     import oracle
-    from paper_1408_6497_b200 import problems
+    from paper_1408_6497_b200 import problems  # pure Python: the package maps no CUDA library on import
 
-    kind = oracle.best_kind()
+    n = args.n
     threads = len(os.sched_getaffinity(0))
-    oracle.set_threads(threads, kind)
-    n = args.cpu_n
     src = problems.config(args.config, n)
-    f = _host_source(src)
+    t0 = time.perf_counter()
+    f = problems.host_field(src, "f")
+    f -= f.mean()
+    t_src = time.perf_counter() - t0
+    kind = oracle.best_kind()
+    oracle.set_threads(threads, kind)
     for _ in range(args.warmup):
         oracle.poisson_solve(f, kind)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle.poisson_solve(f, kind)
-    el = time.perf_counter() - t0
+    ts, kind, u = cpu_reference_solves(f, args.steps, threads)
+    el = sum(ts)
     v = n ** 3 * args.steps / el
-    sample = (f"{n}^3 sample of config {args.config}'s source (same 64 modes), full solve per step; "
-              f"engine: {'reference fft_solver.cpp over FFTW3-API shim (oracle/_ref)' if kind == 'ref' else 'C restatement (oracle/lib)'}")
+    engine = ("reference fft_solver.cpp (unmodified) over the FFTW3-API shim, oracle/_ref" if kind == "ref"
+              else "C restatement of fft_solver.cpp, oracle/lib")
+    parity = {}
+    if isinstance(src, problems.ModeSource):  # band-limited: the analytic u is exact on the grid
+        ua = problems.host_field(src, "u")
+        ua -= ua.mean()
+        parity["rel_l2_vs_analytic"] = float(np.linalg.norm(u - ua) / np.linalg.norm(ua))
+        del ua
+    extras = {}
+    # the reference's FFTW is single-threaded (no fftw_init_threads, proj/src/CMakeLists.txt:3,17)
+    if not args.no_one_core:
+        t1, _, _ = cpu_reference_solves(f, 1, 1)
+        extras["one_core"] = {"value": n ** 3 / t1[0], "unit": UNIT, "cores": 1, "s_per_solve": t1[0],
+                              "kind": "reference" if kind == "ref" else "port",
+                              "note": "reference-faithful: FFTW single-threaded, one full solve"}
+    # B-all: the strongest CPU engine here (scipy pocketfft, all cores), median of 3
+    tb, ub = [], None
+    for _ in range(3):
+        t0 = time.perf_counter()
+        ub = oracle.pocketfft_poisson(f, threads)
+        tb.append(time.perf_counter() - t0)
+    extras["b_all"] = {"value": n ** 3 / _median(tb), "unit": UNIT, "cores": threads, "s_per_solve": _median(tb),
+                       "runs": len(tb), "kind": "port",
+                       "engine": "scipy.fft pocketfft restatement of fft_solver.cpp:51-87 (oracle.pocketfft_poisson)",
+                       "rel_l2_vs_reference": float(np.linalg.norm(ub - u) / np.linalg.norm(u))}
+    del ub
+    mapped = _repo_libs_mapped()
+    sample = (f"full {n}^3 solves of config {args.config}'s source (the GPU arm's workload), one per step; "
+              f"engine: {engine}; {threads} OpenMP threads on the FFT lines (the reference's own copies, "
+              f"zero-fills and scale loop run single-threaded as written)")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C{args.config}: {problems.CONFIG_TEXT[args.config]}", "n": args.n,
-                   "sample_n": n},
+        "config": {"workload": _workload(args.config, n, 64), "n": n, "sample_n": n, "same_config": True,
+                   "source_seconds": t_src},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference" if kind == "ref" else "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": _cpu_model(), "s_per_solve_median": _median(ts), **extras},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "parity": parity,
+        "repo_libs_mapped": mapped,
     }
+    if any(m.startswith("paper_1408_6497_b200") for m in mapped):
+        line["invalid"] = "the reference arm mapped this repo's CUDA library"
     print(json.dumps(line), flush=True)
 
 
@@ -340,6 +400,32 @@ def run_ours(args, rank, world, local):
         rel_an, linf_an = cmp["rel_l2"], cmp["linf_rel"]
         del ua
 
+    # ---- CPU baseline (rank 0, N=1 only) on the IDENTICAL fp64 buffer the GPU solved, before any
+    # pinned allocation: the reference's own solver, median of --cpu-runs full solves; its output
+    # is also the oracle the timed GPU output is compared with (north_star: rel L2 <= 1e-12 fp64,
+    # <= 1e-5 fp32 against the fp64 oracle).
+    cpu, rel_or = None, None
+    if rank == 0 and world == 1 and not args.no_cpu and not inplace:
+        try:
+            fh = f64.cpu().numpy()
+            threads = len(os.sched_getaffinity(0))
+            ts, kind, uo = cpu_reference_solves(fh, max(1, args.cpu_runs), threads)
+            del fh
+            uo_d = torch.from_numpy(uo).to("cuda")
+            del uo
+            ud = u.double() if prec != 64 else u
+            rel_or = ((ud - uo_d).norm() / uo_d.norm()).item()
+            del uo_d, ud
+            cpu = {"value": n ** 3 / _median(ts), "unit": UNIT, "cores": threads,
+                   "kind": "reference" if kind == "ref" else "port",
+                   "sample": f"the same {n}^3 fp64 field the GPU solved, {len(ts)} full solve(s), median; "
+                             + ("reference fft_solver.cpp (unmodified) over the FFTW3-API shim (oracle/_ref)"
+                                if kind == "ref" else "C restatement (oracle/lib)")
+                             + f", {threads} OpenMP threads on the FFT lines",
+                   "s_per_solve": ts, "cpu_model": _cpu_model()}
+        except Exception as exc:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": None, "sample": f"failed: {exc}"}
+
     # ---- roofline of the dominant kernel
     peak, peak_kind = _peaks()
     per_kernel, b_solve = algorithmic_bytes(n, elem)
@@ -387,25 +473,13 @@ def run_ours(args, rank, world, local):
         e2e["matches_device_path"] = bool(torch.allclose(hu[0], u.cpu()))
         del hf, hu
 
-    # ---- CPU baseline (rank 0, N=1 only), bounded sample
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        try:
-            v, kind, threads, runs = cpu_sample(args.cpu_n, args.config)
-            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference" if kind == "ref" else "port",
-                   "sample": f"{args.cpu_n}^3 solve(s) of config {args.config}'s source ({runs} run(s)), "
-                             f"{'reference fft_solver.cpp over FFTW3-API shim' if kind == 'ref' else 'C restatement'}"
-                             f", OpenMP over lines"}
-        except Exception as exc:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": None, "sample": f"failed: {exc}"}
-
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
             "dtype": "f64" if prec == 64 else "f32", "data": "synthetic",
-            "config": {"workload": f"C{args.config}: {problems.CONFIG_TEXT[args.config]}", "n": n,
+            "config": {"workload": _workload(args.config, n, prec), "n": n,
                        "precision": prec, "decomposition": "single-GPU" if world == 1 else f"{world} replicas",
                        "l2": f"inputs larger than L2 ({n ** 3 * elem / 1e9:.1f} GB field), no flush",
                        "in_place": inplace,
@@ -418,7 +492,8 @@ def run_ours(args, rank, world, local):
             "e2e": e2e,
             "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
-            "parity": {"rel_l2_vs_analytic": rel_an, "linf_rel_vs_analytic": linf_an},
+            "parity": {"rel_l2_vs_analytic": rel_an, "linf_rel_vs_analytic": linf_an, "rel_l2_vs_oracle": rel_or,
+                       "tolerance_vs_oracle": 1e-12 if prec == 64 else 1e-5},
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -563,6 +638,22 @@ def run_slab(args, rank, world, local):
         slab.barrier_status()
     rel_an = rel_vs_analytic()
 
+    # ---- per-stage times (a second, separately timed run with events between the stages;
+    # the headline region above has no extra events), max over ranks per stage
+    stages = None
+    if not pencil:
+        slab.set_stage_timing(True)
+        kst = max(1, min(args.steps, 5))
+        dist.barrier()
+        for _ in range(kst):
+            slab.solve_device(f, u, sh)
+        torch.cuda.synchronize()
+        st_ms, nst = slab.stage_times()
+        slab.set_stage_timing(False)
+        tt = torch.tensor([st_ms[k] / nst for k in arena.Slab.STAGES], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        stages = {k: tt[i].item() for i, k in enumerate(arena.Slab.STAGES)}
+
     peak, peak_kind = _peaks()
     _, b_solve = algorithmic_bytes(n, elem)
     C = n * n * (n // 2 + 1) * 2 * elem
@@ -572,7 +663,21 @@ def run_slab(args, rank, world, local):
     else:
         nvl_per_gpu = 2 * (C / world) * (world - 1) / world
     nvl_peak = 770.0  # GB/s per direction, measured peer copy (B200_PROFILING.md)
+    nvl_spec = 900.0  # NVLink 5, 18 links, per direction
     t_roof = max(hbm_per_gpu / (peak * 1e9), nvl_per_gpu / (nvl_peak * 1e9))
+    nvlink = {"bytes_per_gpu_per_solve": nvl_per_gpu, "peak_gbs_measured_copy": nvl_peak, "spec_gbs": nvl_spec,
+              "achieved_gbs_whole_solve": nvl_per_gpu / (ms_step / 1e3) / 1e9}
+    if stages is not None:
+        # exchange #1 leaves in K2 (peer stores) or in the NCCL send/recv after it; #2 in K3 / after it
+        sent = slab.chunk_bytes * (world - 1)
+        ph1 = stages["xchg1"] + (stages["k1k2"] if xchg == "peer" else 0.0)
+        ph2 = stages["xchg2"] + (stages["k3"] if xchg == "peer" else 0.0)
+        nvlink.update({"bytes_sent_per_exchange": sent, "stage_ms": stages,
+                       "exchange_gbs": [sent / (ph1 / 1e3) / 1e9 if ph1 > 0 else None,
+                                        sent / (ph2 / 1e3) / 1e9 if ph2 > 0 else None],
+                       "exchange_gbs_note": ("peer: bytes over the time of the pass that stores them (K2 / K3) "
+                                             "plus its barrier" if xchg == "peer" else
+                                             "nccl: bytes over the grouped send/recv stage")})
 
     e2e = None
     if not args.no_e2e:
@@ -600,7 +705,7 @@ def run_slab(args, rank, world, local):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if prec == 64 else "f32", "data": "synthetic",
-            "config": {"workload": f"C{args.config}: {problems.CONFIG_TEXT[args.config]}", "n": n, "precision": prec,
+            "config": {"workload": _workload(args.config, n, prec), "n": n, "precision": prec,
                        "decomposition": ((f"pencil {pr}x{pc}, " + (
                                              "4 row/column all-to-alls fused into K1-K4 as stores into the peers' "
                                              "buffers (CUDA IPC over NVLink) + device flag barriers"
@@ -615,7 +720,9 @@ def run_slab(args, rank, world, local):
                          "unit": "GB/s", "frac": t_roof / (ms_step / 1e3), "traffic": None, "peak_kind": peak_kind,
                          "nvlink_bytes_per_gpu": nvl_per_gpu, "nvlink_peak_gbs": nvl_peak,
                          "t_roof_ms": t_roof * 1e3},
+            "nvlink": nvlink,
             "cpu_baseline": None,
+            "cpu_baseline_note": "measured on rank 0 at N=1 only (bench.py --gpus 1)",
             "e2e": e2e,
             "gpu_launches": slab.launches_per_solve * args.steps,
             "clocks": clk.summary(),
@@ -625,11 +732,57 @@ def run_slab(args, rank, world, local):
     dist.destroy_process_group()
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _relaunch(args) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: one rank per GPU under
+    torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    env = dict(os.environ)
+    if "NCCL_DEBUG" not in env:  # NCCL communicator creation stays checkable, off stdout
+        env["NCCL_DEBUG"] = "INFO"
+        env["NCCL_DEBUG_SUBSYS"] = "INIT"
+        env["NCCL_DEBUG_FILE"] = os.path.join("/tmp", "arena_bench_nccl.%h.%p.log")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def run_dry(args, rank, world):
+    """Launcher check (no GPU, gloo): every rank joins, the max over ranks of a per-rank
+    number is reduced as the real timing is, rank 0 prints one line."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "dry_run": True, "max_over_ranks": t.item(),
+                          "world_size": dist.get_world_size()}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = _args()
+    launched = "WORLD_SIZE" in os.environ
+    if not launched and args.gpus > 1 and args.impl == "ours":
+        sys.exit(_relaunch(args))
     rank, world, local = _dist()
-    if args.impl == "reference":
-        run_reference(args, rank, world)
+    if launched and args.gpus != world and args.impl == "ours":
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
+    if args.dry_run:
+        run_dry(args, rank, world)
+    elif args.impl == "reference":
+        run_reference(args, rank, world if launched else args.gpus)
     elif world > 1 or args.slab or args.pgrid:
         run_slab(args, rank, world, local)
     else:

@@ -61,7 +61,11 @@ arena_status arena_fft_plan_info(const arena_fft_plan* plan, int* n, int* precis
  * cudaStream_t (NULL = legacy default stream).  Asynchronous: returns after
  * enqueueing; errors from the launches are reported, kernel faults surface on
  * the caller's next synchronisation.  Semantics of fft_solver.cpp:51-87:
- * u = IFFT( FFT(f) * (k2 == 0 ? 0 : (1/n^3) / (4 pi^2 k2)) ), k2 = |signed k|^2. */
+ * u = IFFT( FFT(f) * (k2 == 0 ? 0 : (1/n^3) / (4 pi^2 k2)) ), k2 = |signed k|^2.
+ * Thread-safe; the plan's workspace is shared by all its solves, so a solve
+ * enqueued on one stream waits (cudaStreamWaitEvent) for the plan's previous
+ * solve on any stream — solves on one plan never overlap.  Use one plan per
+ * stream for concurrent solves. */
 arena_status arena_poisson_solve_device(arena_fft_plan* plan, const void* d_f, void* d_u, void* stream);
 
 /* The drop-in path: host buffers in and out (pageable or pinned), copies
@@ -152,6 +156,12 @@ arena_status arena_slab_peer_export(arena_fft_slab* slab, void* out, int len);
 arena_status arena_slab_peer_attach(arena_fft_slab* slab, const void* all_handles, int len);
 /* Switch the exchange of a loopback slab (or an attached NCCL slab). */
 arena_status arena_slab_set_exchange(arena_fft_slab* slab, int mode);
+/* Per-stage CUDA-event timing of arena_slab_solve_device on the solve's stream:
+ * ms5 = total ms over the timed solves of {K1+K2, exchange #1, K3, exchange #2,
+ * K4+K5} (PEER mode: the exchanges are inside K2 / K3 and the "exchange" stages
+ * are the device barriers, i.e. the wait for the slowest rank). */
+arena_status arena_slab_set_stage_timing(arena_fft_slab* slab, int enable);
+arena_status arena_slab_stage_times(arena_fft_slab* slab, double* ms5, int* n_solves);
 /* Phase p in {0, 1, 2} of a solve (K1+K2, K3, K4+K5, with the COPY exchanges
  * after phases 0 and 1).  In PEER mode the caller must synchronise all ranks
  * between phases (arena_slab_solve_device does it on the device). */
@@ -214,6 +224,10 @@ arena_status arena_interpolant_eval(int device, int nmodes, const int* k, const 
  * contiguous-axis (z) kernels, out15[5..9] the y kernels, out15[10..14] the x
  * kernel.  Host-only (no device needed); used by the CPU index-model tests. */
 int arena_pow2_kernel_geometry(int n, int precision_bits, int* out15);
+
+/* The calling thread's current CUDA device ordinal, or -1 when none is usable
+ * (lets a plan cache keyed by device resolve "current device" before keying). */
+int arena_current_device(void);
 
 /* Thread-local description of the last failure on this thread ("" if none). */
 const char* arena_last_error(void);

@@ -111,6 +111,38 @@ def dft3_inverse(spec: np.ndarray, n: int, kind: Optional[str] = None) -> np.nda
     return out
 
 
+def pocketfft_poisson(f: np.ndarray, workers: Optional[int] = None) -> np.ndarray:
+    """fft_solver.cpp:51-87 restated on scipy.fft (pocketfft, `workers` threads): the
+    strongest CPU engine in this image ("B-all" of BASELINE.md §3) — rfftn, the
+    symbol (k2 == 0 ? 0 : (1/n^3) / (4 pi^2 k2)) applied plane block by plane block
+    on a thread pool (numpy releases the GIL), irfftn."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import scipy.fft as sf
+
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    n = f.shape[0]
+    w = workers or len(os.sched_getaffinity(0))
+    F = sf.rfftn(f, workers=w)
+    sfreq = np.where(np.arange(n) <= n // 2, np.arange(n), np.arange(n) - n).astype(np.float64)  # fft_solver.hpp:19
+    kk2 = np.arange(n // 2 + 1, dtype=np.float64) ** 2
+    kj2 = sfreq ** 2
+    four_pi2 = 4.0 * np.pi * np.pi  # fft_solver.cpp:66
+    scale = 1.0 / (float(n) ** 3)
+
+    def block(i0, i1):
+        for i in range(i0, i1):
+            k2 = sfreq[i] ** 2 + kj2[:, None] + kk2[None, :]
+            with np.errstate(divide="ignore"):
+                s = np.where(k2 == 0.0, 0.0, scale / (four_pi2 * k2))  # fft_solver.cpp:76
+            F[i] *= s
+
+    step = max(1, n // (4 * w))
+    with ThreadPoolExecutor(w) as ex:
+        list(ex.map(lambda a: block(a, min(n, a + step)), range(0, n, step)))
+    return sf.irfftn(F, s=f.shape, workers=w, overwrite_x=True, norm="forward")  # unnormalised, as FFTW c2r
+
+
 def direct_dft3(g: np.ndarray) -> np.ndarray:
     """O(N^2) direct-summation DFT (the algorithm of oracle::direct_dft3,
     /root/reference/proj/tests/oracles.cpp:13-29), vectorised per output mode.

@@ -2,12 +2,15 @@
  * FFTW3-API shim over oracle/offt.c — TEST INFRASTRUCTURE ONLY.
  * Lets the reference's own fft_solver.cpp run unmodified as the CPU oracle /
  * CPU baseline (oracle/_ref/libref_poisson.so).  A plan just records its
- * arguments; fftw_execute runs the offt transform on the recorded buffers.
+ * arguments; fftw_execute runs the vfft.c transform (the FFTW stand-in engine,
+ * cross-checked against the independent oracle/offt.c in tests/test_oracle.py)
+ * on the recorded buffers.
  */
 #include <stdlib.h>
 
 #include "../offt.h"
 #include "fftw3.h"
+#include "vfft.h"
 
 enum { K_C2C, K_R2C, K_C2R };
 
@@ -44,9 +47,9 @@ fftw_plan fftw_plan_dft_c2r_3d(int n0, int n1, int n2, fftw_complex* in, double*
 void fftw_execute(const fftw_plan p) {
   if (!p) return;
   switch (p->kind) {
-    case K_C2C: offt_c2c_3d(p->n0, p->n1, p->n2, (const double*)p->in, (double*)p->out, p->sign); break;
-    case K_R2C: offt_r2c_3d(p->n0, p->n1, p->n2, (const double*)p->in, (double*)p->out); break;
-    case K_C2R: offt_c2r_3d(p->n0, p->n1, p->n2, (double*)p->in, (double*)p->out); break;
+    case K_C2C: vfft_c2c_3d(p->n0, p->n1, p->n2, (const double*)p->in, (double*)p->out, p->sign); break;
+    case K_R2C: vfft_r2c_3d(p->n0, p->n1, p->n2, (const double*)p->in, (double*)p->out); break;
+    case K_C2R: vfft_c2r_3d(p->n0, p->n1, p->n2, (double*)p->in, (double*)p->out); break;
   }
 }
 

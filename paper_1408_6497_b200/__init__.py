@@ -41,7 +41,6 @@ if not os.path.exists(LIB_PATH):
         "(or `make -C paper_1408_6497_b200`). There is no CPU fallback."
     )
 
-lib = ctypes.CDLL(LIB_PATH)
 
 _vp = ctypes.c_void_p
 _i = ctypes.c_int
@@ -85,6 +84,8 @@ _sig = {
     "arena_slab_set_exchange": (_i, [_vp, _i]),
     "arena_slab_solve_phase": (_i, [_vp, _i, _vp, _vp, _vp]),
     "arena_slab_barrier_status": (_i, [_vp]),
+    "arena_slab_set_stage_timing": (_i, [_vp, _i]),
+    "arena_slab_stage_times": (_i, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i)]),
     "arena_peer_barrier_selftest": (_i, [_i, _i, _i, ctypes.POINTER(_i)]),
     "arena_pencil_create_peer": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _i, _i, _i]),
     "arena_pencil_peer_handle_bytes": (_i, []),
@@ -108,11 +109,37 @@ _sig = {
     "arena_interpolant_eval": (_i, [_i, _i, _vp, _vp, _i, _vp, _vp]),
     "arena_last_error": (ctypes.c_char_p, []),
     "arena_fft_abi_version": (_i, []),
+    "arena_current_device": (_i, []),
 }
-for _name, (_res, _args) in _sig.items():
-    _fn = getattr(lib, _name)
-    _fn.restype = _res
-    _fn.argtypes = _args
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def _load_lib() -> ctypes.CDLL:
+    """Load libarena_fft.so on first use (not at import: importing the package —
+    e.g. problems.py for a CPU-only reference run — must not map the CUDA library)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is None:
+            h = ctypes.CDLL(LIB_PATH)
+            for _name, (_res, _args) in _sig.items():
+                _fn = getattr(h, _name)
+                _fn.restype = _res
+                _fn.argtypes = _args
+            _lib = h
+    return _lib
+
+
+class _LazyLib:
+    """Attribute access loads the library (``arena.lib.arena_...`` as before)."""
+
+    def __getattr__(self, name):
+        return getattr(_load_lib(), name)
+
+
+lib = _LazyLib()
 
 
 class ArenaError(RuntimeError):
@@ -142,6 +169,30 @@ def _ptr(x) -> int:
     if isinstance(x, np.ndarray):
         return x.ctypes.data
     return x.data_ptr()
+
+
+def _check_buffer(x, numel: int, itemsize: int, what: str, device: Optional[int] = None) -> None:
+    """Validate a buffer before its raw pointer crosses the C ABI: contiguous,
+    `numel` elements of `itemsize` bytes, and (device is not None) a CUDA tensor
+    on that device — or (device is None) host memory.  The kernels and copies
+    trust the sizes, so a short or mistyped buffer would be read past its end."""
+    if isinstance(x, np.ndarray):
+        if device is not None:
+            raise TypeError(f"{what}: expected a CUDA tensor on device {device}, got a numpy array")
+        ok_c, n_el, isz = x.flags.c_contiguous, x.size, x.itemsize
+    else:
+        is_cuda = bool(getattr(x, "is_cuda", False))
+        if device is not None and (not is_cuda or x.device.index != device):
+            raise TypeError(f"{what}: expected a CUDA tensor on device {device}, got {x.device}")
+        if device is None and is_cuda:
+            raise TypeError(f"{what}: expected host memory, got a CUDA tensor")
+        ok_c, n_el, isz = x.is_contiguous(), x.numel(), x.element_size()
+    if not ok_c:
+        raise ValueError(f"{what}: buffer must be contiguous")
+    if isz != itemsize:
+        raise TypeError(f"{what}: element size {isz} B, the plan needs {itemsize} B")
+    if n_el != numel:
+        raise ValueError(f"{what}: {n_el} elements, the plan needs {numel}")
 
 
 class Plan:
@@ -183,6 +234,9 @@ class Plan:
     def solve_device(self, f, u, stream: Optional[int] = None) -> None:
         """Enqueue u = solve(f) on `stream` (cudaStream_t as int; None = torch's current stream).
         f, u: CUDA tensors of n^3 values of the plan's precision (may be the same tensor)."""
+        n3, isz = self.n ** 3, self.precision // 8
+        _check_buffer(f, n3, isz, "solve_device f", self.device)
+        _check_buffer(u, n3, isz, "solve_device u", self.device)
         if stream is None:
             import torch
             stream = torch.cuda.current_stream(f.device).cuda_stream
@@ -191,22 +245,30 @@ class Plan:
 
     # ---- host boundary (the drop-in path)
     def solve_host(self, f, u) -> None:
+        n3, isz = self.n ** 3, self.precision // 8
+        _check_buffer(f, n3, isz, "solve_host f")
+        _check_buffer(u, n3, isz, "solve_host u")
         _check(lib.arena_poisson_solve_host(self._p, _vp(_ptr(f)), _vp(_ptr(u))), "arena_poisson_solve_host")
 
     def solve_host_batch(self, fs, us) -> None:
         """Solve fields fs[s] -> us[s] (host arrays / pinned tensors) with copy/compute overlap."""
         if len(fs) != len(us):
             raise ValueError("fs and us must have the same length")
+        n3, isz = self.n ** 3, self.precision // 8
+        for x in list(fs) + list(us):
+            _check_buffer(x, n3, isz, "solve_host_batch field")
         fa = (_vp * len(fs))(*[_ptr(x) for x in fs])
         ua = (_vp * len(us))(*[_ptr(x) for x in us])
         _check(lib.arena_poisson_solve_host_batch(self._p, len(fs), fa, ua), "arena_poisson_solve_host_batch")
 
     def dft3_forward_host(self, g: np.ndarray) -> np.ndarray:
+        _check_buffer(g, self.n ** 3, self.precision // 8, "dft3_forward g")
         out = np.empty(g.shape, dtype=np.complex128 if self.precision == 64 else np.complex64)
         _check(lib.arena_dft3_forward_host(self._p, _vp(g.ctypes.data), _vp(out.ctypes.data)), "dft3_forward")
         return out
 
     def dft3_inverse_host(self, spec: np.ndarray) -> np.ndarray:
+        _check_buffer(spec, self.n ** 3, self.precision // 4, "dft3_inverse spec")
         out = np.empty(spec.shape, dtype=self.dtype)
         _check(lib.arena_dft3_inverse_host(self._p, _vp(spec.ctypes.data), _vp(out.ctypes.data)), "dft3_inverse")
         return out
@@ -228,6 +290,10 @@ class Plan:
 XCHG_COPY, XCHG_PEER = 0, 1
 
 
+def _resolve_device(device: int) -> int:
+    return int(device) if device >= 0 else lib.arena_current_device()
+
+
 class _Decomposition:
     """Peer-exchange / phase methods shared by Slab and Pencil (prefix arena_slab_ / arena_pencil_)."""
 
@@ -236,7 +302,12 @@ class _Decomposition:
     def _fn(self, name):
         return getattr(lib, f"arena_{self._pfx}_{name}")
 
+    def _check_fields(self, f, u, what):
+        _check_buffer(f, self.field_numel, self.precision // 8, f"{what} f", self.device)
+        _check_buffer(u, self.field_numel, self.precision // 8, f"{what} u", self.device)
+
     def solve_device(self, f, u, stream: Optional[int] = None) -> None:
+        self._check_fields(f, u, "solve_device")
         if stream is None:
             import torch
             stream = torch.cuda.current_stream(f.device).cuda_stream
@@ -245,6 +316,7 @@ class _Decomposition:
 
     def solve_phase(self, phase: int, f, u, stream: Optional[int] = None) -> None:
         """One phase of a solve (slab 0-2, pencil 0-4); peer mode: synchronise the ranks in between."""
+        self._check_fields(f, u, "solve_phase")
         if stream is None:
             import torch
             stream = torch.cuda.current_stream(f.device).cuda_stream
@@ -316,6 +388,21 @@ class Slab(_Decomposition):
         _check(lib.arena_slab_info(self._s, ctypes.byref(ni), ctypes.byref(nj), ctypes.byref(cb), ctypes.byref(wb)),
                "arena_slab_info")
         self.ni, self.nj, self.chunk_bytes, self.workspace_bytes = ni.value, nj.value, cb.value, wb.value
+        self.precision = int(precision)
+        self.device = _resolve_device(device)
+        self.field_numel = self.n ** 3 if loopback else (self.n // self.nranks) * self.n * self.n
+
+    STAGES = ("k1k2", "xchg1", "k3", "xchg2", "k4k5")
+
+    def set_stage_timing(self, enable: bool) -> None:
+        _check(lib.arena_slab_set_stage_timing(self._s, int(bool(enable))), "arena_slab_set_stage_timing")
+
+    def stage_times(self):
+        """-> (dict stage -> total ms over the timed solves, number of solves)."""
+        ms = (ctypes.c_double * 5)()
+        ns = _i()
+        _check(lib.arena_slab_stage_times(self._s, ms, ctypes.byref(ns)), "arena_slab_stage_times")
+        return {k: ms[i] for i, k in enumerate(self.STAGES)}, ns.value
 
 
 class Pencil(_Decomposition):
@@ -348,6 +435,9 @@ class Pencil(_Decomposition):
         kq, bb, kb = _i(), ctypes.c_size_t(), ctypes.c_size_t()
         _check(lib.arena_pencil_info(self._s, ctypes.byref(kq), ctypes.byref(bb), ctypes.byref(kb)), "arena_pencil_info")
         self.kq, self.buffer_bytes, self.block_bytes = kq.value, bb.value, kb.value
+        self.precision = int(precision)
+        self.device = _resolve_device(device)
+        self.field_numel = self.n ** 3 if loopback else (self.n // self.pr) * (self.n // self.pc) * self.n
 
 
 def nccl_unique_id() -> bytes:

@@ -45,7 +45,7 @@ struct PlanDeleter {
 
 int selected_device() {
   if (const char* s = std::getenv("ARENA_FFT_DEVICE")) return std::atoi(s);
-  return -1;  // current device
+  return arena_current_device();  // resolved before keying: threads on other devices get their own plan
 }
 
 // (n, precision, device) -> plan.  Mirrors the reference's single planner

@@ -21,7 +21,7 @@ constexpr int kPow2Launches = 5;
 // (encoded on first use; they depend only on the buffers and the geometry).
 struct alignas(64) TmaCache {
   unsigned char maps[4][128];  // CUtensorMap: y boxes over B, x boxes over C, fused-kernel y boxes over B,
-                              // half-row y boxes over B (k_ystream)
+                              // (spare)
   const void* specB = nullptr;
   const void* specC = nullptr;
   int n = 0, ni = 0, nj = 0, nchunks = 0, quad = 0;

@@ -118,6 +118,13 @@ struct arena_fft_plan {
   std::vector<double> stage_ms;
   int solves = 0;
   std::mutex ev_mu;
+  // Every solve on this plan reads and writes the plan's workspace (spec, Q) and
+  // may update the graph / TMA caches.  enq_mu serialises the enqueues, and
+  // ws_ev (recorded after each solve's last launch) makes the next solve's
+  // stream wait for the previous one, whatever streams the callers use.
+  std::mutex enq_mu;
+  cudaEvent_t ws_ev = nullptr;
+  bool ws_ev_live = false;
 
   int launches() const {
     if (path != ARENA_PATH_POW2) return split3 ? kSplit3Launches : kGenLaunches;
@@ -195,6 +202,7 @@ void free_plan(arena_fft_plan* p) {
   delete p->tma;
   delete p->stager;
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
+  if (p->ws_ev) cudaEventDestroy(p->ws_ev);
   delete p;
 }
 
@@ -220,7 +228,7 @@ arena_status enqueue_kernels(arena_fft_plan* p, const void* d_f, void* d_u, cuda
 // their launch sequence is captured once per (f, u) into a CUDA graph and
 // replayed with one cudaGraphLaunch.  Not used with stage timing or on the
 // legacy default stream (which cannot be captured).
-arena_status enqueue_solve(arena_fft_plan* p, const void* d_f, void* d_u, cudaStream_t s) {
+arena_status enqueue_solve_locked(arena_fft_plan* p, const void* d_f, void* d_u, cudaStream_t s) {
   if (p->use_graphs && !p->timing && s != nullptr) {
     for (auto& ge : p->graphs)
       if (ge.f == d_f && ge.u == d_u) {
@@ -253,6 +261,21 @@ arena_status enqueue_solve(arena_fft_plan* p, const void* d_f, void* d_u, cudaSt
     return ARENA_OK;
   }
   return enqueue_kernels(p, d_f, d_u, s, timing_events(p));
+}
+
+// Workspace ordering across callers and streams (see arena_fft_plan::enq_mu).
+arena_status enqueue_solve(arena_fft_plan* p, const void* d_f, void* d_u, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(p->enq_mu);
+  cudaError_t e;
+  if (!p->ws_ev && (e = cudaEventCreateWithFlags(&p->ws_ev, cudaEventDisableTiming)) != cudaSuccess)
+    return cuda_fail(e, "cudaEventCreate");
+  if (p->ws_ev_live && (e = cudaStreamWaitEvent(s, p->ws_ev, 0)) != cudaSuccess)
+    return cuda_fail(e, "cudaStreamWaitEvent (previous solve on this plan)");
+  arena_status st = enqueue_solve_locked(p, d_f, d_u, s);
+  if (st != ARENA_OK) return st;
+  if ((e = cudaEventRecord(p->ws_ev, s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  p->ws_ev_live = true;
+  return ARENA_OK;
 }
 
 arena_status enqueue_kernels(arena_fft_plan* p, const void* d_f, void* d_u, cudaStream_t s, cudaEvent_t* ev) {
@@ -336,7 +359,12 @@ extern "C" {
 
 const char* arena_last_error(void) { return g_last_error.c_str(); }
 
-int arena_fft_abi_version(void) { return 100; }
+int arena_fft_abi_version(void) { return 101; }
+
+int arena_current_device(void) {
+  int d = -1;
+  return cudaGetDevice(&d) == cudaSuccess ? d : -1;
+}
 
 }  // extern "C"
 
@@ -466,7 +494,7 @@ arena_status arena_fft_plan_info(const arena_fft_plan* p, int* n, int* precision
   if (precision_bits) *precision_bits = p->prec;
   if (path) *path = p->path;
   if (device) *device = p->device;
-  if (workspace_bytes) *workspace_bytes = p->spec_bytes;
+  if (workspace_bytes) *workspace_bytes = p->spec_bytes + (p->Q ? p->spec_bytes : 0);  // split plans own Q too
   return ARENA_OK;
 }
 
@@ -891,14 +919,23 @@ struct arena_fft_slab {
   int xmode = ARENA_XCHG_COPY;  // ARENA_XCHG_PEER: K2 / K3 store into the peers' workspaces
   bool attached = false;        // peer pointers of the other ranks opened (multi-process)
   PeerSync sync;
+  // stage timing (arena_slab_set_stage_timing): kSlabMarks events per solve
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  int ev_sets = 0;
+  double stage_ms[5] = {0, 0, 0, 0, 0};
+  int solves = 0;
 };
 
 namespace {
+
+constexpr int kSlabMarks = 6;  // K1+K2 | exchange #1 | K3 | exchange #2 | K4+K5
 
 void free_slab(arena_fft_slab* s) {
   if (!s) return;
   if (s->base) {
     DeviceGuard g(s->base->device);
+    for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
     s->sync.release();
     for (SlabRank& r : s->ranks) {
       if (r.B) cudaFree(r.B);
@@ -1083,7 +1120,7 @@ arena_status arena_slab_info(const arena_fft_slab* s, int* ni, int* nj, size_t* 
 // mode every rank must have finished phase p before any rank starts phase p+1
 // (arena_slab_solve_device inserts a device barrier; a caller driving the
 // phases itself synchronises the ranks between them).
-static arena_status slab_run_phase(arena_fft_slab* s, int phase, const void* d_f, void* d_u, cudaStream_t st) {
+static arena_status slab_run_kernels(arena_fft_slab* s, int phase, const void* d_f, void* d_u, cudaStream_t st) {
   static const int kPh[3] = {kPhaseZY, kPhaseX, kPhaseYZ};
   static const char* kWhat[3] = {"slab K1+K2", "slab K3", "slab K4+K5"};
   if (phase < 0 || phase > 2) return fail(ARENA_EINVAL, "slab phase must be 0, 1 or 2");
@@ -1098,8 +1135,26 @@ static arena_status slab_run_phase(arena_fft_slab* s, int phase, const void* d_f
     cudaError_t e = slab_phase(s, s->ranks[v], rank, f, u, st, kPh[phase]);
     if (e != cudaSuccess) return cuda_fail(e, kWhat[phase]);
   }
+  return ARENA_OK;
+}
+
+static arena_status slab_run_phase(arena_fft_slab* s, int phase, const void* d_f, void* d_u, cudaStream_t st) {
+  arena_status stt = slab_run_kernels(s, phase, d_f, d_u, st);
+  if (stt != ARENA_OK) return stt;
   if (phase < 2 && s->xmode != ARENA_XCHG_PEER) return slab_exchange(s, st, phase == 0);
   return ARENA_OK;
+}
+
+// Events of one timed solve (kSlabMarks), recycled by arena_slab_stage_times.
+static cudaEvent_t* slab_timing_events(arena_fft_slab* s) {
+  if (!s->timing) return nullptr;
+  const size_t need = size_t(s->ev_sets + 1) * kSlabMarks;
+  while (s->ev_pool.size() < need) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    s->ev_pool.push_back(e);
+  }
+  return s->ev_pool.data() + size_t(s->ev_sets++) * kSlabMarks;
 }
 
 arena_status arena_slab_solve_device(arena_fft_slab* s, const void* d_f, void* d_u, void* stream) {
@@ -1107,11 +1162,47 @@ arena_status arena_slab_solve_device(arena_fft_slab* s, const void* d_f, void* d
   DeviceGuard g(s->base->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool barrier = s->xmode == ARENA_XCHG_PEER && !s->loopback && s->P > 1;
+  cudaEvent_t* ev = slab_timing_events(s);
   for (int phase = 0; phase < 3; ++phase) {
-    arena_status stt = slab_run_phase(s, phase, d_f, d_u, st);
+    if (ev) cudaEventRecord(ev[2 * phase], st);
+    arena_status stt = slab_run_kernels(s, phase, d_f, d_u, st);
     if (stt != ARENA_OK) return stt;
-    if (barrier && phase < 2 && (stt = slab_peer_barrier(s, st)) != ARENA_OK) return stt;
+    if (ev) cudaEventRecord(ev[2 * phase + 1], st);
+    if (phase == 2) break;
+    if (s->xmode != ARENA_XCHG_PEER) stt = slab_exchange(s, st, phase == 0);
+    else if (barrier) stt = slab_peer_barrier(s, st);
+    if (stt != ARENA_OK) return stt;
   }
+  return ARENA_OK;
+}
+
+arena_status arena_slab_set_stage_timing(arena_fft_slab* s, int enable) {
+  if (!s) return fail(ARENA_EINVAL, "slab is NULL");
+  s->timing = enable != 0;
+  s->ev_sets = 0;
+  for (double& x : s->stage_ms) x = 0.0;
+  s->solves = 0;
+  return ARENA_OK;
+}
+
+arena_status arena_slab_stage_times(arena_fft_slab* s, double* ms5, int* n_solves) {
+  if (!s) return fail(ARENA_EINVAL, "slab is NULL");
+  DeviceGuard g(s->base->device);
+  for (int k = 0; k < s->ev_sets; ++k) {
+    cudaEvent_t* ev = s->ev_pool.data() + size_t(k) * kSlabMarks;
+    cudaError_t e = cudaEventSynchronize(ev[kSlabMarks - 1]);
+    if (e != cudaSuccess) return cuda_fail(e, "slab stage timing sync");
+    for (int m = 0; m + 1 < kSlabMarks; ++m) {
+      float t = 0.f;
+      if ((e = cudaEventElapsedTime(&t, ev[m], ev[m + 1])) != cudaSuccess) return cuda_fail(e, "cudaEventElapsedTime");
+      s->stage_ms[m] += t;
+    }
+    ++s->solves;
+  }
+  s->ev_sets = 0;
+  if (ms5)
+    for (int m = 0; m < 5; ++m) ms5[m] = s->stage_ms[m];
+  if (n_solves) *n_solves = s->solves;
   return ARENA_OK;
 }
 

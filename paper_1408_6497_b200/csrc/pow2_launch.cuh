@@ -11,7 +11,6 @@
 #include "poisson_fused.cuh"
 #include "poisson_quad.cuh"
 #include "poisson_split3.cuh"
-#include "poisson_ystream.cuh"
 
 namespace arena_fft {
 
@@ -118,27 +117,6 @@ cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* 
                                                a.nchunks, a.j0, ks, static_cast<V*>(out ? out : spec),
                                                gout ? *gout : g, pov);
   return cudaGetLastError();
-}
-
-template <typename T, int N, int PASS>
-cudaError_t launch_ystream(const Pow2Args& a, const CUtensorMap& map, const Layout& g, KSpan ks, void* out,
-                           const Layout& gout) {
-  using C = YsCfg<T, N>;
-  using V = vec2_t<T>;
-  if constexpr (!C::OK) {
-    return cudaErrorNotSupported;
-  } else {
-    auto kern = k_ystream<T, N, PASS>;
-    cudaError_t e = ensure_smem<k_ystream<T, N, PASS>>(C::SMEM, C::THREADS);
-    if (e) return e;
-    int per_sm = 1;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM))) return e;
-    const int tiles = g.ni * ((ks.kc + C::L - 1) / C::L);
-    int grid = a.sm_count * (per_sm > 0 ? per_sm : 1);
-    if (grid > tiles) grid = tiles;
-    kern<<<grid, C::THREADS, C::SMEM, a.stream>>>(map, stw_ptr<T>(a, 1, C::E), g, ks, static_cast<V*>(out), gout);
-    return cudaGetLastError();
-  }
 }
 
 // Peer destinations of a scattering pass: chunk c -> peers[c] (rank c's
@@ -375,11 +353,6 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
       if ((e = encode_map<T, NR>(c->maps[2], a.spec, gB, a.nchunks, true, NR / 2 + 1, spec_pitch(NR),
                                  TmaCfg<T, NR, false>::L)))
         return e;
-      if constexpr (ARENA_YSTREAM && YsCfg<T, NR>::OK) {
-        if ((e = encode_map<T, NR>(c->maps[3], a.spec, gB, a.nchunks, true, NR / 2 + 1, spec_pitch(NR),
-                                   YsCfg<T, NR>::LH)))
-          return e;
-      }
       c->specB = a.spec;
       c->specC = a.specC;
       c->n = NR;
@@ -392,8 +365,6 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   const CUtensorMap* my = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[0]) : nullptr;
   const CUtensorMap* mx = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[1]) : nullptr;
   const CUtensorMap* mf = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[2]) : nullptr;
-  const CUtensorMap* mys = tma ? reinterpret_cast<const CUtensorMap*>(a.tma->maps[3]) : nullptr;
-  constexpr bool ys = ARENA_YSTREAM && YsCfg<T, NR>::OK;
   const KSpan kfull{NR / 2 + 1, spec_pitch(NR), 0};
   // one GPU, in place: the x kernel's compile-time geometry (FIXED) applies (B200
   // 1024^3: x 4.53 -> 4.32 ms fp64, 2.57 -> 2.20 ms fp32; the y passes measured
@@ -424,8 +395,7 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
       }
       if (e) return e;
     } else if (tma) {
-      if constexpr (ys) e = launch_ystream<T, NR, 0>(a, *mys, gB, kfull, a.spec, gB);
-      else e = launch_strided_tma<T, NR, 0>(a, *my, a.spec, gB, scale, four_pi2);
+      e = launch_strided_tma<T, NR, 0>(a, *my, a.spec, gB, scale, four_pi2);
       if (e) return e;
     } else {
       if ((e = ensure_smem<k_ypass<T, NR, -1>>(SC::SMEM, SC::THREADS))) return e;
@@ -462,8 +432,7 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   } else if (a.phases & kPhaseYZ) {
     mark(a, mk++);
     if (tma) {
-      if constexpr (ys) e = launch_ystream<T, NR, 1>(a, *mys, gB, kfull, a.spec, gB);
-      else e = launch_strided_tma<T, NR, 1>(a, *my, a.spec, gB, scale, four_pi2);
+      e = launch_strided_tma<T, NR, 1>(a, *my, a.spec, gB, scale, four_pi2);
       if (e) return e;
     } else {
       if ((e = ensure_smem<k_ypass<T, NR, +1>>(SC::SMEM, SC::THREADS))) return e;

@@ -173,6 +173,39 @@ def fill_device(src, which: str, out, precision: int = 64, stream: int = 0, i0: 
         source_gaussian(src.n, src.alpha, src.center, 1 if which == "f" else 0, out, precision, stream, i0, ni, j0, nj)
 
 
+def host_field(src, which: str = "f", workers: Optional[int] = None) -> np.ndarray:
+    """f (or the analytic u) of `src` on the host at any n, without the GPU.
+
+    Mode sources are band-limited, so the field is the c2r transform of a sparse
+    half spectrum (scipy pocketfft, `workers` threads): with N = n^3 and kz taken
+    mod n, a mode with 0 < kz < n/2 puts a N/2 at (kx, ky, kz), n/2 < kz puts
+    conj(a) N/2 at -k, and the self-conjugate planes kz = 0, n/2 take a N, whose
+    imaginary part the c2r's last axis drops — Re(a e^{2 pi i k.x}) in every case.  Other sources: eval_host (small n)."""
+    if not isinstance(src, ModeSource):
+        return eval_host(src, which)
+    import os
+
+    import scipy.fft as sf
+
+    n = src.n
+    N = float(n) ** 3
+    nc = n // 2 + 1
+    coef = src.f_coef() if which == "f" else src.u_coef()
+    H = np.zeros((n, n, nc), dtype=np.complex128)
+    for (kx, ky, kz), c in zip(src.k, coef):
+        kz = int(kz) % n  # the grid aliases k to k mod n
+        if kz == 0 or 2 * kz == n:  # self-conjugate planes (DC, Nyquist): c2r keeps Re
+            H[kx % n, ky % n, kz] += c * N
+        elif kz < nc:
+            H[kx % n, ky % n, kz] += 0.5 * c * N
+        else:
+            H[-kx % n, -ky % n, n - kz] += 0.5 * np.conj(c) * N
+    w = workers or len(os.sched_getaffinity(0))
+    out = sf.irfftn(H, s=(n, n, n), workers=w, overwrite_x=True)
+    del H
+    return np.ascontiguousarray(out)
+
+
 def eval_host(src, which: str) -> np.ndarray:
     """Host (numpy) evaluation of f or analytic u — for small n only (tests, oracle inputs)."""
     n = src.n

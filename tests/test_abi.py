@@ -47,7 +47,7 @@ def test_kernels_are_sm100a():
 
 
 def test_abi_version():
-    assert arena.lib.arena_fft_abi_version() == 100
+    assert arena.lib.arena_fft_abi_version() == 101
 
 
 def test_invalid_n_raises_like_gridfield():

@@ -96,3 +96,24 @@ def test_config_sources_deterministic():
     assert c.k.shape == (32, 3) and np.all(np.abs(c.k) <= 8)
     g = problems.config(3)
     assert all(0.0 <= x < 1.0 for x in g.center) and g.alpha == 1e4
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 6, 7, 9, 12, 16, 30, 64, 96])
+def test_shim_engine_vs_independent_restatement(n):
+    """The FFTW stand-in behind the shim (oracle/fftw_shim/vfft.c: Stockham, 8 lines per
+    SIMD batch, two real rows per complex FFT) against the independent recursive
+    restatement (oracle/offt.c) — odd n, odd row counts, generic radices."""
+    if not oracle.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    f = np.random.default_rng(n).standard_normal((n, n, n))
+    a, b = oracle.poisson_solve(f, "ref"), oracle.poisson_solve(f, "port")
+    assert _rel(a, b) <= 1e-14
+    g = np.random.default_rng(n + 1).standard_normal((n, n, n))
+    assert _rel(oracle.dft3_forward(g, "ref"), oracle.dft3_forward(g, "port")) <= 1e-14
+
+
+def test_pocketfft_restatement_vs_reference():
+    """B-all engine of the CPU baseline (scipy pocketfft) against the reference solver."""
+    for n in (6, 7, 32):
+        f = np.random.default_rng(n).standard_normal((n, n, n))
+        assert _rel(oracle.pocketfft_poisson(f), oracle.poisson_solve(f)) <= 1e-14

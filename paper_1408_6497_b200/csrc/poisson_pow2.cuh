@@ -458,6 +458,9 @@ namespace arena_fft {
 #ifndef ARENA_TMA_X_TILE
 #define ARENA_TMA_X_TILE (64 * 1024)  // x-pass tile budget (bytes)
 #endif
+#ifndef ARENA_TMA_E_XS
+#define ARENA_TMA_E_XS 32  // fp64 x pass on lines of N <= 512 points (quadrant / split lines)
+#endif
 #ifndef ARENA_TMA_NBUF_Y
 #define ARENA_TMA_NBUF_Y ARENA_TMA_NBUF
 #endif
@@ -514,7 +517,9 @@ template <typename T, int N, bool YP, bool XW>
 struct TmaCfg {
   static constexpr bool F64 = sizeof(T) == 8;
   static constexpr int VB = 2 * sizeof(T);
-  static constexpr int E = imin(YP ? (F64 ? ARENA_TMA_E_Y : ARENA_TMA_E_Y32) : (F64 ? ARENA_TMA_E : ARENA_TMA_E32), N);
+  static constexpr int E = imin(YP ? (F64 ? ARENA_TMA_E_Y : ARENA_TMA_E_Y32)
+                                   : (F64 ? (N <= 512 ? ARENA_TMA_E_XS : ARENA_TMA_E) : ARENA_TMA_E32),
+                                N);
   static constexpr int P = N / E;
   static constexpr int BUDGET0 = YP ? (F64 ? ARENA_TMA_Y_TILE : ARENA_TMA_Y_TILE32)
                                     : (F64 ? ARENA_TMA_X_TILE : ARENA_TMA_X_TILE32);
@@ -555,6 +560,31 @@ struct KSpan {
   int kc, kq, k0;
 };
 
+// Chunked ("split") layouts of the single-GPU path, selected by the SPL template
+// argument of the strided kernels: SPL = R > 0 splits both i and j by R (R*R
+// chunks of (n/R)^2 rows: the quadrant formulation R = 2, poisson_quad.cuh; the
+// radix-3/5 splits, poisson_split3.cuh); SPL = kSplitI splits only i by 2 (two
+// chunks of (n/2) x n rows: poisson_hq.cuh), so the y lines keep all n points
+// and only the x lines are halved.
+constexpr int kSplitI = -2;
+__host__ __device__ constexpr int spl_chunks(int spl) { return spl > 0 ? spl * spl : spl == kSplitI ? 2 : 1; }
+// Compile-time geometry of a FIXED (single-GPU) strided pass on N-point lines.
+template <int N, int SPL, int PASS>
+__host__ __device__ constexpr Layout fixed_geom() {
+  if constexpr (SPL == kSplitI) {
+    return PASS == 2 ? Layout{N, 2 * N, ilog2_c(N), ilog2_c(2 * N), ilog2_c(2 * N < ARENA_JBLOCK ? 2 * N : ARENA_JBLOCK)}
+                     : Layout{N / 2, N, ilog2_c(N / 2), ilog2_c(N), ilog2_c(N < ARENA_JBLOCK ? N : ARENA_JBLOCK)};
+  } else {
+    return fixed_layout<N>();
+  }
+}
+template <int N, int SPL, int PASS>
+__host__ __device__ constexpr KSpan fixed_kspan() {
+  // the n of the grid the N-point lines belong to
+  constexpr int NG = SPL > 0 ? SPL * N : (SPL == kSplitI && PASS == 2) ? 2 * N : N;
+  return KSpan{NG / 2 + 1, spec_pitch(NG), 0};
+}
+
 // PASS 0: y forward, 1: y backward (layout B, tiles over (il, k-tile)); the y
 // passes may write to another buffer / layout (`out`, `gout`; the pencil path
 // re-chunks j between its two exchanges).
@@ -578,31 +608,31 @@ struct PeerOut {
 // tile index gt = (chunk * lines + outer) * KT + k-tile, and the symbol reads
 // ki = SPL i' + ci, kj = SPL j' + cj of the n-point transform (chunk = SPL ci + cj).
 template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false, int SPL = 0>
-__global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, (SPL > 0)>()>::THREADS,
-                                  TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, (SPL > 0)>()>::MINB)
+__global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, (SPL != 0)>()>::THREADS,
+                                  TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, (SPL != 0)>()>::MINB)
     k_strided_tma(const __grid_constant__ CUtensorMap tmap, vec2_t<T>* __restrict__ spec,
                   const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g_, int nchunks_, int j0_, KSpan ks_,
                   vec2_t<T>* __restrict__ out_, Layout gout_, const __grid_constant__ PeerOut<vec2_t<T>> po) {
   static_assert(!(FIXED && PEER), "the fixed geometry is the single-GPU one");
-  constexpr bool QUAD = SPL > 0;
+  constexpr bool QUAD = SPL != 0;  // chunked split layout (SPL > 0: i and j split by SPL; kSplitI: i by 2)
+  constexpr int NCH = spl_chunks(SPL);
   static_assert(!(QUAD && PEER), "the quadrant layout is single-GPU");
-  const Layout g = FIXED ? fixed_layout<N>() : g_;
-  const Layout gout = FIXED ? fixed_layout<N>() : gout_;
+  const Layout g = FIXED ? fixed_geom<N, SPL, PASS>() : g_;
+  const Layout gout = FIXED ? fixed_geom<N, SPL, PASS>() : gout_;
   const int nchunks = FIXED ? 1 : nchunks_;
   const int j0 = FIXED ? 0 : j0_;
   // FIXED: the single-GPU geometry (QUAD: a chunk of the 2N grid's quadrant layout)
-  const KSpan ks = FIXED ? (QUAD ? KSpan{SPL * N / 2 + 1, spec_pitch(SPL * N), 0} : KSpan{N / 2 + 1, spec_pitch(N), 0})
-                         : ks_;
+  const KSpan ks = FIXED ? fixed_kspan<N, SPL, PASS>() : ks_;
   vec2_t<T>* __restrict__ out = FIXED ? spec : out_;
   using V = vec2_t<T>;
-  using C = TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, (SPL > 0)>()>;
+  using C = TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, (SPL != 0)>()>;
   constexpr int E = C::E, P = C::P, L = C::L, TILE = C::TILE;
   constexpr uint32_t TILE_BYTES = TILE * sizeof(V);
   constexpr int NBUF = C::NBUF;
   const int KT = (ks.kc + L - 1) / L;
   const size_t kq = size_t(ks.kq);
   const int NL = (PASS < 2 ? g.ni : g.nj) * KT;  // tiles per chunk (QUAD) / in all
-  const int NT = NL * (QUAD ? SPL * SPL : 1);
+  const int NT = NL * NCH;
   constexpr bool TWS = PASS == 2 ? bool(ARENA_TMA_TWSMEM_X) : bool(ARENA_TMA_TWSMEM_Y);
   V* bufs = smem_base<V>();
   V* tws = bufs + NBUF * TILE;
@@ -722,12 +752,18 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
       line_fft_tail<N, E, L, +1>(v, cur, twp, t, l);
     } else {
       line_fft<N, E, L, -1>(v, cur, twp, t, l);
-      const T kj = QUAD ? T(signed_freq(SPL * outer + qd % imax(SPL, 1), SPL * N)) : T(signed_freq(j0 + outer, N));
+      // full-grid frequencies: SPL > 0: (ki, kj) = (SPL i'' + ci, SPL j'' + cj), chunk SPL ci + cj;
+      // kSplitI: ki = 2 i'' + chunk, kj = j (lines of N = n/2 points)
+      constexpr int NG = SPL > 0 ? SPL * N : QUAD ? 2 * N : N;
+      const T kj = SPL > 0 ? T(signed_freq(SPL * outer + qd % imax(SPL, 1), NG))
+                           : T(signed_freq(j0 + outer, NG));
       const T kk = T(ks.k0 + k);
       const T c = kj * kj + kk * kk;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const T ki = QUAD ? T(signed_freq(SPL * (t + P * e) + qd / imax(SPL, 1), SPL * N)) : T(signed_freq(t + P * e, N));
+        const T ki = SPL > 0 ? T(signed_freq(SPL * (t + P * e) + qd / imax(SPL, 1), NG))
+                     : QUAD  ? T(signed_freq(2 * (t + P * e) + qd, NG))
+                             : T(signed_freq(t + P * e, NG));
         const T k2 = ki * ki + c;
         const T m = poisson_symbol(k2, scale, four_pi2);
         v[e].x *= m;

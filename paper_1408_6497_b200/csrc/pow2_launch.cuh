@@ -99,7 +99,7 @@ template <typename T, int N, int PASS, bool PEER = false, bool FIXED = false, in
 cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* spec, const Layout& g, T scale,
                                T four_pi2, KSpan ks = KSpan{N / 2 + 1, spec_pitch(N), 0}, void* out = nullptr,
                                const Layout* gout = nullptr, const PeerOut<vec2_t<T>>* po = nullptr) {
-  using C = TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, (SPL > 0)>()>;
+  using C = TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T, (SPL != 0)>()>;
   using V = vec2_t<T>;
   auto kern = k_strided_tma<T, N, PASS, PEER, FIXED, SPL>;
   constexpr int SMEM = PASS == 2 ? C::SMEM_X : C::SMEM_Y;
@@ -109,11 +109,11 @@ cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* 
   if (po) pov = *po;
   int per_sm = 1;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, SMEM))) return e;
-  const int tiles = (PASS < 2 ? g.ni : g.nj) * ((ks.kc + C::L - 1) / C::L) * (SPL ? SPL * SPL : 1);
+  const int tiles = (PASS < 2 ? g.ni : g.nj) * ((ks.kc + C::L - 1) / C::L) * spl_chunks(SPL);
   int grid = a.sm_count * (per_sm > 0 ? per_sm : 1);
   if (grid > tiles) grid = tiles;
-  // stage twiddles of N-point lines: table `which` 1 (N = n), 0 (N = n/2, quadrant lines)
-  kern<<<grid, C::THREADS, SMEM, a.stream>>>(map, static_cast<V*>(spec), stw_ptr<T>(a, SPL ? 0 : 1, C::E), scale, four_pi2, g,
+  // stage twiddles of N-point lines: table `which` 1 (N = n), 0 (N = n/2: quadrant / split lines)
+  kern<<<grid, C::THREADS, SMEM, a.stream>>>(map, static_cast<V*>(spec), stw_ptr<T>(a, N == a.n ? 1 : 0, C::E), scale, four_pi2, g,
                                                a.nchunks, a.j0, ks, static_cast<V*>(out ? out : spec),
                                                gout ? *gout : g, pov);
   return cudaGetLastError();

@@ -156,6 +156,20 @@ arena_status arena_slab_peer_export(arena_fft_slab* slab, void* out, int len);
 arena_status arena_slab_peer_attach(arena_fft_slab* slab, const void* all_handles, int len);
 /* Switch the exchange of a loopback slab (or an attached NCCL slab). */
 arena_status arena_slab_set_exchange(arena_fft_slab* slab, int mode);
+/* COPY exchange in sub-steps (default 4 per direction, env ARENA_SLAB_CHUNKS): the
+ * all-to-all of sub-range k (forward: the rank's i planes; backward: whole 64-row j
+ * blocks of its j lines) runs on the slab's exchange stream while K1+K2 (K3) of
+ * sub-range k+1 run on the solve's stream.  1, 1 = whole passes, then whole chunks. */
+arena_status arena_slab_set_chunking(arena_fft_slab* slab, int fwd_substeps, int bwd_substeps);
+arena_status arena_slab_get_chunking(const arena_fft_slab* slab, int* fwd_substeps, int* bwd_substeps);
+/* Host-only (no device needed): the in-chunk row ranges {first[k], rows[k]} a sub-step
+ * [lo, hi) of an exchange moves between every pair of ranks; returns their count
+ * (-1: bad arguments).  For the CPU model tests of the chunked schedule. */
+int arena_slab_exchange_pieces(int n, int nranks, int forward, int lo, int hi, size_t* first, size_t* rows, int max);
+/* Wait for a solve enqueued on `stream` with NCCL error / hang detection: polls
+ * ncclCommGetAsyncError, aborts the communicator (ARENA_ENCCL) on an asynchronous
+ * error or when the solve has not completed after timeout_s seconds. */
+arena_status arena_slab_wait(arena_fft_slab* slab, void* stream, double timeout_s);
 /* Per-stage CUDA-event timing of arena_slab_solve_device on the solve's stream:
  * ms5 = total ms over the timed solves of {K1+K2, exchange #1, K3, exchange #2,
  * K4+K5} (PEER mode: the exchanges are inside K2 / K3 and the "exchange" stages
@@ -210,6 +224,22 @@ arena_status arena_pencil_peer_attach(arena_fft_pencil* pencil, const void* all_
 arena_status arena_pencil_set_exchange(arena_fft_pencil* pencil, int mode);
 arena_status arena_pencil_solve_phase(arena_fft_pencil* pencil, int phase, const void* d_f, void* d_u, void* stream);
 arena_status arena_pencil_barrier_status(arena_fft_pencil* pencil);
+
+/* One process driving P GPUs (P <= 8; the drop-in's multi-GPU path, selected by
+ * ARENA_FFT_NGPU): rank v lives on devices[v] (NULL: v mod device count) and holds
+ * the planes i in [v n/P, (v+1) n/P) — a contiguous slab of GridField.data.  The
+ * all-to-alls are fused into K2 / K3 as stores into the other GPUs' workspaces
+ * through peer access (NVLink), the phases ordered by cross-device events.
+ * Power-of-two n >= 16, n/P >= 4.  solve_device: per-rank shard pointers (and
+ * streams, NULL = the object's own); solve_host: the whole n^3 host field, moved
+ * slab by slab over the P PCIe links in parallel (synchronous). */
+typedef struct arena_fft_mgpu arena_fft_mgpu;
+arena_status arena_mgpu_create(arena_fft_mgpu** mgpu, int n, int precision_bits, int nranks, const int* devices);
+void arena_mgpu_destroy(arena_fft_mgpu* mgpu);
+arena_status arena_mgpu_info(const arena_fft_mgpu* mgpu, int* nranks, int* devices, size_t* slab_bytes);
+arena_status arena_mgpu_solve_device(arena_fft_mgpu* mgpu, const void* const* d_f, void* const* d_u,
+                                     void* const* streams);
+arena_status arena_mgpu_solve_host(arena_fft_mgpu* mgpu, const void* f, void* u);
 
 /* Batch evaluation of arena::SpectralInterpolant (fft_solver.cpp:89-114) on the
  * GPU: out[p] = sum_m Re(amp_m exp(2 pi i k_m . x_p)).  k: 3*nmodes ints (signed

@@ -85,6 +85,11 @@ _sig = {
     "arena_slab_solve_phase": (_i, [_vp, _i, _vp, _vp, _vp]),
     "arena_slab_barrier_status": (_i, [_vp]),
     "arena_slab_set_stage_timing": (_i, [_vp, _i]),
+    "arena_slab_set_chunking": (_i, [_vp, _i, _i]),
+    "arena_slab_get_chunking": (_i, [_vp, ctypes.POINTER(_i), ctypes.POINTER(_i)]),
+    "arena_slab_exchange_pieces": (_i, [_i, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_size_t),
+                                        ctypes.POINTER(ctypes.c_size_t), _i]),
+    "arena_slab_wait": (_i, [_vp, _vp, ctypes.c_double]),
     "arena_slab_stage_times": (_i, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i)]),
     "arena_peer_barrier_selftest": (_i, [_i, _i, _i, ctypes.POINTER(_i)]),
     "arena_pencil_create_peer": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _i, _i, _i]),
@@ -110,6 +115,11 @@ _sig = {
     "arena_last_error": (ctypes.c_char_p, []),
     "arena_fft_abi_version": (_i, []),
     "arena_current_device": (_i, []),
+    "arena_mgpu_create": (_i, [ctypes.POINTER(_vp), _i, _i, _i, ctypes.POINTER(_i)]),
+    "arena_mgpu_destroy": (None, [_vp]),
+    "arena_mgpu_info": (_i, [_vp, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(ctypes.c_size_t)]),
+    "arena_mgpu_solve_device": (_i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "arena_mgpu_solve_host": (_i, [_vp, _vp, _vp]),
 }
 _lib = None
 _lib_lock = threading.Lock()
@@ -394,6 +404,24 @@ class Slab(_Decomposition):
 
     STAGES = ("k1k2", "xchg1", "k3", "xchg2", "k4k5")
 
+    def set_chunking(self, fwd: int, bwd: int) -> None:
+        """Sub-steps of the COPY exchange per direction (1, 1: whole chunks after whole passes)."""
+        _check(lib.arena_slab_set_chunking(self._s, int(fwd), int(bwd)), "arena_slab_set_chunking")
+
+    @property
+    def chunking(self):
+        f, b = _i(), _i()
+        _check(lib.arena_slab_get_chunking(self._s, ctypes.byref(f), ctypes.byref(b)), "arena_slab_get_chunking")
+        return f.value, b.value
+
+    def wait(self, stream: Optional[int] = None, timeout_s: float = 60.0) -> None:
+        """Block until the solves enqueued on `stream` finish, with NCCL error / hang detection
+        (the communicator is aborted and ArenaError raised on an async error or timeout)."""
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        _check(lib.arena_slab_wait(self._s, _vp(stream), float(timeout_s)), "arena_slab_wait")
+
     def set_stage_timing(self, enable: bool) -> None:
         _check(lib.arena_slab_set_stage_timing(self._s, int(bool(enable))), "arena_slab_set_stage_timing")
 
@@ -438,6 +466,71 @@ class Pencil(_Decomposition):
         self.precision = int(precision)
         self.device = _resolve_device(device)
         self.field_numel = self.n ** 3 if loopback else (self.n // self.pr) * (self.n // self.pc) * self.n
+
+
+class MultiGPU:
+    """P GPUs driven by this process (include/arena_fft.h arena_mgpu_*): rank v on
+    devices[v] owns planes [v n/P, (v+1) n/P); the exchanges are peer stores fused
+    into K2 / K3, the phases ordered by cross-device events.  The drop-in C++
+    poisson_spectral_solve uses it when ARENA_FFT_NGPU > 1."""
+
+    def __init__(self, n: int, nranks: int, devices=None, precision: int = 64):
+        self._m = _vp()
+        dv = None
+        if devices is not None:
+            if len(devices) != nranks:
+                raise ValueError("one device per rank")
+            dv = (_i * nranks)(*[int(d) for d in devices])
+        _check(lib.arena_mgpu_create(ctypes.byref(self._m), int(n), int(precision), int(nranks), dv),
+               "arena_mgpu_create")
+        self.n, self.nranks, self.precision = int(n), int(nranks), int(precision)
+        P, sb = _i(), ctypes.c_size_t()
+        devs = (_i * nranks)()
+        _check(lib.arena_mgpu_info(self._m, ctypes.byref(P), devs, ctypes.byref(sb)), "arena_mgpu_info")
+        self.devices, self.slab_bytes = list(devs), sb.value
+
+    def solve_device(self, fs, us, streams=None) -> None:
+        """fs[v], us[v]: rank v's (n/P) x n x n CUDA tensors on devices[v] (may alias)."""
+        P = self.nranks
+        numel = (self.n // P) * self.n * self.n
+        if len(fs) != P or len(us) != P:
+            raise ValueError("one shard per rank")
+        for v in range(P):
+            _check_buffer(fs[v], numel, self.precision // 8, f"shard f[{v}]", self.devices[v])
+            _check_buffer(us[v], numel, self.precision // 8, f"shard u[{v}]", self.devices[v])
+        fa = (_vp * P)(*[_ptr(x) for x in fs])
+        ua = (_vp * P)(*[_ptr(x) for x in us])
+        sa = (_vp * P)(*[int(x) for x in streams]) if streams is not None else None
+        _check(lib.arena_mgpu_solve_device(self._m, fa, ua, sa), "arena_mgpu_solve_device")
+
+    def solve_host(self, f, u) -> None:
+        """Whole n^3 host field in, whole field out (synchronous)."""
+        n3 = self.n ** 3
+        _check_buffer(f, n3, self.precision // 8, "solve_host f")
+        _check_buffer(u, n3, self.precision // 8, "solve_host u")
+        _check(lib.arena_mgpu_solve_host(self._m, _vp(_ptr(f)), _vp(_ptr(u))), "arena_mgpu_solve_host")
+
+    def close(self) -> None:
+        if getattr(self, "_m", None) and self._m.value:
+            lib.arena_mgpu_destroy(self._m)
+            self._m = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def slab_exchange_pieces(n: int, nranks: int, forward: bool, lo: int, hi: int):
+    """Host-only: in-chunk row ranges [(first, rows), ...] that one sub-step [lo, hi) of the
+    slab's chunked all-to-all moves between every pair of ranks (include/arena_fft.h)."""
+    first = (ctypes.c_size_t * 4096)()
+    rows = (ctypes.c_size_t * 4096)()
+    k = lib.arena_slab_exchange_pieces(int(n), int(nranks), int(bool(forward)), int(lo), int(hi), first, rows, 4096)
+    if k < 0:
+        raise ValueError("bad exchange sub-step")
+    return [(first[i], rows[i]) for i in range(k)]
 
 
 def nccl_unique_id() -> bytes:
@@ -591,7 +684,7 @@ def source_gaussian(n: int, alpha: float, center, which: int, out, precision: in
 
 
 __all__ = [
-    "Plan", "Slab", "Pencil", "SpectralInterpolant", "nccl_unique_id", "get_plan", "poisson_spectral_solve", "dft3_forward", "dft3_inverse", "signed_freq",
+    "Plan", "Slab", "Pencil", "MultiGPU", "SpectralInterpolant", "nccl_unique_id", "get_plan", "poisson_spectral_solve", "dft3_forward", "dft3_inverse", "signed_freq",
     "source_modes", "source_gaussian", "ArenaError", "lib", "LIB_PATH", "CORE_PATH", "HEADER_PATH",
     "PATH_POW2", "PATH_GENERIC",
 ]

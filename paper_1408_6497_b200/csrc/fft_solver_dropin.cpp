@@ -11,8 +11,12 @@
 //   fftw_execute + scale loop (fft_solver.cpp:65-80)   arena_poisson_solve_host (5 sm_100a kernels)
 //
 // Device selection: the calling thread's current CUDA device, or
-// ARENA_FFT_DEVICE if set.  No CPU fallback: without a B200 every call
-// throws std::runtime_error.
+// ARENA_FFT_DEVICE if set.  ARENA_FFT_NGPU = P > 1 spreads poisson_spectral_solve
+// over P GPUs of this process (arena_mgpu_*: slab v on GPU v, or on the devices
+// listed in ARENA_FFT_DEVICES, e.g. "0,1,2,3"), for power-of-two n >= 16 with
+// n/P >= 4; other sizes use one GPU.  The signature stays the reference's
+// (fft_solver.hpp:23).  No CPU fallback: without a B200 every call throws
+// std::runtime_error.
 #include <algorithm>
 #include <cmath>
 #include <complex>
@@ -42,6 +46,48 @@ namespace {
 struct PlanDeleter {
   void operator()(arena_fft_plan* p) const { arena_fft_plan_destroy(p); }
 };
+struct MgpuDeleter {
+  void operator()(arena_fft_mgpu* m) const { arena_mgpu_destroy(m); }
+};
+
+int selected_ngpu(int n) {
+  const char* s = std::getenv("ARENA_FFT_NGPU");
+  const int P = s ? std::atoi(s) : 1;
+  if (P <= 1 || P > 8 || (P & (P - 1))) return 1;
+  if (n < 16 || (n & (n - 1)) || n % P || n / P < 4) return 1;
+  return P;
+}
+
+std::vector<int> selected_devices(int P) {
+  std::vector<int> d;
+  if (const char* s = std::getenv("ARENA_FFT_DEVICES")) {
+    std::string v(s);
+    size_t pos = 0;
+    while (pos < v.size() && int(d.size()) < P) {
+      const size_t c = v.find(',', pos);
+      d.push_back(std::atoi(v.substr(pos, c == std::string::npos ? std::string::npos : c - pos).c_str()));
+      if (c == std::string::npos) break;
+      pos = c + 1;
+    }
+  }
+  return int(d.size()) == P ? d : std::vector<int>{};
+}
+
+// (n, P) -> multi-GPU object, created once like the plans.
+arena_fft_mgpu* cached_mgpu(int n, int P) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, std::unique_ptr<arena_fft_mgpu, MgpuDeleter>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(n, P);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second.get();
+  const std::vector<int> dev = selected_devices(P);
+  arena_fft_mgpu* m = nullptr;
+  const arena_status st = arena_mgpu_create(&m, n, 64, P, dev.empty() ? nullptr : dev.data());
+  if (st != ARENA_OK) raise(st, "arena_mgpu_create");
+  cache.emplace(key, std::unique_ptr<arena_fft_mgpu, MgpuDeleter>(m));
+  return m;
+}
 
 int selected_device() {
   if (const char* s = std::getenv("ARENA_FFT_DEVICE")) return std::atoi(s);
@@ -91,7 +137,9 @@ GridField dft3_inverse(const std::vector<std::complex<double>>& spec, int n) {
 GridField poisson_spectral_solve(const GridField& f) {
   GridField u(f.n);  // throws std::invalid_argument for n < 2, as the reference does
   check_grid(f, "poisson_spectral_solve");
-  const arena_status st = arena_poisson_solve_host(cached_plan(f.n), f.data.data(), u.data.data());
+  const int P = selected_ngpu(f.n);
+  const arena_status st = P > 1 ? arena_mgpu_solve_host(cached_mgpu(f.n, P), f.data.data(), u.data.data())
+                                : arena_poisson_solve_host(cached_plan(f.n), f.data.data(), u.data.data());
   if (st != ARENA_OK) raise(st, "poisson_spectral_solve");
   return u;
 }

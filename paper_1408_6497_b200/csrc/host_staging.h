@@ -94,7 +94,8 @@ class Stager {
     }
     delete pool_;
   }
-  cudaError_t init() {
+  // threads: host copy threads of this ring (0: ARENA_FFT_COPY_THREADS or min(8, cores)).
+  cudaError_t init(int threads = 0) {
     cudaError_t e;
     for (int s = 0; s < kSlots; ++s) {
       if ((e = cudaMallocHost(&pin_[s], kChunk)) != cudaSuccess) return e;
@@ -103,6 +104,7 @@ class Stager {
     const unsigned hc = std::thread::hardware_concurrency();
     int nt = int(std::max(1u, std::min(8u, hc ? hc : 1u)));  // B200 box: 8 and 16 threads equal (~35 GB/s)
     if (const char* env = getenv("ARENA_FFT_COPY_THREADS")) nt = std::max(1, atoi(env));
+    if (threads > 0) nt = threads;
     pool_ = new CopyPool(nt);
     return cudaSuccess;
   }

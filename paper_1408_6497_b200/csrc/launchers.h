@@ -4,6 +4,15 @@
 
 #include <cuda_runtime.h>
 
+#ifndef ARENA_JBLOCK
+#define ARENA_JBLOCK 64  // j-block of the half-spectrum layout (see Layout).  B200 A/B (ms per solve,
+                         // JB = 8 / 32 / 64): 1024^3 fp64 16.68 / 16.40 / 16.38 (y passes 3.41 -> 3.19,
+                         // x 4.13 -> 4.23), 512^3 2.007 / 1.957 / 1.945, 2048^3 143.3 / 141.6 / 141.5;
+                         // JB = 4: 16.87, 128: 16.36 fp64 but fp32 worse
+#endif
+// Rows per j block of a half-spectrum layout with nj j lines (poisson_pow2.cuh Layout).
+inline int layout_jb(int nj) { return nj < ARENA_JBLOCK ? nj : ARENA_JBLOCK; }
+
 namespace arena_fft {
 
 constexpr int kPow2MaxN = 2048;
@@ -63,7 +72,10 @@ struct Pow2Args {
   // nullptr = in-place (the exchange is a separate step).
   void* const* peer_y = nullptr;
   void* const* peer_x = nullptr;
-  // Single GPU: quadrant formulation (poisson_quad.cuh), H = n/2-point y / x lines.
+  // Slab chunked exchange: with subn > 0 and phases == kPhaseZY (kPhaseX) only local i
+  // planes (local j lines, whole JB blocks) [sub0, sub0 + subn) are transformed.
+  int sub0 = 0, subn = 0;
+  // Single GPU: 1 = quadrant formulation (poisson_quad.cuh, H = n/2-point y / x lines), 2 = i-split (poisson_hq.cuh).
   int quad = 0;
 };
 enum : int { kFuseFwd = 1, kFuseInv = 2 };

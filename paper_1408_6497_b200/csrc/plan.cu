@@ -7,8 +7,10 @@
 // compiled for (sm_100a); anything else is ARENA_EUNSUPPORTED.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <thread>
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
@@ -427,10 +429,19 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
     // B200 A/B (ms per solve, plain / quadrant): 2048^3 fp64 178 / 148, fp32 95 / 84;
     // 1024^3 17.5 / 18.2; 512^3 fp64 2.10 / 2.01, fp32 1.10 / 1.10; 256^3 0.295 / 0.307.
     // ARENA_FFT_QUAD = 0 | 1 overrides (any n >= 32 with the TMA kernels).
+    // i-split formulation (poisson_hq.cuh): only the i transform's first radix-2 step
+    // moves into the z passes, so the x pass runs n/2-point lines at twice the
+    // occupancy while the y lines keep all n points.  ARENA_FFT_QUAD = hq selects it.
     {
       const char* qz = std::getenv("ARENA_FFT_QUAD");
-      const bool want = qz ? std::string(qz) == "1" : (n >= 2048 || (n == 512 && precision_bits == 64));
-      p->quad = (want && p->tma && n >= 32 && !p->fuse) ? 1 : 0;
+      int want = 0;
+      if (qz) {
+        const std::string v(qz);
+        want = v == "1" ? 1 : (v == "hq" || v == "2") ? 2 : 0;
+      } else {
+        want = (n >= 2048 || (n == 512 && precision_bits == 64)) ? 1 : 0;
+      }
+      p->quad = (want && p->tma && n >= 32 && !p->fuse) ? want : 0;
     }
   } else {
     p->path = ARENA_PATH_GENERIC;
@@ -729,6 +740,8 @@ struct NcclApi {
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;  // optional (hang / error detection)
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   bool ok = false;
 };
 
@@ -752,6 +765,8 @@ NcclApi* nccl_api() {
     api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
     api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    api.CommGetAsyncError = reinterpret_cast<decltype(api.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
+    api.CommAbort = reinterpret_cast<decltype(api.CommAbort)>(sym("ncclCommAbort"));
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GroupStart && api.GroupEnd && api.Send &&
              api.Recv && api.GetErrorString;
   });
@@ -919,6 +934,13 @@ struct arena_fft_slab {
   int xmode = ARENA_XCHG_COPY;  // ARENA_XCHG_PEER: K2 / K3 store into the peers' workspaces
   bool attached = false;        // peer pointers of the other ranks opened (multi-process)
   PeerSync sync;
+  // Chunked COPY exchange (NCCL or loopback copies): the all-to-alls run on comm_st in
+  // sub-steps, each gated by an event after the kernels that produced its rows, so
+  // exchange s overlaps the transform of sub-range s + 1.
+  int chunk_fwd = 1, chunk_bwd = 1;  // sub-steps per direction (1 = the whole chunk at once)
+  cudaStream_t comm_st = nullptr;
+  std::vector<cudaEvent_t> xev;      // chunk_fwd + chunk_bwd + 2 ordering events
+  bool aborted = false;              // NCCL communicator aborted after an error / timeout
   // stage timing (arena_slab_set_stage_timing): kSlabMarks events per solve
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -936,13 +958,15 @@ void free_slab(arena_fft_slab* s) {
   if (s->base) {
     DeviceGuard g(s->base->device);
     for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : s->xev) cudaEventDestroy(e);
+    if (s->comm_st) cudaStreamDestroy(s->comm_st);
     s->sync.release();
     for (SlabRank& r : s->ranks) {
       if (r.B) cudaFree(r.B);
       if (r.C) cudaFree(r.C);
       if (r.ctrs) cudaFree(r.ctrs);
     }
-    if (s->comm) {
+    if (s->comm && !s->aborted) {
       if (NcclApi* a = nccl_api()) a->CommDestroy(s->comm);
     }
   }
@@ -1009,6 +1033,27 @@ arena_status slab_init(arena_fft_slab** out, int n, int prec, int device, int P,
       return nccl_fail(r, "ncclCommInitRank");
     }
   }
+  {
+    // Chunked COPY exchange: ARENA_SLAB_CHUNKS sub-steps per all-to-all (default 4; 1 = whole
+    // chunks after whole passes).  Forward sub-steps split the rank's i planes; backward ones
+    // whole JB blocks of its j lines (the rows of a layout-C chunk are contiguous per block).
+    int want = 4;
+    if (const char* c = std::getenv("ARENA_SLAB_CHUNKS")) want = std::max(1, std::atoi(c));
+    const int JB = layout_jb(s->nj);
+    s->chunk_fwd = std::min(want, s->ni);
+    s->chunk_bwd = std::min(want, s->nj / JB);
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&s->comm_st, cudaStreamNonBlocking)) != cudaSuccess) {
+      free_slab(s);
+      return cuda_fail(e, "slab exchange stream");
+    }
+    s->xev.resize(size_t(s->ni + s->nj / JB + 2), nullptr);  // enough for any chunking
+    for (cudaEvent_t& x : s->xev)
+      if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) {
+        free_slab(s);
+        return cuda_fail(e, "slab exchange events");
+      }
+  }
   *out = s;
   return ARENA_OK;
 }
@@ -1019,8 +1064,11 @@ Pow2Args slab_args(arena_fft_slab* s, SlabRank& r, int rank, const void* f, void
                   s->ni, s->nj, s->P, rank * s->nj, r.C, phases, r.ctrs, p->lag, p->fuse};
 }
 
-cudaError_t slab_phase(arena_fft_slab* s, SlabRank& r, int rank, const void* f, void* u, cudaStream_t st, int phases) {
+cudaError_t slab_phase(arena_fft_slab* s, SlabRank& r, int rank, const void* f, void* u, cudaStream_t st, int phases,
+                       int sub0 = 0, int subn = 0) {
   Pow2Args a = slab_args(s, r, rank, f, u, st, phases);
+  a.sub0 = sub0;
+  a.subn = subn;
   if (s->xmode == ARENA_XCHG_PEER) {
     a.peer_y = r.peerC;
     a.peer_x = r.peerB;
@@ -1039,6 +1087,61 @@ void slab_fill_loopback_peers(arena_fft_slab* s) {
 }
 
 arena_status slab_peer_barrier(arena_fft_slab* s, cudaStream_t st) { return s->sync.barrier(st, s->rank, s->P); }
+
+// In-chunk row ranges {first row, rows} that sub-step [lo, hi) of an exchange moves:
+// forward — local i planes [lo, hi) of a layout-B chunk, one range per JB block of j
+// (row (jb ni + il) JB + jl % JB); backward — local j lines [lo, hi) (whole JB blocks) of
+// a layout-C chunk, one contiguous range.  Chunk d of B and chunk r of C share the
+// in-chunk order, so the same ranges serve the sender and the receiver.
+void slab_piece_rows(int ni, int nj, bool forward, int lo, int hi, std::vector<std::pair<size_t, size_t>>& out) {
+  const int JB = layout_jb(nj);
+  out.clear();
+  if (forward) {
+    for (int jb = 0; jb < nj / JB; ++jb) out.emplace_back((size_t(jb) * ni + lo) * JB, size_t(hi - lo) * JB);
+  } else {
+    out.emplace_back(size_t(lo / JB) * ni * JB, size_t((hi - lo) / JB) * ni * JB);
+  }
+}
+
+// One sub-step of a chunked exchange on stream st (every rank's rows [lo, hi)).
+arena_status slab_exchange_sub(arena_fft_slab* s, cudaStream_t st, bool forward, int lo, int hi) {
+  std::vector<std::pair<size_t, size_t>> pcs;
+  slab_piece_rows(s->ni, s->nj, forward, lo, hi, pcs);
+  const size_t rowb = size_t(s->base->ncp) * 2 * s->base->elem;
+  const size_t chunk_rows = size_t(s->ni) * s->nj;
+  if (s->loopback) {
+    for (int r = 0; r < s->P; ++r)
+      for (int d = 0; d < s->P; ++d) {
+        const char* src = static_cast<const char*>(forward ? s->ranks[r].B : s->ranks[r].C) + d * chunk_rows * rowb;
+        char* dst = static_cast<char*>(forward ? s->ranks[d].C : s->ranks[d].B) + r * chunk_rows * rowb;
+        for (const auto& pc : pcs) {
+          cudaError_t e = cudaMemcpyAsync(dst + pc.first * rowb, src + pc.first * rowb, pc.second * rowb,
+                                          cudaMemcpyDeviceToDevice, st);
+          if (e != cudaSuccess) return cuda_fail(e, "loopback exchange");
+        }
+      }
+    return ARENA_OK;
+  }
+  NcclApi* a = nccl_api();
+  if (s->aborted) return fail(ARENA_ENCCL, "the slab's NCCL communicator was aborted");
+  const ncclDataType_t dt = s->base->prec == 64 ? ncclFloat64 : ncclFloat32;
+  const size_t elems_per_row = size_t(s->base->ncp) * 2;
+  SlabRank& me = s->ranks[0];
+  const char* src = static_cast<const char*>(forward ? me.B : me.C);
+  char* dst = static_cast<char*>(forward ? me.C : me.B);
+  ncclResult_t res = a->GroupStart();
+  if (res != ncclSuccess) return nccl_fail(res, "ncclGroupStart");
+  for (int d = 0; d < s->P; ++d)
+    for (const auto& pc : pcs) {
+      const size_t off = (d * chunk_rows + pc.first) * rowb;
+      if ((res = a->Send(src + off, pc.second * elems_per_row, dt, d, s->comm, st)) != ncclSuccess)
+        return nccl_fail(res, "ncclSend");
+      if ((res = a->Recv(dst + off, pc.second * elems_per_row, dt, d, s->comm, st)) != ncclSuccess)
+        return nccl_fail(res, "ncclRecv");
+    }
+  if ((res = a->GroupEnd()) != ncclSuccess) return nccl_fail(res, "ncclGroupEnd");
+  return ARENA_OK;
+}
 
 // All-to-all between workspaces: forward (B chunk d of rank r -> C chunk r of rank d)
 // or backward (C chunk d of rank r -> B chunk r of rank d).
@@ -1157,12 +1260,64 @@ static cudaEvent_t* slab_timing_events(arena_fft_slab* s) {
   return s->ev_pool.data() + size_t(s->ev_sets++) * kSlabMarks;
 }
 
+// Kernels of one phase over every (virtual) rank, restricted to a sub-range when subn > 0.
+static arena_status slab_kernels_sub(arena_fft_slab* s, int phases, int sub0, int subn, const void* d_f, void* d_u,
+                                     cudaStream_t st) {
+  const size_t slab_bytes = size_t(s->ni) * s->n * s->n * s->base->elem;
+  for (int v = 0; v < int(s->ranks.size()); ++v) {
+    const int rank = s->loopback ? v : s->rank;
+    const char* f = static_cast<const char*>(d_f) + (s->loopback ? size_t(v) * slab_bytes : 0);
+    char* u = static_cast<char*>(d_u) + (s->loopback ? size_t(v) * slab_bytes : 0);
+    cudaError_t e = slab_phase(s, s->ranks[v], rank, f, u, st, phases, sub0, subn);
+    if (e != cudaSuccess) return cuda_fail(e, "slab sub-range kernels");
+  }
+  return ARENA_OK;
+}
+
+// COPY exchange, chunked: the transform of sub-range k+1 overlaps the all-to-all of
+// sub-range k, which runs on the slab's exchange stream gated by an event.
+static arena_status slab_solve_chunked(arena_fft_slab* s, const void* d_f, void* d_u, cudaStream_t st,
+                                       cudaEvent_t* ev) {
+  const int cf = s->chunk_fwd, cb = s->chunk_bwd;
+  const int JB = layout_jb(s->nj), nb = s->nj / JB;
+  cudaEvent_t* x = s->xev.data();
+  arena_status stt;
+  if (ev) cudaEventRecord(ev[0], st);
+  for (int k = 0; k < cf; ++k) {
+    const int lo = k * s->ni / cf, hi = (k + 1) * s->ni / cf;
+    if ((stt = slab_kernels_sub(s, kPhaseZY, lo, hi - lo, d_f, d_u, st)) != ARENA_OK) return stt;
+    cudaEventRecord(x[k], st);
+    cudaStreamWaitEvent(s->comm_st, x[k], 0);
+    if ((stt = slab_exchange_sub(s, s->comm_st, true, lo, hi)) != ARENA_OK) return stt;
+  }
+  if (ev) cudaEventRecord(ev[1], st);
+  cudaEventRecord(x[cf + cb], s->comm_st);
+  cudaStreamWaitEvent(st, x[cf + cb], 0);
+  if (ev) cudaEventRecord(ev[2], st);
+  for (int k = 0; k < cb; ++k) {
+    const int lo = (k * nb / cb) * JB, hi = ((k + 1) * nb / cb) * JB;
+    if ((stt = slab_kernels_sub(s, kPhaseX, lo, hi - lo, d_f, d_u, st)) != ARENA_OK) return stt;
+    cudaEventRecord(x[cf + k], st);
+    cudaStreamWaitEvent(s->comm_st, x[cf + k], 0);
+    if ((stt = slab_exchange_sub(s, s->comm_st, false, lo, hi)) != ARENA_OK) return stt;
+  }
+  if (ev) cudaEventRecord(ev[3], st);
+  cudaEventRecord(x[cf + cb + 1], s->comm_st);
+  cudaStreamWaitEvent(st, x[cf + cb + 1], 0);
+  if (ev) cudaEventRecord(ev[4], st);
+  if ((stt = slab_run_kernels(s, 2, d_f, d_u, st)) != ARENA_OK) return stt;
+  if (ev) cudaEventRecord(ev[5], st);
+  return ARENA_OK;
+}
+
 arena_status arena_slab_solve_device(arena_fft_slab* s, const void* d_f, void* d_u, void* stream) {
   if (!s || !d_f || !d_u) return fail(ARENA_EINVAL, "NULL slab or buffer");
   DeviceGuard g(s->base->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool barrier = s->xmode == ARENA_XCHG_PEER && !s->loopback && s->P > 1;
   cudaEvent_t* ev = slab_timing_events(s);
+  if (s->xmode != ARENA_XCHG_PEER && (s->chunk_fwd > 1 || s->chunk_bwd > 1) && !s->base->ctrs)
+    return slab_solve_chunked(s, d_f, d_u, st, ev);
   for (int phase = 0; phase < 3; ++phase) {
     if (ev) cudaEventRecord(ev[2 * phase], st);
     arena_status stt = slab_run_kernels(s, phase, d_f, d_u, st);
@@ -1173,6 +1328,74 @@ arena_status arena_slab_solve_device(arena_fft_slab* s, const void* d_f, void* d
     else if (barrier) stt = slab_peer_barrier(s, st);
     if (stt != ARENA_OK) return stt;
   }
+  return ARENA_OK;
+}
+
+arena_status arena_slab_set_chunking(arena_fft_slab* s, int fwd, int bwd) {
+  if (!s || fwd < 1 || bwd < 1) return fail(ARENA_EINVAL, "bad slab chunking");
+  const int JB = layout_jb(s->nj);
+  if (fwd > s->ni || bwd > s->nj / JB) return fail(ARENA_EINVAL, "more sub-steps than the slab has planes / j blocks");
+  s->chunk_fwd = fwd;
+  s->chunk_bwd = bwd;
+  return ARENA_OK;
+}
+
+arena_status arena_slab_get_chunking(const arena_fft_slab* s, int* fwd, int* bwd) {
+  if (!s) return fail(ARENA_EINVAL, "slab is NULL");
+  if (fwd) *fwd = s->chunk_fwd;
+  if (bwd) *bwd = s->chunk_bwd;
+  return ARENA_OK;
+}
+
+int arena_slab_exchange_pieces(int n, int nranks, int forward, int lo, int hi, size_t* first, size_t* rows, int max) {
+  if (n < 4 || nranks < 1 || n % nranks) return -1;
+  const int ni = n / nranks, nj = n / nranks;
+  const int JB = layout_jb(nj);
+  const int lim = forward ? ni : nj;
+  if (lo < 0 || hi > lim || lo >= hi || (!forward && (lo % JB || hi % JB))) return -1;
+  std::vector<std::pair<size_t, size_t>> pcs;
+  slab_piece_rows(ni, nj, forward != 0, lo, hi, pcs);
+  for (int k = 0; k < int(pcs.size()) && k < max; ++k) {
+    if (first) first[k] = pcs[k].first;
+    if (rows) rows[k] = pcs[k].second;
+  }
+  return int(pcs.size());
+}
+
+// Wait for a solve enqueued on `stream` (and the slab's exchange stream) with NCCL
+// error / hang detection: polls ncclCommGetAsyncError and aborts the communicator
+// after timeout_s, instead of blocking forever on a stuck peer.
+arena_status arena_slab_wait(arena_fft_slab* s, void* stream, double timeout_s) {
+  if (!s) return fail(ARENA_EINVAL, "slab is NULL");
+  DeviceGuard g(s->base->device);
+  NcclApi* a = s->comm ? nccl_api() : nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    cudaError_t q1 = cudaStreamQuery(static_cast<cudaStream_t>(stream));
+    cudaError_t q2 = s->comm_st ? cudaStreamQuery(s->comm_st) : cudaSuccess;
+    if (q1 == cudaSuccess && q2 == cudaSuccess) break;
+    if (q1 != cudaSuccess && q1 != cudaErrorNotReady) return cuda_fail(q1, "slab solve");
+    if (q2 != cudaSuccess && q2 != cudaErrorNotReady) return cuda_fail(q2, "slab exchange");
+    if (a && a->CommGetAsyncError && !s->aborted) {
+      ncclResult_t r = ncclSuccess;
+      if (a->CommGetAsyncError(s->comm, &r) == ncclSuccess && r != ncclSuccess && r != ncclInProgress) {
+        if (a->CommAbort) a->CommAbort(s->comm);
+        s->aborted = true;
+        return nccl_fail(r, "NCCL asynchronous error (communicator aborted)");
+      }
+    }
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > timeout_s) {
+      if (a && a->CommAbort && !s->aborted) {
+        a->CommAbort(s->comm);
+        s->aborted = true;
+      }
+      return fail(ARENA_ENCCL, "slab solve did not complete within " + std::to_string(timeout_s) +
+                                   " s (a peer is stuck or gone); NCCL communicator aborted");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  if (s->xmode == ARENA_XCHG_PEER && !s->loopback) return s->sync.status();
   return ARENA_OK;
 }
 
@@ -1301,6 +1524,227 @@ arena_status arena_peer_barrier_selftest(int device, int nranks, int rounds, int
   cudaFree(dbad);
   if (e != cudaSuccess) return cuda_fail(e, "barrier self-test");
   return herr ? fail(ARENA_ECUDA, "barrier self-test timed out") : ARENA_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================
+// One process, P GPUs (the drop-in's multi-GPU path, ARENA_FFT_NGPU): rank v = a
+// slab rank on devices[v] holding planes [v n/P, (v+1) n/P).  Its K2 / K3 store the
+// exchange chunks straight into the other ranks' workspaces through peer access
+// (cudaDeviceEnablePeerAccess: NVLink on a B200 box), exactly the peer-exchange
+// kernels of the multi-process slab, and the phases are ordered by cross-device
+// events instead of a device flag barrier (all ranks' streams belong to this
+// process).  The host path moves the P slabs of a GridField over P PCIe links in
+// parallel (one host thread and one staging ring per GPU).
+struct arena_fft_mgpu {
+  int n = 0, P = 1, prec = 64;
+  size_t elem = 8, slab_bytes = 0;
+  std::vector<int> dev;
+  std::vector<arena_fft_slab*> sl;
+  std::vector<cudaStream_t> st;
+  std::vector<cudaEvent_t> ev;  // 2 * P: after phase 0 / 1 of each rank
+  std::vector<void*> fbuf;      // host path: each rank's real slab (solved in place)
+  std::vector<Stager*> stg;
+  std::mutex mu;
+};
+
+namespace {
+
+void free_mgpu(arena_fft_mgpu* m) {
+  if (!m) return;
+  for (int v = 0; v < int(m->sl.size()); ++v) {
+    DeviceGuard g(m->dev[v]);
+    if (v < int(m->fbuf.size()) && m->fbuf[v]) cudaFree(m->fbuf[v]);
+    if (v < int(m->stg.size())) delete m->stg[v];
+    if (v < int(m->st.size()) && m->st[v]) cudaStreamDestroy(m->st[v]);
+    for (int ph = 0; ph < 2; ++ph) {
+      const size_t k = size_t(ph) * m->P + v;
+      if (k < m->ev.size() && m->ev[k]) cudaEventDestroy(m->ev[k]);
+    }
+    m->sl[v]->attached = false;  // peer pointers are plain device pointers here: nothing to close
+    free_slab(m->sl[v]);
+  }
+  delete m;
+}
+
+arena_status mgpu_enqueue(arena_fft_mgpu* m, const void* const* f, void* const* u, const cudaStream_t* st) {
+  for (int phase = 0; phase < 3; ++phase) {
+    for (int v = 0; v < m->P; ++v) {
+      DeviceGuard g(m->dev[v]);
+      arena_status stt = slab_run_kernels(m->sl[v], phase, f[v], u[v], st[v]);
+      if (stt != ARENA_OK) return stt;
+      if (phase < 2 && cudaEventRecord(m->ev[size_t(phase) * m->P + v], st[v]) != cudaSuccess)
+        return fail(ARENA_ECUDA, "multi-GPU phase event");
+    }
+    if (phase == 2) break;
+    // every rank's next phase reads what every rank's previous phase stored into it
+    for (int w = 0; w < m->P; ++w) {
+      DeviceGuard g(m->dev[w]);
+      for (int v = 0; v < m->P; ++v)
+        if (cudaStreamWaitEvent(st[w], m->ev[size_t(phase) * m->P + v], 0) != cudaSuccess)
+          return fail(ARENA_ECUDA, "multi-GPU cross-device wait");
+    }
+  }
+  return ARENA_OK;
+}
+
+cudaError_t mgpu_copy(arena_fft_mgpu* m, int v, void* dst, const void* src, size_t bytes, bool to_host) {
+  const void* host = to_host ? dst : src;
+  if (host_ptr_pinned(host)) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice,
+                                    m->st[v]);
+    return (e || !to_host) ? e : cudaStreamSynchronize(m->st[v]);
+  }
+  if (!m->stg[v]) {
+    m->stg[v] = new (std::nothrow) Stager;
+    if (!m->stg[v]) return cudaErrorMemoryAllocation;
+    cudaError_t e = m->stg[v]->init(std::max(2, 16 / m->P));
+    if (e != cudaSuccess) {
+      delete m->stg[v];
+      m->stg[v] = nullptr;
+      return e;
+    }
+  }
+  return to_host ? m->stg[v]->d2h(dst, src, bytes, m->st[v]) : m->stg[v]->h2d(dst, src, bytes, m->st[v]);
+}
+
+}  // namespace
+
+extern "C" {
+
+arena_status arena_mgpu_create(arena_fft_mgpu** out, int n, int precision_bits, int nranks, const int* devices) {
+  if (!out) return fail(ARENA_EINVAL, "multi-GPU pointer is NULL");
+  *out = nullptr;
+  if (nranks < 1 || nranks > kMaxPeers) return fail(ARENA_EUNSUPPORTED, "1 to 8 GPUs per process");
+  if (!is_pow2(n) || n < 16 || n % nranks || n / nranks < 4)
+    return fail(ARENA_EUNSUPPORTED, "multi-GPU path needs a power-of-two n >= 16 with n / P >= 4");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(ARENA_EUNSUPPORTED, "no CUDA device visible (this library has no CPU path)");
+  arena_fft_mgpu* m = new (std::nothrow) arena_fft_mgpu;
+  if (!m) return fail(ARENA_ENOMEM, "multi-GPU object");
+  m->n = n;
+  m->P = nranks;
+  m->prec = precision_bits;
+  m->elem = precision_bits == 64 ? 8 : 4;
+  m->slab_bytes = size_t(n / nranks) * n * n * m->elem;
+  for (int v = 0; v < nranks; ++v) m->dev.push_back(devices ? devices[v] : v % ndev);
+  for (int v = 0; v < nranks; ++v) {
+    if (m->dev[v] < 0 || m->dev[v] >= ndev) {
+      free_mgpu(m);
+      return fail(ARENA_EINVAL, "device ordinal out of range");
+    }
+    arena_fft_slab* s = nullptr;
+    arena_status st = slab_init(&s, n, precision_bits, m->dev[v], nranks, v, 0, nullptr);
+    if (st != ARENA_OK) {
+      free_mgpu(m);
+      return st;
+    }
+    m->sl.push_back(s);
+  }
+  // peer access between every pair of distinct devices
+  for (int v = 0; v < nranks; ++v)
+    for (int d = 0; d < nranks; ++d) {
+      if (m->dev[v] == m->dev[d]) continue;
+      DeviceGuard g(m->dev[v]);
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, m->dev[v], m->dev[d]);
+      if (!can) {
+        free_mgpu(m);
+        return fail(ARENA_EUNSUPPORTED, "no peer access between devices " + std::to_string(m->dev[v]) + " and " +
+                                            std::to_string(m->dev[d]));
+      }
+      cudaError_t e = cudaDeviceEnablePeerAccess(m->dev[d], 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        free_mgpu(m);
+        return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      }
+    }
+  const size_t cb = m->sl[0]->chunk_elems * m->elem;
+  for (int v = 0; v < nranks; ++v) {
+    SlabRank& me = m->sl[v]->ranks[0];
+    for (int d = 0; d < nranks; ++d) {
+      me.peerB[d] = static_cast<char*>(m->sl[d]->ranks[0].B) + size_t(v) * cb;
+      me.peerC[d] = static_cast<char*>(m->sl[d]->ranks[0].C) + size_t(v) * cb;
+    }
+    m->sl[v]->attached = true;
+    m->sl[v]->xmode = ARENA_XCHG_PEER;
+  }
+  m->st.assign(nranks, nullptr);
+  m->ev.assign(size_t(2) * nranks, nullptr);
+  m->fbuf.assign(nranks, nullptr);
+  m->stg.assign(nranks, nullptr);
+  for (int v = 0; v < nranks; ++v) {
+    DeviceGuard g(m->dev[v]);
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&m->st[v], cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&m->ev[v], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&m->ev[size_t(nranks) + v], cudaEventDisableTiming)) != cudaSuccess) {
+      free_mgpu(m);
+      return cuda_fail(e, "multi-GPU streams / events");
+    }
+  }
+  *out = m;
+  g_last_error.clear();
+  return ARENA_OK;
+}
+
+void arena_mgpu_destroy(arena_fft_mgpu* m) { free_mgpu(m); }
+
+arena_status arena_mgpu_info(const arena_fft_mgpu* m, int* nranks, int* devices, size_t* slab_bytes) {
+  if (!m) return fail(ARENA_EINVAL, "multi-GPU object is NULL");
+  if (nranks) *nranks = m->P;
+  if (devices)
+    for (int v = 0; v < m->P; ++v) devices[v] = m->dev[v];
+  if (slab_bytes) *slab_bytes = m->slab_bytes;
+  return ARENA_OK;
+}
+
+arena_status arena_mgpu_solve_device(arena_fft_mgpu* m, const void* const* f, void* const* u, void* const* streams) {
+  if (!m || !f || !u) return fail(ARENA_EINVAL, "NULL multi-GPU object or shard list");
+  for (int v = 0; v < m->P; ++v)
+    if (!f[v] || !u[v]) return fail(ARENA_EINVAL, "NULL shard");
+  std::lock_guard<std::mutex> lk(m->mu);
+  std::vector<cudaStream_t> st(m->P);
+  for (int v = 0; v < m->P; ++v) st[v] = streams ? static_cast<cudaStream_t>(streams[v]) : m->st[v];
+  return mgpu_enqueue(m, f, u, st.data());
+}
+
+arena_status arena_mgpu_solve_host(arena_fft_mgpu* m, const void* f, void* u) {
+  if (!m || !f || !u) return fail(ARENA_EINVAL, "NULL multi-GPU object or buffer");
+  std::lock_guard<std::mutex> lk(m->mu);
+  for (int v = 0; v < m->P; ++v) {
+    if (m->fbuf[v]) continue;
+    DeviceGuard g(m->dev[v]);
+    if (cudaMalloc(&m->fbuf[v], m->slab_bytes) != cudaSuccess)
+      return fail(ARENA_ENOMEM, "multi-GPU slab buffer (" + std::to_string(m->slab_bytes) + " B)");
+  }
+  // P slabs over P links at once: one host thread per GPU
+  std::vector<cudaError_t> err(m->P, cudaSuccess);
+  auto par = [&](bool to_host) {
+    std::vector<std::thread> th;
+    for (int v = 0; v < m->P; ++v)
+      th.emplace_back([&, v] {
+        cudaSetDevice(m->dev[v]);
+        const size_t off = size_t(v) * m->slab_bytes;
+        err[v] = to_host ? mgpu_copy(m, v, static_cast<char*>(u) + off, m->fbuf[v], m->slab_bytes, true)
+                         : mgpu_copy(m, v, m->fbuf[v], static_cast<const char*>(f) + off, m->slab_bytes, false);
+      });
+    for (auto& t : th) t.join();
+    for (cudaError_t e : err)
+      if (e != cudaSuccess) return e;
+    return cudaSuccess;
+  };
+  cudaError_t e = par(false);
+  if (e != cudaSuccess) return cuda_fail(e, "multi-GPU H2D");
+  std::vector<const void*> fs(m->fbuf.begin(), m->fbuf.end());
+  arena_status st = mgpu_enqueue(m, fs.data(), m->fbuf.data(), m->st.data());
+  if (st != ARENA_OK) return st;
+  if ((e = par(true)) != cudaSuccess) return cuda_fail(e, "multi-GPU D2H");
+  return ARENA_OK;
 }
 
 }  // extern "C"

@@ -75,12 +75,6 @@ __host__ __device__ constexpr int pow2_floor(int x) { return x <= 1 ? 1 : 2 * po
 #ifndef ARENA_SMS
 #define ARENA_SMS 148  // B200 SM count (sets the prefetch distance of the z passes)
 #endif
-#ifndef ARENA_JBLOCK
-#define ARENA_JBLOCK 64  // j-block of the half-spectrum layout (see Layout).  B200 A/B (ms per solve,
-                         // JB = 8 / 32 / 64): 1024^3 fp64 16.68 / 16.40 / 16.38 (y passes 3.41 -> 3.19,
-                         // x 4.13 -> 4.23), 512^3 2.007 / 1.957 / 1.945, 2048^3 143.3 / 141.6 / 141.5;
-                         // JB = 4: 16.87, 128: 16.36 fp64 but fp32 worse
-#endif
 
 
 // ------------------------------------------------------------ configuration
@@ -558,6 +552,8 @@ __host__ __device__ constexpr int tma_ib(int ni) { return ni < 256 ? ni : 256; }
 // k chunk.
 struct KSpan {
   int kc, kq, k0;
+  int no = 0;  // lines (outer index) to transform, 0 = all of the layout's (sub-range launches of the
+               // slab's chunked exchange pass a shifted base and the sub-range's count)
 };
 
 // Chunked ("split") layouts of the single-GPU path, selected by the SPL template
@@ -631,7 +627,7 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
   constexpr int NBUF = C::NBUF;
   const int KT = (ks.kc + L - 1) / L;
   const size_t kq = size_t(ks.kq);
-  const int NL = (PASS < 2 ? g.ni : g.nj) * KT;  // tiles per chunk (QUAD) / in all
+  const int NL = (ks.no ? ks.no : (PASS < 2 ? g.ni : g.nj)) * KT;  // tiles per chunk (QUAD) / in all
   const int NT = NL * NCH;
   constexpr bool TWS = PASS == 2 ? bool(ARENA_TMA_TWSMEM_X) : bool(ARENA_TMA_TWSMEM_Y);
   V* bufs = smem_base<V>();

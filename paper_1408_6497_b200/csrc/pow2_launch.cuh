@@ -9,6 +9,7 @@
 
 #include "launchers.h"
 #include "poisson_fused.cuh"
+#include "poisson_hq.cuh"
 #include "poisson_quad.cuh"
 #include "poisson_split3.cuh"
 
@@ -58,10 +59,12 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 #define ARENA_TMA_PROMO 0  // L2 promotion of the TMA boxes: 0 none, 1 64B, 2 128B, 3 256B
 #endif
 // TMA descriptor of a workspace in Layout g (5-D, see k_strided_tma).
+// ni_count / njb_count (0 = all): a sub-range view for the slab's chunked exchange —
+// `spec` already advanced to the sub-range, strides those of the full layout g.
 template <typename T, int N>
 cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool ybox, int kc = N / 2 + 1,
                        int kq = spec_pitch(N), int ly = TmaCfg<T, N, true>::L, bool one_chunk = false,
-                       int lx = TmaCfg<T, N, false, x_wide<T, false>()>::L) {
+                       int lx = TmaCfg<T, N, false, x_wide<T, false>()>::L, int ni_count = 0, int njb_count = 0) {
   const int LX = lx;
   const int LY = ly;
   auto enc = tensor_map_encoder();
@@ -69,8 +72,8 @@ cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool
   const CUtensorMapDataType dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const cuuint64_t row = cuuint64_t(kq) * 2 * sizeof(T);
   const int JB = 1 << g.jbs;
-  const cuuint64_t dims[5] = {cuuint64_t(2 * kc), cuuint64_t(JB), cuuint64_t(g.ni), cuuint64_t(g.nj / JB),
-                              cuuint64_t(nchunks)};
+  const cuuint64_t dims[5] = {cuuint64_t(2 * kc), cuuint64_t(JB), cuuint64_t(ni_count ? ni_count : g.ni),
+                              cuuint64_t(njb_count ? njb_count : g.nj / JB), cuuint64_t(nchunks)};
   const cuuint64_t strides[4] = {row, row * JB, row * JB * g.ni, row * g.ni * g.nj};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   cuuint32_t box[5];
@@ -109,7 +112,7 @@ cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* 
   if (po) pov = *po;
   int per_sm = 1;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, SMEM))) return e;
-  const int tiles = (PASS < 2 ? g.ni : g.nj) * ((ks.kc + C::L - 1) / C::L) * spl_chunks(SPL);
+  const int tiles = (ks.no ? ks.no : (PASS < 2 ? g.ni : g.nj)) * ((ks.kc + C::L - 1) / C::L) * spl_chunks(SPL);
   int grid = a.sm_count * (per_sm > 0 ? per_sm : 1);
   if (grid > tiles) grid = tiles;
   // stage twiddles of N-point lines: table `which` 1 (N = n), 0 (N = n/2: quadrant / split lines)
@@ -175,7 +178,7 @@ cudaError_t launch_quad(const Pow2Args& a) {
     const Layout gq = make_layout(H, H);
     const KSpan ks{NR / 2 + 1, spec_pitch(NR), 0};
     TmaCache* c = a.tma;
-    if (c->specB != a.spec || c->specC != a.spec || c->n != NR || c->nchunks != 4 || !c->quad) {
+    if (c->specB != a.spec || c->specC != a.spec || c->n != NR || c->nchunks != 4 || c->quad != 1) {
       if ((e = encode_map<T, H>(c->maps[0], a.spec, gq, 4, true, ks.kc, ks.kq, TmaCfg<T, H, true>::L, true))) return e;
       if ((e = encode_map<T, H>(c->maps[1], a.spec, gq, 4, false, ks.kc, ks.kq, TmaCfg<T, H, true>::L, false,
                                 TmaCfg<T, H, false, x_wide<T, true>()>::L)))
@@ -212,6 +215,68 @@ cudaError_t launch_quad(const Pow2Args& a) {
       mark(a, mk++);
       k_zinv_quad<T, NR><<<qgrid, QC::THREADS, QC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw,
                                                                      stw_ptr<T>(a, 0, QC::E), gq);
+      mark(a, mk++);
+    }
+    return cudaGetLastError();
+  }
+}
+
+// Single-GPU i-split path (poisson_hq.cuh): K1h, the n-point y passes and the
+// H-point x pass on the two i-parity chunks, K5h.
+constexpr int kTmaTagHq = 102;  // TmaCache::quad tag of the i-split maps
+template <typename T, int NR>
+cudaError_t launch_hq(const Pow2Args& a) {
+  if constexpr (!(HqZCfg<T, NR>::OK && NR >= 16)) {
+    return cudaErrorNotSupported;
+  } else {
+    constexpr int H = NR / 2;
+    using V = vec2_t<T>;
+    using ZC = HqZCfg<T, NR>;
+    cudaError_t e;
+    if (!a.tma || a.nchunks != 1 || a.specC != a.spec || a.ni != NR || a.nj != NR) return cudaErrorNotSupported;
+    if (a.ncp != spec_pitch(NR) || a.nc != NR / 2 + 1) return cudaErrorInvalidValue;
+    if ((e = ensure_smem<k_zfwd_hq<T, NR>>(ZC::SMEM, ZC::THREADS))) return e;
+    if ((e = ensure_smem<k_zinv_hq<T, NR>>(ZC::SMEM, ZC::THREADS))) return e;
+    const Layout gh = make_layout(H, NR);
+    const KSpan ks{NR / 2 + 1, spec_pitch(NR), 0};
+    TmaCache* c = a.tma;
+    if (c->specB != a.spec || c->specC != a.spec || c->n != NR || c->nchunks != 2 || c->quad != kTmaTagHq) {
+      if ((e = encode_map<T, NR>(c->maps[0], a.spec, gh, 2, true, ks.kc, ks.kq, TmaCfg<T, NR, true>::L, true))) return e;
+      if ((e = encode_map<T, H>(c->maps[1], a.spec, gh, 2, false, ks.kc, ks.kq, TmaCfg<T, H, true>::L, false,
+                                TmaCfg<T, H, false, x_wide<T, true>()>::L)))
+        return e;
+      c->specB = c->specC = a.spec;
+      c->n = NR;
+      c->ni = H;
+      c->nj = NR;
+      c->nchunks = 2;
+      c->quad = kTmaTagHq;
+    }
+    const CUtensorMap* my = reinterpret_cast<const CUtensorMap*>(c->maps[0]);
+    const CUtensorMap* mx = reinterpret_cast<const CUtensorMap*>(c->maps[1]);
+    const T scale = T(1.0 / (double(NR) * NR * NR));  // fft_solver.cpp:67
+    const T four_pi2 = T(4.0 * M_PI * M_PI);           // fft_solver.cpp:66
+    const V* tw = static_cast<const V*>(a.tw);
+    V* S = static_cast<V*>(a.spec);
+    const unsigned zgrid = unsigned(H) * NR;
+    int mk = 0;
+    if (a.phases & kPhaseZY) {
+      mark(a, mk++);
+      k_zfwd_hq<T, NR><<<zgrid, ZC::THREADS, ZC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw,
+                                                                   stw_ptr<T>(a, 0, ZC::E));
+      mark(a, mk++);
+      if ((e = launch_strided_tma<T, NR, 0, false, false, kSplitI>(a, *my, a.spec, gh, scale, four_pi2, ks))) return e;
+    }
+    if (a.phases & kPhaseX) {
+      mark(a, mk++);
+      if ((e = launch_strided_tma<T, H, 2, false, true, kSplitI>(a, *mx, a.spec, gh, scale, four_pi2, ks))) return e;
+    }
+    if (a.phases & kPhaseYZ) {
+      mark(a, mk++);
+      if ((e = launch_strided_tma<T, NR, 1, false, false, kSplitI>(a, *my, a.spec, gh, scale, four_pi2, ks))) return e;
+      mark(a, mk++);
+      k_zinv_hq<T, NR><<<zgrid, ZC::THREADS, ZC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw,
+                                                                   stw_ptr<T>(a, 0, ZC::E));
       mark(a, mk++);
     }
     return cudaGetLastError();
@@ -322,7 +387,8 @@ cudaError_t launch_split3(const Split3Args& s) {
 
 template <typename T, int NR>
 cudaError_t launch_pow2_n(const Pow2Args& a) {
-  if (a.quad) return launch_quad<T, NR>(a);
+  if (a.quad == 1) return launch_quad<T, NR>(a);
+  if (a.quad == 2) return launch_hq<T, NR>(a);
   using V = vec2_t<T>;
   using CC = ContigCfg<T, NR>;
   using SC = StridedCfg<T, NR, 0>;
@@ -372,6 +438,44 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   const bool single = a.nchunks == 1 && a.ni == NR && a.nj == NR && a.specC == a.spec && a.j0 == 0;
   int mk = 0;
   const bool fused = tma && a.ctrs != nullptr && FusedCfg<T, NR>::OK && !a.peer_y;
+  // Sub-range launches of the slab's chunked exchange (a.subn > 0, one phase): K1 + K2 on
+  // local i planes [sub0, sub0 + subn), or K3 on local j lines [sub0, sub0 + subn) (whole
+  // JB blocks).  Rows of layout B are linear in il (rowB(g, il0 + il, j) = rowB(g, il, j) +
+  // il0 JB) and rows of layout C in whole j blocks, so a sub-range is the full layout's
+  // kernels on advanced bases, with TMA views of the sub-range's extent.
+  if (a.subn > 0) {
+    if (!tma || fused || a.peer_y || a.peer_x || single) return cudaErrorNotSupported;
+    const size_t ncp = size_t(spec_pitch(NR));
+    if (a.phases == kPhaseZY) {
+      const int JB = 1 << gB.jbs;
+      if (a.sub0 < 0 || a.sub0 + a.subn > a.ni) return cudaErrorInvalidValue;
+      V* Ssub = S + size_t(a.sub0) * JB * ncp;
+      k_zfwd<T, NR><<<unsigned(size_t(a.subn) * NR / CC::L), CC::THREADS, CC::SMEM, a.stream>>>(
+          static_cast<const T*>(a.f) + size_t(a.sub0) * NR * NR, Ssub, tw, stw_ptr<T>(a, 0, CC::E), gB);
+      alignas(64) CUtensorMap m;
+      if ((e = encode_map<T, NR>(&m, Ssub, gB, a.nchunks, true, NR / 2 + 1, spec_pitch(NR), TmaCfg<T, NR, true>::L,
+                                 false, TmaCfg<T, NR, false, x_wide<T, false>()>::L, a.subn)))
+        return e;
+      KSpan ks{NR / 2 + 1, spec_pitch(NR), 0};
+      ks.no = a.subn;
+      return launch_strided_tma<T, NR, 0>(a, m, Ssub, gB, scale, four_pi2, ks);
+    }
+    if (a.phases == kPhaseX) {
+      const int JB = 1 << gC.jbs;
+      if (a.sub0 % JB || a.subn % JB || a.sub0 + a.subn > a.nj) return cudaErrorInvalidValue;
+      V* Csub = static_cast<V*>(a.specC) + size_t(a.sub0 / JB) * gC.ni * JB * ncp;
+      alignas(64) CUtensorMap m;
+      if ((e = encode_map<T, NR>(&m, Csub, gC, a.nchunks, false, NR / 2 + 1, spec_pitch(NR), TmaCfg<T, NR, true>::L,
+                                 false, TmaCfg<T, NR, false, x_wide<T, false>()>::L, 0, a.subn / JB)))
+        return e;
+      Pow2Args a2 = a;
+      a2.j0 = a.j0 + a.sub0;  // global j of the sub-range's first line (symbol)
+      KSpan ks{NR / 2 + 1, spec_pitch(NR), 0};
+      ks.no = a.subn;
+      return launch_strided_tma<T, NR, 2>(a2, m, Csub, gC, scale, four_pi2, ks);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (fused && (a.fuse & kFuseFwd) && (a.phases & kPhaseZY)) {
     mark(a, mk++);
     if constexpr (FusedCfg<T, NR>::OK) {

@@ -120,3 +120,22 @@ def test_1024_pencil_2x4_loopback_vs_oracle(cuda, headline, xchg):
     e = _rel(torch, u, uo)
     s.close()
     assert e <= TOL64, e
+
+
+def test_1024_multi_gpu_object_vs_oracle(cuda, headline):
+    """The single-process multi-GPU path (ARENA_FFT_NGPU's arena_mgpu, 4 ranks placed on
+    device 0 here) on the headline buffer, device shards."""
+    torch = cuda
+    arena.clear_plan_cache()
+    f, uo = headline
+    P = 4
+    m = arena.MultiGPU(N, P, devices=[0] * P)
+    ni = N // P
+    us = [torch.empty((ni, N, N), dtype=torch.float64, device="cuda") for _ in range(P)]
+    m.solve_device([f[v * ni:(v + 1) * ni] for v in range(P)], us)
+    torch.cuda.synchronize()
+    num = sum(((us[v] - uo[v * ni:(v + 1) * ni]) ** 2).sum().item() for v in range(P))
+    e = (num ** 0.5) / uo.norm().item()
+    m.close()
+    del us
+    assert e <= TOL64, e

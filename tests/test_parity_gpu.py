@@ -229,6 +229,47 @@ def test_slab_loopback_vs_oracle(cuda, n, P):
     assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64
 
 
+@pytest.mark.parametrize("n,P,cf,cb", [(128, 2, 1, 1), (128, 2, 4, 1), (256, 2, 3, 2), (256, 4, 4, 1),
+                                        (512, 2, 4, 4), (512, 4, 2, 2), (1024, 8, 4, 2)])
+def test_slab_loopback_chunked_exchange(cuda, n, P, cf, cb):
+    """The chunked COPY exchange (sub-steps on the exchange stream, gated by events after
+    the sub-range kernels) with P virtual ranks: every chunking gives the oracle's u."""
+    torch = cuda
+    f_np = np.random.default_rng(n + 11 * P + cf).uniform(-1, 1, (n, n, n))
+    f = torch.from_numpy(f_np).cuda()
+    u = torch.empty_like(f)
+    s = arena.Slab(n, P, loopback=True)
+    s.set_chunking(cf, cb)
+    assert s.chunking == (cf, cb)
+    s.solve_device(f, u)
+    s.wait(timeout_s=60)
+    ref = oracle.poisson_solve(f_np)
+    assert _rel(u.cpu().numpy(), ref) <= TOL64
+    # repeated solves through the same streams / events stay exact
+    s.solve_device(f, u)
+    s.solve_device(f, u)
+    s.wait(timeout_s=60)
+    assert _rel(u.cpu().numpy(), ref) <= TOL64
+    s.close()
+
+
+def test_slab_nccl_single_rank_chunked(cuda):
+    """The chunked NCCL exchange with a one-rank communicator (self send / recv per piece),
+    and arena_slab_wait's NCCL error polling on a healthy communicator."""
+    torch = cuda
+    n = 256
+    f_np = np.random.default_rng(6).uniform(-1, 1, (n, n, n))
+    f = torch.from_numpy(f_np).cuda()
+    u = torch.empty_like(f)
+    s = arena.Slab(n, 1, rank=0, nccl_id=arena.nccl_unique_id())
+    assert s.chunking == (4, 4)
+    for _ in range(3):
+        s.solve_device(f, u)
+    s.wait(timeout_s=60)
+    assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64
+    s.close()
+
+
 def test_slab_loopback_config4_1024(cuda):
     """1024^3 config 4 through 8 virtual slabs vs the analytic solution."""
     torch = cuda
@@ -622,12 +663,14 @@ def test_graph_replay_small_n(cuda):
 
 @pytest.mark.parametrize("n", [32, 64, 128, 256, 512])
 @pytest.mark.parametrize("precision", [64, 32])
-def test_quadrant_path_vs_oracle(cuda, n, precision, monkeypatch):
+@pytest.mark.parametrize("mode", ["1", "hq"])
+def test_quadrant_path_vs_oracle(cuda, n, precision, mode, monkeypatch):
     """The quadrant formulation (poisson_quad.cuh: the first radix-2 step of the i
     and j transforms in the z passes, four n/2-point quadrant problems for the
-    strided passes), forced at small n, against the oracle."""
+    strided passes) and the i-split (poisson_hq.cuh: the i step only, two chunks
+    with n-point y lines and n/2-point x lines), forced at small n, against the oracle."""
     torch = cuda
-    monkeypatch.setenv("ARENA_FFT_QUAD", "1")
+    monkeypatch.setenv("ARENA_FFT_QUAD", mode)
     f_np = np.random.default_rng(n + 7).uniform(-1, 1, (n, n, n))
     dt = torch.float64 if precision == 64 else torch.float32
     f = torch.from_numpy(f_np).to(dtype=dt, device="cuda")
@@ -643,10 +686,11 @@ def test_quadrant_path_vs_oracle(cuda, n, precision, monkeypatch):
     assert len(times) == 5, times
 
 
-def test_quadrant_path_1024_analytic(cuda, monkeypatch):
-    """Quadrant formulation at 1024^3 (config 4) against the analytic solution, in place."""
+@pytest.mark.parametrize("mode", ["1", "hq"])
+def test_quadrant_path_1024_analytic(cuda, mode, monkeypatch):
+    """Quadrant / i-split formulations at 1024^3 (config 4) against the analytic solution, in place."""
     torch = cuda
-    monkeypatch.setenv("ARENA_FFT_QUAD", "1")
+    monkeypatch.setenv("ARENA_FFT_QUAD", mode)
     src, f, ua = _config_device(torch, 4)
     arena.Plan(1024).solve_device(f, f)
     torch.cuda.synchronize()
@@ -654,7 +698,7 @@ def test_quadrant_path_1024_analytic(cuda, monkeypatch):
     assert e <= 1e-12, e
 
 
-@pytest.mark.parametrize("quad", ["0", "1"])
+@pytest.mark.parametrize("quad", ["0", "1", "hq"])
 @pytest.mark.parametrize("n,precision", [(64, 64), (128, 64), (256, 64), (128, 32), (512, 32)])
 def test_repeat_bitwise_deterministic(cuda, n, precision, quad, monkeypatch):
     """No atomics anywhere on the path, so repeated solves must agree bit for bit; a

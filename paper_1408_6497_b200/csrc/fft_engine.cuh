@@ -335,10 +335,16 @@ __device__ __forceinline__ void xbarrier() {
   }
 }
 
+// Called after every exchange barrier (a caller's producer thread can advance its
+// asynchronous copies there without a barrier of its own); no-op by default.
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
 // Write stage outputs to shared memory at their Stockham destinations and
 // read back the natural-order inputs of the next stage.
-template <int N, int E, int L, int R, int NS, int SW, int SYNC, typename V>
-__device__ __forceinline__ void stage_exchange(V (&v)[E], V* sm, int t, int l) {
+template <int N, int E, int L, int R, int NS, int SW, int SYNC, typename V, typename HK = NoHook>
+__device__ __forceinline__ void stage_exchange(V (&v)[E], V* sm, int t, int l, const HK& hook = HK{}) {
   constexpr int P = N / E, NB = E / R;
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
@@ -348,21 +354,24 @@ __device__ __forceinline__ void stage_exchange(V (&v)[E], V* sm, int t, int l) {
     for (int r = 0; r < R; ++r) sm[smem_idx<L, SW, V>(dst + r * NS, l)] = v[q + NB * r];
   }
   xbarrier<SYNC>();
+  hook();
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = sm[smem_idx<L, SW, V>(t + P * e, l)];
   xbarrier<SYNC>();
+  hook();
 }
 
-template <int N, int E, int L, int S, int SYNC, int STAGE, typename V, typename TW, int STOP = num_stages(N, E)>
-__device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, TW stw, int t, int l) {
+template <int N, int E, int L, int S, int SYNC, int STAGE, typename V, typename TW, int STOP = num_stages(N, E),
+          typename HK = NoHook>
+__device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, TW stw, int t, int l, const HK& hook = HK{}) {
   constexpr int NSTAGE = num_stages(N, E);
   if constexpr (STAGE < STOP) {
     constexpr int R = 1 << stage_log2(N, E, STAGE);
     constexpr int NS = stage_ns(N, E, STAGE);
     constexpr int SW = stage_log2(N, E, 0);
     stage_compute<N, E, R, NS, S>(v, t, stw + (STAGE >= 1 ? stage_tw_offset(N, E, STAGE) : 0));
-    if constexpr (STAGE + 1 < NSTAGE) stage_exchange<N, E, L, R, NS, SW, SYNC>(v, sm, t, l);
-    fft_stages<N, E, L, S, SYNC, STAGE + 1, V, TW, STOP>(v, sm, stw, t, l);
+    if constexpr (STAGE + 1 < NSTAGE) stage_exchange<N, E, L, R, NS, SW, SYNC>(v, sm, t, l, hook);
+    fft_stages<N, E, L, S, SYNC, STAGE + 1, V, TW, STOP>(v, sm, stw, t, l, hook);
   }
 }
 
@@ -370,18 +379,18 @@ __device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, TW stw, int t, int 
 // line-l elements t + P*e (natural order).  `sm` must hold N*L elements and
 // be free (all threads past their last access) on entry; on exit it is free.
 // `stw` is the (N, E) stage-twiddle table (stage_tw_total(N, E) entries).
-template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V, typename TW>
-__device__ __forceinline__ void line_fft(V (&v)[E], V* sm, TW stw, int t, int l) {
-  fft_stages<N, E, L, S, SYNC, 0>(v, sm, stw, t, l);
+template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V, typename TW, typename HK = NoHook>
+__device__ __forceinline__ void line_fft(V (&v)[E], V* sm, TW stw, int t, int l, const HK& hook = HK{}) {
+  fft_stages<N, E, L, S, SYNC, 0, V, TW, num_stages(N, E), HK>(v, sm, stw, t, l, hook);
 }
 
 // The same transform split in two: `head` runs every stage but the last
 // (with all exchanges, so `sm` is free on return), `tail` the last stage,
 // in registers only.  Lets a caller refill `sm` while the tail computes.
-template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V, typename TW>
-__device__ __forceinline__ void line_fft_head(V (&v)[E], V* sm, TW stw, int t, int l) {
+template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V, typename TW, typename HK = NoHook>
+__device__ __forceinline__ void line_fft_head(V (&v)[E], V* sm, TW stw, int t, int l, const HK& hook = HK{}) {
   constexpr int NST = num_stages(N, E);
-  if constexpr (NST > 1) fft_stages<N, E, L, S, SYNC, 0, V, TW, NST - 1>(v, sm, stw, t, l);
+  if constexpr (NST > 1) fft_stages<N, E, L, S, SYNC, 0, V, TW, NST - 1, HK>(v, sm, stw, t, l, hook);
 }
 template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V, typename TW>
 __device__ __forceinline__ void line_fft_tail(V (&v)[E], V* sm, TW stw, int t, int l) {

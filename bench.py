@@ -500,6 +500,18 @@ def run_ours(args, rank, world, local):
         dist.destroy_process_group()
 
 
+def _nccl_init_lines():
+    """This rank's NCCL communicator-creation lines (NCCL_DEBUG=INFO into the file _relaunch set)."""
+    import socket
+
+    path = os.path.join("/tmp", f"arena_bench_nccl.{socket.gethostname()}.{os.getpid()}.log")
+    try:
+        with open(path) as fh:
+            return [ln.strip() for ln in fh if "Init COMPLETE" in ln or "nranks" in ln.lower()][-4:]
+    except OSError:
+        return None
+
+
 def run_slab(args, rank, world, local):
     """N > 1: slab decomposition over the ranks' GPUs, NCCL all-to-alls (strong scaling:
     the n^3 problem is fixed, each rank owns n/N planes)."""
@@ -721,6 +733,7 @@ def run_slab(args, rank, world, local):
                          "nvlink_bytes_per_gpu": nvl_per_gpu, "nvlink_peak_gbs": nvl_peak,
                          "t_roof_ms": t_roof * 1e3},
             "nvlink": nvlink,
+            "nccl_init": _nccl_init_lines(),
             "cpu_baseline": None,
             "cpu_baseline_note": "measured on rank 0 at N=1 only (bench.py --gpus 1)",
             "e2e": e2e,

@@ -97,6 +97,7 @@ struct arena_fft_plan {
   int lag = 2;
   int fuse = 0;             // kFuseFwd | kFuseInv
   int quad = 0;             // quadrant formulation (poisson_quad.cuh)
+  int xtmem = 0;            // x pass with TMEM-staged tiles (poisson_xtmem.cuh)
   bool split3 = false;      // generic n = 3M: radix-3 split onto the power-of-two passes (poisson_split3.cuh)
   void* Q = nullptr;        // split3: nine-chunk workspace
   void* stwz = nullptr;     // split3: stage tables of the M/2-point z sub-FFTs (nullptr: generic z passes)
@@ -286,6 +287,7 @@ arena_status enqueue_kernels(arena_fft_plan* p, const void* d_f, void* d_u, cuda
     Pow2Args a{d_f, d_u, p->spec, p->tw, p->stw, p->n, p->nc, p->ncp, s, ev, p->tma, p->sm_count,
                /*ni*/ p->n, /*nj*/ p->n, /*nchunks*/ 1, /*j0*/ 0, /*specC*/ p->spec, kPhaseAll, p->ctrs, p->lag, p->fuse};
     a.quad = p->quad;
+    a.xtmem = p->xtmem;
     e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
   } else if (p->split3) {
     const int R = split_radix(p->n);
@@ -442,6 +444,12 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
         want = (n >= 2048 || (n == 512 && precision_bits == 64)) ? 1 : 0;
       }
       p->quad = (want && p->tma && n >= 32 && !p->fuse) ? want : 0;
+    }
+    // x pass with the next tile staged in tensor memory (fp64 n = 1024).  ARENA_FFT_XTMEM = 0 | 1.
+    {
+      const char* xt = std::getenv("ARENA_FFT_XTMEM");
+      const bool want = xt ? std::string(xt) == "1" : false;
+      p->xtmem = (want && p->tma && !p->quad && n == 1024 && precision_bits == 64) ? 1 : 0;
     }
   } else {
     p->path = ARENA_PATH_GENERIC;

@@ -191,6 +191,20 @@ __device__ __forceinline__ double poisson_symbol(double k2, double scale, double
   }
   return k2 == 0.0 ? 0.0 : scale * r;
 }
+// Lean fp64 symbol of the x passes: m = 1 / (k2 * (four_pi2 / scale)), the scale folded
+// into the divisor (exact for the power-of-two path, scale = 2^-3 log2 n), the MUFU
+// estimate refined by one cubic step r (1 + e + e^2) (~2^-66 from its ~2^-22), and no
+// k2 == 0 select — the caller zeroes the one k = 0 mode (ARENA_LEAN_SYMBOL).
+#ifndef ARENA_LEAN_SYMBOL
+#define ARENA_LEAN_SYMBOL 1
+#endif
+__device__ __forceinline__ double poisson_symbol_lean(double k2, double cinv) {
+  const double d = k2 * cinv;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  const double e = fma(-d, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
 __device__ __forceinline__ float poisson_symbol(float k2, float scale, float four_pi2) {
   const float d = four_pi2 * k2;
   float r;
@@ -755,15 +769,24 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
                            : T(signed_freq(j0 + outer, NG));
       const T kk = T(ks.k0 + k);
       const T c = kj * kj + kk * kk;
+      auto kiof = [&](int e) {
+        return SPL > 0 ? T(signed_freq(SPL * (t + P * e) + qd / imax(SPL, 1), NG))
+               : QUAD  ? T(signed_freq(2 * (t + P * e) + qd, NG))
+                       : T(signed_freq(t + P * e, NG));
+      };
+      constexpr bool LEAN = sizeof(T) == 8 && ARENA_LEAN_SYMBOL;
+      const T cinv = four_pi2 / scale;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const T ki = SPL > 0 ? T(signed_freq(SPL * (t + P * e) + qd / imax(SPL, 1), NG))
-                     : QUAD  ? T(signed_freq(2 * (t + P * e) + qd, NG))
-                             : T(signed_freq(t + P * e, NG));
-        const T k2 = ki * ki + c;
-        const T m = poisson_symbol(k2, scale, four_pi2);
+        const T k2 = kiof(e) * kiof(e) + c;
+        T m;
+        if constexpr (LEAN) m = poisson_symbol_lean(k2, cinv);
+        else m = poisson_symbol(k2, scale, four_pi2);
         v[e].x *= m;
         v[e].y *= m;
+      }
+      if constexpr (LEAN) {
+        if (c == T(0) && t == 0 && kiof(0) == T(0)) v[0] = V{T(0), T(0)};  // k = 0: the mean, dropped
       }
       line_fft_head<N, E, L, +1>(v, cur, twp, t, l);
       if constexpr (num_stages(N, E) == 1) __syncthreads();  // no exchange: make the buffer reads complete

@@ -10,6 +10,7 @@
 #include "launchers.h"
 #include "poisson_fused.cuh"
 #include "poisson_hq.cuh"
+#include "poisson_xtmem.cuh"
 #include "poisson_quad.cuh"
 #include "poisson_split3.cuh"
 
@@ -258,7 +259,7 @@ cudaError_t launch_hq(const Pow2Args& a) {
     const T four_pi2 = T(4.0 * M_PI * M_PI);           // fft_solver.cpp:66
     const V* tw = static_cast<const V*>(a.tw);
     V* S = static_cast<V*>(a.spec);
-    const unsigned zgrid = unsigned(H) * NR;
+    const unsigned zgrid = unsigned(H) * (NR / ZC::JR);
     int mk = 0;
     if (a.phases & kPhaseZY) {
       mark(a, mk++);
@@ -518,9 +519,22 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
       }
       if (e) return e;
     } else if (tma) {
-      if (single) e = launch_strided_tma<T, NR, 2, false, true>(a, *mx, a.specC, gC, scale, four_pi2);
-      else e = launch_strided_tma<T, NR, 2>(a, *mx, a.specC, gC, scale, four_pi2);
-      if (e) return e;
+      bool done = false;
+      if constexpr (sizeof(T) == 8 && NR == XTmemCfg::N) {
+        if (single && a.xtmem) {  // next tile staged in TMEM (poisson_xtmem.cuh)
+          if ((e = ensure_smem<k_xpass_tmem<T, NR>>(XTmemCfg::SMEM, XTmemCfg::THREADS))) return e;
+          const int tiles = NR * ((NR / 2 + 1 + XTmemCfg::L - 1) / XTmemCfg::L);
+          k_xpass_tmem<T, NR><<<imin(a.sm_count, tiles), XTmemCfg::THREADS, XTmemCfg::SMEM, a.stream>>>(
+              *mx, static_cast<V*>(a.specC), stw_ptr<T>(a, 1, XTmemCfg::E), scale, four_pi2);
+          if ((e = cudaGetLastError())) return e;
+          done = true;
+        }
+      }
+      if (!done) {
+        if (single) e = launch_strided_tma<T, NR, 2, false, true>(a, *mx, a.specC, gC, scale, four_pi2);
+        else e = launch_strided_tma<T, NR, 2>(a, *mx, a.specC, gC, scale, four_pi2);
+        if (e) return e;
+      }
     } else {
       if ((e = ensure_smem<k_xmid<T, NR>>(XC::SMEM, XC::THREADS))) return e;
       k_xmid<T, NR><<<dim3((a.nc + XC::L - 1) / XC::L, NR), XC::THREADS, XC::SMEM, a.stream>>>(

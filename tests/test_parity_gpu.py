@@ -270,6 +270,22 @@ def test_slab_nccl_single_rank_chunked(cuda):
     s.close()
 
 
+@pytest.mark.parametrize("n", [64, 256])
+def test_pencil_nccl_single_rank(cuda, n):
+    """The pencil's NCCL code path (ncclCommSplit row / column communicators, four
+    grouped send/recv all-to-alls) with a one-rank 1 x 1 grid."""
+    torch = cuda
+    f_np = np.random.default_rng(n + 17).uniform(-1, 1, (n, n, n))
+    f = torch.from_numpy(f_np).cuda()
+    u = torch.empty_like(f)
+    s = arena.Pencil(n, 1, 1, rank=0, nccl_id=arena.nccl_unique_id())
+    for _ in range(2):
+        s.solve_device(f, u)
+    torch.cuda.synchronize()
+    assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64
+    s.close()
+
+
 def test_slab_loopback_config4_1024(cuda):
     """1024^3 config 4 through 8 virtual slabs vs the analytic solution."""
     torch = cuda
@@ -821,3 +837,29 @@ def test_split3_path_vs_oracle(cuda, n, precision, monkeypatch):
     ref = oracle.poisson_solve(f.double().cpu().numpy())
     tol = TOL64 if precision == 64 else TOL32
     assert _rel(out["1"], ref) <= tol and _rel(out["0"], ref) <= tol
+
+
+@pytest.mark.parametrize("xtmem", ["0", "1"])
+def test_x_pass_tmem_staging_1024(cuda, xtmem, monkeypatch):
+    """fp64 1024^3 with the x pass's next tile staged through TMEM (poisson_xtmem.cuh:
+    TMA -> shared staging -> tcgen05.cp -> TMEM -> tcgen05.ld) against the oracle on a
+    random field, and bit-identical to itself over repeated solves."""
+    torch = cuda
+    monkeypatch.setenv("ARENA_FFT_XTMEM", xtmem)
+    arena.clear_plan_cache()
+    n = 1024
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    f = torch.rand((n, n, n), dtype=torch.float64, device="cuda", generator=g) - 0.5
+    u = torch.empty_like(f)
+    p = arena.Plan(n, 64)
+    p.solve_device(f, u)
+    torch.cuda.synchronize()
+    ref = torch.from_numpy(oracle.poisson_solve(f.cpu().numpy())).cuda()
+    e = ((u - ref).norm() / ref.norm()).item()
+    assert e <= TOL64, e
+    u2 = torch.empty_like(f)
+    for _ in range(3):
+        p.solve_device(f, u2)
+    torch.cuda.synchronize()
+    assert torch.equal(u, u2)
+    p.close()

@@ -58,6 +58,8 @@ def _args():
     ap.add_argument("--slab", action="store_true", help="use the slab (NCCL) path even with one rank")
     ap.add_argument("--decomp", default="slab", choices=("slab", "pencil"), help="multi-GPU decomposition")
     ap.add_argument("--pgrid", default=None, help="pencil process grid RxC (default: near-square, R <= C)")
+    ap.add_argument("--fold", action="store_true",
+                    help="pencil: folded distribution (quadrant z passes, n/2-point strided passes; NCCL exchange)")
     ap.add_argument("--xchg", default="peer", choices=("peer", "nccl"),
                     help="exchange: peer = fused into the passes as NVLink stores (CUDA IPC), nccl = send/recv")
     return ap.parse_args()
@@ -547,7 +549,19 @@ def run_slab(args, rank, world, local):
 
     # this rank's block of f, global mean removed
     f64 = torch.empty((ni, nj, n), dtype=torch.float64, device="cuda")
-    problems.fill_device(src, "f", f64, 64, sh, i0, ni, j0, nj)
+    fold = pencil and args.fold
+
+    def fill_block(which, out):
+        if not fold:
+            problems.fill_device(src, which, out, 64, sh, i0, ni, j0, nj)
+            return
+        for gi, gj, li, lj, bi, bj in arena.fold_blocks(n, pr, pc, rank // pc, rank % pc):
+            tmp = torch.empty((bi, bj, n), dtype=torch.float64, device="cuda")
+            problems.fill_device(src, which, tmp, 64, sh, gi, bi, gj, bj)
+            out[li:li + bi, lj:lj + bj].copy_(tmp)
+            del tmp
+
+    fill_block("f", f64)
     tot = f64.sum().reshape(1)
     dist.all_reduce(tot)
     f64 -= tot.item() / float(n) ** 3
@@ -555,7 +569,7 @@ def run_slab(args, rank, world, local):
     u = torch.empty_like(f)
 
     ua = torch.empty((ni, nj, n), dtype=torch.float64, device="cuda")
-    problems.fill_device(src, "u", ua, 64, sh, i0, ni, j0, nj)
+    fill_block("u", ua)
 
     def rel_vs_analytic():
         sums = torch.stack([ua.sum()])
@@ -573,7 +587,7 @@ def run_slab(args, rank, world, local):
         dist.broadcast(idt, 0)
         nid = bytes(idt.cpu().numpy().tobytes())
         if pencil:
-            return arena.Pencil(n, pr, pc, rank=rank, nccl_id=nid, precision=prec, device=local)
+            return arena.Pencil(n, pr, pc, rank=rank, nccl_id=nid, precision=prec, device=local, folded=fold)
         return arena.Slab(n, world, rank=rank, nccl_id=nid, precision=prec, device=local)
 
     def vote(ok):  # every rank takes the same branch
@@ -620,6 +634,8 @@ def run_slab(args, rank, world, local):
     xchg = args.xchg
     note = None
     slab = None
+    if fold and xchg == "peer":
+        xchg, note = "nccl", "the folded pencil runs the NCCL exchange"
     if xchg == "peer":
         slab, err = try_peer()
         if slab is None:  # fall back to the NCCL exchange, and say so
@@ -726,7 +742,7 @@ def run_slab(args, rank, world, local):
                                              "all-to-alls fused into K2/K3 as stores into the peers' "
                                              "workspaces (CUDA IPC over NVLink) + device flag barriers"
                                              if xchg == "peer" else "NCCL grouped send/recv all-to-all")),
-                       "exchange": xchg, "exchange_note": note,
+                       "exchange": xchg, "exchange_note": note, "folded": fold,
                        "l2": "inputs larger than L2, no flush"},
             "roofline": {"bound": "hbm+nvlink", "achieved": hbm_per_gpu / (ms_step / 1e3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": t_roof / (ms_step / 1e3), "traffic": None, "peak_kind": peak_kind,

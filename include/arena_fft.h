@@ -224,6 +224,14 @@ arena_status arena_pencil_peer_attach(arena_fft_pencil* pencil, const void* all_
 arena_status arena_pencil_set_exchange(arena_fft_pencil* pencil, int mode);
 arena_status arena_pencil_solve_phase(arena_fft_pencil* pencil, int phase, const void* d_f, void* d_u, void* stream);
 arena_status arena_pencil_barrier_status(arena_fft_pencil* pencil);
+/* Folded distribution (config 5 at 2048^3): rank (r, c) owns i in I_r U (I_r + n/2),
+ * j in J_c U (J_c + n/2) (I_r, J_c: its n/(2 Pr), n/(2 Pc) slices of [0, n/2)) as a
+ * (n/Pr) x (n/Pc) x n block whose local i < n/(2 Pr) is I_r and the rest I_r + n/2
+ * (j alike).  The first radix-2 steps of the i and j transforms then run in the
+ * rank's z passes and the strided passes are n/2-point (128-byte-row tiles at
+ * 2048^3).  Set before the first solve; COPY (NCCL / loopback) exchange only. */
+enum { ARENA_PENCIL_PLAIN = 0, ARENA_PENCIL_FOLDED = 1 };
+arena_status arena_pencil_set_layout(arena_fft_pencil* pencil, int layout);
 
 /* One process driving P GPUs (P <= 8; the drop-in's multi-GPU path, selected by
  * ARENA_FFT_NGPU): rank v lives on devices[v] (NULL: v mod device count) and holds

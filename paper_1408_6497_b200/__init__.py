@@ -99,6 +99,7 @@ _sig = {
     "arena_pencil_set_exchange": (_i, [_vp, _i]),
     "arena_pencil_solve_phase": (_i, [_vp, _i, _vp, _vp, _vp]),
     "arena_pencil_barrier_status": (_i, [_vp]),
+    "arena_pencil_set_layout": (_i, [_vp, _i]),
     "arena_field_stats": (_i, [ctypes.c_size_t, _i, _vp, ctypes.POINTER(ctypes.c_double),
                                ctypes.POINTER(ctypes.c_double)]),
     "arena_field_compare": (_i, [ctypes.c_size_t, _i, _vp, _vp, ctypes.POINTER(ctypes.c_double),
@@ -440,12 +441,15 @@ class Pencil(_Decomposition):
     Pencil(n, Pr, Pc, rank=r, peer=True)    — one rank, exchanges fused into K1-K4 as stores
                                               into the peers' buffers (peer_attach first);
     Pencil(n, Pr, Pc, loopback=True)        — all ranks on one device (full field in/out).
+    folded=True: the folded distribution (include/arena_fft.h ARENA_PENCIL_FOLDED; a rank's
+    block is fold_blocks(n, Pr, Pc, r, c)), quadrant z passes and n/2-point strided passes.
     """
 
     _pfx = "pencil"
 
     def __init__(self, n: int, pr: int, pc: int, rank: int = 0, nccl_id: Optional[bytes] = None,
-                 precision: int = 64, device: int = -1, loopback: bool = False, peer: bool = False):
+                 precision: int = 64, device: int = -1, loopback: bool = False, peer: bool = False,
+                 folded: bool = False):
         self._s = _vp()
         if loopback:
             _check(lib.arena_pencil_create_loopback(ctypes.byref(self._s), int(n), int(precision), int(device),
@@ -466,6 +470,16 @@ class Pencil(_Decomposition):
         self.precision = int(precision)
         self.device = _resolve_device(device)
         self.field_numel = self.n ** 3 if loopback else (self.n // self.pr) * (self.n // self.pc) * self.n
+        self.folded = bool(folded)
+        if folded:
+            _check(lib.arena_pencil_set_layout(self._s, 1), "arena_pencil_set_layout")
+
+
+def fold_blocks(n: int, pr: int, pc: int, r: int, c: int):
+    """Sub-blocks of rank (r, c)'s folded pencil block: [(i0, j0, li0, lj0, ni, nj)] — global
+    plane / line offsets of the n^3 field, local offsets in the (n/Pr) x (n/Pc) x n block."""
+    H, hi, hj = n // 2, n // (2 * pr), n // (2 * pc)
+    return [(a * H + r * hi, b * H + c * hj, a * hi, b * hj, hi, hj) for a in (0, 1) for b in (0, 1)]
 
 
 class MultiGPU:
@@ -684,7 +698,7 @@ def source_gaussian(n: int, alpha: float, center, which: int, out, precision: in
 
 
 __all__ = [
-    "Plan", "Slab", "Pencil", "MultiGPU", "SpectralInterpolant", "nccl_unique_id", "get_plan", "poisson_spectral_solve", "dft3_forward", "dft3_inverse", "signed_freq",
+    "Plan", "Slab", "Pencil", "MultiGPU", "fold_blocks", "SpectralInterpolant", "nccl_unique_id", "get_plan", "poisson_spectral_solve", "dft3_forward", "dft3_inverse", "signed_freq",
     "source_modes", "source_gaussian", "ArenaError", "lib", "LIB_PATH", "CORE_PATH", "HEADER_PATH",
     "PATH_POW2", "PATH_GENERIC",
 ]

@@ -108,6 +108,7 @@ struct PencilArgs {
   void* const* py1 = nullptr;
   void* const* px = nullptr;
   void* const* py2 = nullptr;
+  int fold = 0;  // folded distribution (poisson_qpencil.cuh): quadrant z passes, H-point strided passes
 };
 enum : int { kPencilZ1 = 0, kPencilY1, kPencilX, kPencilY2, kPencilZ2 };
 cudaError_t pencil_phase_f64(const PencilArgs& a, int phase);

@@ -1792,6 +1792,7 @@ struct arena_fft_pencil {
   int xmode = ARENA_XCHG_COPY;
   bool attached = false;
   PeerSync sync;
+  int fold = 0;  // ARENA_PENCIL_FOLDED (poisson_qpencil.cuh)
   size_t row_chunk_bytes() const { return size_t(n / Pr) * (n / Pc) * kq * 2 * base->elem; }
   size_t col_chunk_bytes() const { return size_t(n / Pr) * (n / Pr) * kq * 2 * base->elem; }
 };
@@ -1803,7 +1804,7 @@ void free_pencil(arena_fft_pencil* s) {
   if (s->base) {
     DeviceGuard g(s->base->device);
     for (PencilRank& r : s->ranks)
-      for (void* p : {r.buf1, r.buf2, r.fblk, r.ublk})
+      for (void* p : {r.buf1, r.buf2, r.fblk})  // ublk aliases fblk
         if (p) cudaFree(p);
     s->sync.release();
     if (NcclApi* a = nccl_api()) {
@@ -1852,11 +1853,14 @@ arena_status pencil_init(arena_fft_pencil** out, int n, int prec, int device, in
   s->ranks.resize(loopback ? Pr * Pc : 1);
   for (PencilRank& r : s->ranks) {
     cudaError_t e = cudaSuccess;
+    // loopback: one block per virtual rank for f and u (K1 reads it in phase 0, K5 writes
+    // it in phase 4), so a 2048^3 fp32 field solved in place fits one GPU
     if ((e = cudaMalloc(&r.buf1, s->buf_bytes)) || (e = cudaMalloc(&r.buf2, s->buf_bytes)) ||
-        (loopback && ((e = cudaMalloc(&r.fblk, s->blk_bytes)) || (e = cudaMalloc(&r.ublk, s->blk_bytes))))) {
+        (loopback && (e = cudaMalloc(&r.fblk, s->blk_bytes)))) {
       free_pencil(s);
       return fail(ARENA_ENOMEM, "pencil buffers: " + std::string(cudaGetErrorString(e)));
     }
+    r.ublk = r.fblk;
   }
   if (cudaError_t e = s->sync.init(Pr * Pc)) {
     free_pencil(s);
@@ -1908,6 +1912,7 @@ PencilArgs pencil_args(arena_fft_pencil* s, PencilRank& pr, int rank, const void
   a.tma = &pr.tma;
   a.tma2 = &pr.tma2;
   a.sm_count = p->sm_count;
+  a.fold = s->fold;
   if (s->xmode == ARENA_XCHG_PEER) {
     a.pz = pr.pz;
     a.py1 = pr.py1;
@@ -1935,10 +1940,13 @@ void pencil_fill_peers(arena_fft_pencil* s, PencilRank& me, int rk, const std::v
 // (1 = buf1, 2 = buf2); chunk q of a rank's source goes to peer q's chunk
 // (sender's index in the group).
 arena_status pencil_exchange(arena_fft_pencil* s, cudaStream_t st, bool rowgrp, int from, int to) {
-  const int ni = s->n / s->Pr;
+  // folded: the same exchange for each quadrant's H problem, quadrant q's region at q qbytes
+  const int nq = s->fold ? 4 : 1, ne = s->fold ? s->n / 2 : s->n;
+  const int ni = ne / s->Pr;
   const int grp = rowgrp ? s->Pc : s->Pr;
-  const size_t chunk_rows = size_t(ni) * (rowgrp ? s->n / s->Pc : s->n / s->Pr);
+  const size_t chunk_rows = size_t(ni) * (rowgrp ? ne / s->Pc : ne / s->Pr);
   const size_t bytes = chunk_rows * s->kq * 2 * s->base->elem;
+  const size_t qbytes = size_t(ni) * ne * s->kq * 2 * s->base->elem;
   auto buf = [&](PencilRank& r, int which) { return static_cast<char*>(which == 1 ? r.buf1 : r.buf2); };
   if (s->loopback) {
     for (int rk = 0; rk < s->Pr * s->Pc; ++rk) {
@@ -1946,9 +1954,12 @@ arena_status pencil_exchange(arena_fft_pencil* s, cudaStream_t st, bool rowgrp, 
       const int me = rowgrp ? c : r;
       for (int q = 0; q < grp; ++q) {
         const int peer = rowgrp ? r * s->Pc + q : q * s->Pc + c;
-        cudaError_t e = cudaMemcpyAsync(buf(s->ranks[peer], to) + size_t(me) * bytes,
-                                        buf(s->ranks[rk], from) + size_t(q) * bytes, bytes, cudaMemcpyDeviceToDevice, st);
-        if (e != cudaSuccess) return cuda_fail(e, "loopback pencil exchange");
+        for (int qd = 0; qd < nq; ++qd) {
+          cudaError_t e = cudaMemcpyAsync(buf(s->ranks[peer], to) + qd * qbytes + size_t(me) * bytes,
+                                          buf(s->ranks[rk], from) + qd * qbytes + size_t(q) * bytes, bytes,
+                                          cudaMemcpyDeviceToDevice, st);
+          if (e != cudaSuccess) return cuda_fail(e, "loopback pencil exchange");
+        }
       }
     }
     return ARENA_OK;
@@ -1960,12 +1971,13 @@ arena_status pencil_exchange(arena_fft_pencil* s, cudaStream_t st, bool rowgrp, 
   PencilRank& me = s->ranks[0];
   ncclResult_t res = a->GroupStart();
   if (res != ncclSuccess) return nccl_fail(res, "ncclGroupStart");
-  for (int q = 0; q < grp; ++q) {
-    if ((res = a->Send(buf(me, from) + size_t(q) * bytes, count, dt, q, comm, st)) != ncclSuccess)
-      return nccl_fail(res, "ncclSend");
-    if ((res = a->Recv(buf(me, to) + size_t(q) * bytes, count, dt, q, comm, st)) != ncclSuccess)
-      return nccl_fail(res, "ncclRecv");
-  }
+  for (int q = 0; q < grp; ++q)
+    for (int qd = 0; qd < nq; ++qd) {
+      if ((res = a->Send(buf(me, from) + qd * qbytes + size_t(q) * bytes, count, dt, q, comm, st)) != ncclSuccess)
+        return nccl_fail(res, "ncclSend");
+      if ((res = a->Recv(buf(me, to) + qd * qbytes + size_t(q) * bytes, count, dt, q, comm, st)) != ncclSuccess)
+        return nccl_fail(res, "ncclRecv");
+    }
   if ((res = a->GroupEnd()) != ncclSuccess) return nccl_fail(res, "ncclGroupEnd");
   return ARENA_OK;
 }
@@ -2013,13 +2025,29 @@ static arena_status pencil_run_phase(arena_fft_pencil* s, int phase, const void*
   const size_t elem = s->base->elem;
   const int nr = int(s->ranks.size());
   cudaError_t e;
+  // The rank's block as sub-blocks of the full field: plain — one (ni x nj) block at
+  // (r ni, c nj); folded — four (ni/2 x nj/2) blocks at (r ni/2 + a H, c nj/2 + b H).
+  auto blocks = [&](int rk, auto&& fn) -> cudaError_t {
+    const int r = rk / s->Pc, c = rk % s->Pc;
+    if (!s->fold) return fn(size_t(r) * ni, size_t(c) * nj, size_t(0), size_t(0), ni, nj);
+    const int H = n / 2, hi = ni / 2, hj = nj / 2;
+    for (int a2 = 0; a2 < 2; ++a2)
+      for (int b2 = 0; b2 < 2; ++b2) {
+        cudaError_t e2 = fn(size_t(a2) * H + size_t(r) * hi, size_t(b2) * H + size_t(c) * hj, size_t(a2) * hi,
+                            size_t(b2) * hj, hi, hj);
+        if (e2 != cudaSuccess) return e2;
+      }
+    return cudaSuccess;
+  };
   if (s->loopback && phase == 0) {  // scatter the full field into the virtual ranks' blocks
     for (int rk = 0; rk < nr; ++rk) {
-      const int r = rk / s->Pc, c = rk % s->Pc;
-      const char* src = static_cast<const char*>(d_f) + (size_t(r) * ni * n + size_t(c) * nj) * n * elem;
-      if ((e = cudaMemcpy2DAsync(s->ranks[rk].fblk, size_t(nj) * n * elem, src, size_t(n) * n * elem,
-                                 size_t(nj) * n * elem, ni, cudaMemcpyDeviceToDevice, st)))
-        return cuda_fail(e, "pencil scatter");
+      e = blocks(rk, [&](size_t gi, size_t gj, size_t li, size_t lj, int bi, int bj) {
+        const char* src = static_cast<const char*>(d_f) + (gi * n + gj) * n * elem;
+        char* dst = static_cast<char*>(s->ranks[rk].fblk) + (li * nj + lj) * n * elem;
+        return cudaMemcpy2DAsync(dst, size_t(nj) * n * elem, src, size_t(n) * n * elem, size_t(bj) * n * elem, bi,
+                                 cudaMemcpyDeviceToDevice, st);
+      });
+      if (e != cudaSuccess) return cuda_fail(e, "pencil scatter");
     }
   }
   for (int v = 0; v < nr; ++v) {
@@ -2041,11 +2069,13 @@ static arena_status pencil_run_phase(arena_fft_pencil* s, int phase, const void*
   }
   if (s->loopback && phase == 4) {
     for (int rk = 0; rk < nr; ++rk) {
-      const int rr = rk / s->Pc, c = rk % s->Pc;
-      char* dst = static_cast<char*>(d_u) + (size_t(rr) * ni * n + size_t(c) * nj) * n * elem;
-      if ((e = cudaMemcpy2DAsync(dst, size_t(n) * n * elem, s->ranks[rk].ublk, size_t(nj) * n * elem,
-                                 size_t(nj) * n * elem, ni, cudaMemcpyDeviceToDevice, st)))
-        return cuda_fail(e, "pencil gather");
+      e = blocks(rk, [&](size_t gi, size_t gj, size_t li, size_t lj, int bi, int bj) {
+        char* dst = static_cast<char*>(d_u) + (gi * n + gj) * n * elem;
+        const char* src = static_cast<const char*>(s->ranks[rk].ublk) + (li * nj + lj) * n * elem;
+        return cudaMemcpy2DAsync(dst, size_t(n) * n * elem, src, size_t(nj) * n * elem, size_t(bj) * n * elem, bi,
+                                 cudaMemcpyDeviceToDevice, st);
+      });
+      if (e != cudaSuccess) return cuda_fail(e, "pencil gather");
     }
   }
   return ARENA_OK;
@@ -2113,6 +2143,7 @@ arena_status arena_pencil_set_exchange(arena_fft_pencil* s, int mode) {
   }
   if (mode != ARENA_XCHG_PEER) return fail(ARENA_EINVAL, "unknown exchange mode");
   if (s->Pr * s->Pc > kMaxPeers) return fail(ARENA_EUNSUPPORTED, "peer exchange supports at most 8 ranks");
+  if (s->fold) return fail(ARENA_EUNSUPPORTED, "the folded pencil runs the COPY (NCCL) exchange");
   if (s->loopback) {
     std::vector<std::vector<void*>> bufs;
     for (PencilRank& r : s->ranks) bufs.push_back({r.buf1, r.buf2});
@@ -2121,6 +2152,18 @@ arena_status arena_pencil_set_exchange(arena_fft_pencil* s, int mode) {
     return fail(ARENA_EINVAL, "peer exchange: call arena_pencil_peer_attach first");
   }
   s->xmode = mode;
+  return ARENA_OK;
+}
+
+arena_status arena_pencil_set_layout(arena_fft_pencil* s, int layout) {
+  if (!s) return fail(ARENA_EINVAL, "pencil is NULL");
+  if (layout != ARENA_PENCIL_PLAIN && layout != ARENA_PENCIL_FOLDED) return fail(ARENA_EINVAL, "unknown pencil layout");
+  if (layout == ARENA_PENCIL_FOLDED) {
+    if (s->xmode == ARENA_XCHG_PEER) return fail(ARENA_EUNSUPPORTED, "the folded pencil runs the COPY (NCCL) exchange");
+    if (s->n / 2 / s->Pr < 1 || s->n / 2 / s->Pc < 1 || s->n < 64)
+      return fail(ARENA_EUNSUPPORTED, "folded pencil needs n >= 64 and n/2 divisible by the grid");
+  }
+  s->fold = layout == ARENA_PENCIL_FOLDED ? 1 : 0;
   return ARENA_OK;
 }
 

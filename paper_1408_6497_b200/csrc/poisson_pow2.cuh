@@ -568,6 +568,9 @@ struct KSpan {
   int kc, kq, k0;
   int no = 0;  // lines (outer index) to transform, 0 = all of the layout's (sub-range launches of the
                // slab's chunked exchange pass a shifted base and the sub-range's count)
+  // Folded pencil (poisson_qpencil.cuh): N-point lines of quadrant (fci, fcj) of a 2N grid,
+  // frequencies ki = 2 i'' + fci, kj = 2 (j0 + j'') + fcj (x pass symbol).
+  int fm = 0, fci = 0, fcj = 0;
 };
 
 // Chunked ("split") layouts of the single-GPU path, selected by the SPL template
@@ -766,12 +769,14 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
       // kSplitI: ki = 2 i'' + chunk, kj = j (lines of N = n/2 points)
       constexpr int NG = SPL > 0 ? SPL * N : QUAD ? 2 * N : N;
       const T kj = SPL > 0 ? T(signed_freq(SPL * outer + qd % imax(SPL, 1), NG))
+                   : ks.fm ? T(signed_freq(2 * (j0 + outer) + ks.fcj, 2 * N))
                            : T(signed_freq(j0 + outer, NG));
       const T kk = T(ks.k0 + k);
       const T c = kj * kj + kk * kk;
       auto kiof = [&](int e) {
         return SPL > 0 ? T(signed_freq(SPL * (t + P * e) + qd / imax(SPL, 1), NG))
                : QUAD  ? T(signed_freq(2 * (t + P * e) + qd, NG))
+               : ks.fm ? T(signed_freq(2 * (t + P * e) + ks.fci, 2 * N))
                        : T(signed_freq(t + P * e, NG));
       };
       constexpr bool LEAN = sizeof(T) == 8 && ARENA_LEAN_SYMBOL;

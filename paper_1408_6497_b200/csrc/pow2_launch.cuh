@@ -12,6 +12,7 @@
 #include "poisson_hq.cuh"
 #include "poisson_xtmem.cuh"
 #include "poisson_quad.cuh"
+#include "poisson_qpencil.cuh"
 #include "poisson_split3.cuh"
 
 namespace arena_fft {
@@ -672,8 +673,99 @@ cudaError_t pencil_phase_n(const PencilArgs& a, int phase) {
   return cudaGetLastError();
 }
 
+// Folded pencil (poisson_qpencil.cuh): K1q / K5q on the rank's folded block, and per
+// quadrant q = 2 ci + cj the plain pencil's strided passes of the H = n/2 problem
+// (H-point lines, the n grid's k chunks), quadrant q's regions of buf1 / buf2 at q qstride.
+template <typename T, int NR>
+cudaError_t pencil_fold_phase_n(const PencilArgs& a, int phase) {
+  constexpr int H = NR / 2;
+  using QC = QuadZCfg<T, NR>;
+  if constexpr (!(QC::OK && H >= 32)) {
+    return cudaErrorNotSupported;
+  } else {
+    using V = vec2_t<T>;
+    const int ni = H / a.Pr, nj = H / a.Pc, nj2 = H / a.Pr;
+    const int nc = NR / 2 + 1;
+    KSpan ks{imin(a.kq, nc - a.c * a.kq), a.kq, a.c * a.kq};
+    ks.fm = 1;
+    const bool has_k = ks.kc > 0;
+    const Layout gz = make_layout(ni, nj);
+    const Layout gY = make_layout(ni, nj), gB2 = make_layout(ni, nj2), gC = make_layout(ni, nj2);
+    const T scale = T(1.0 / (double(NR) * NR * NR));
+    const T four_pi2 = T(4.0 * M_PI * M_PI);
+    Pow2Args pa{};
+    pa.n = NR;  // H-point lines read the n/2 stage tables
+    pa.stw = a.stw;
+    pa.stream = a.stream;
+    pa.sm_count = a.sm_count;
+    pa.j0 = a.r * nj2;
+    const size_t qs = size_t(ni) * H * a.kq;  // complex per quadrant region
+    V* b1 = static_cast<V*>(a.buf1);
+    V* b2 = static_cast<V*>(a.buf2);
+    const V* tw = static_cast<const V*>(a.tw);
+    cudaError_t e;
+    if ((e = ensure_smem<k_zfwd_qpencil<T, NR>>(QC::SMEM, QC::THREADS))) return e;
+    if ((e = ensure_smem<k_zinv_qpencil<T, NR>>(QC::SMEM, QC::THREADS))) return e;
+    alignas(64) CUtensorMap m;
+    switch (phase) {
+      case kPencilZ1:
+        k_zfwd_qpencil<T, NR><<<unsigned(ni) * nj, QC::THREADS, QC::SMEM, a.stream>>>(
+            static_cast<const T*>(a.f), b1, tw, stw_ptr<T>(pa, 0, QC::E), gz, a.r * ni, a.c * nj, a.kq, qs);
+        break;
+      case kPencilY1:  // Y (buf2) -> B2 (buf1), per quadrant
+        if (!has_k) break;
+        pa.nchunks = a.Pc;
+        for (int q = 0; q < 4; ++q) {
+          ks.fci = q >> 1;
+          ks.fcj = q & 1;
+          if ((e = encode_map<T, H>(&m, b2 + q * qs, gY, a.Pc, true, ks.kc, ks.kq))) return e;
+          if ((e = launch_strided_tma<T, H, 0>(pa, m, b2 + q * qs, gY, scale, four_pi2, ks, b1 + q * qs, &gB2))) return e;
+        }
+        break;
+      case kPencilX:  // C (buf2) in place, per quadrant
+        if (!has_k) break;
+        pa.nchunks = a.Pr;
+        for (int q = 0; q < 4; ++q) {
+          ks.fci = q >> 1;
+          ks.fcj = q & 1;
+          if ((e = encode_map<T, H>(&m, b2 + q * qs, gC, a.Pr, false, ks.kc, ks.kq))) return e;
+          if ((e = launch_strided_tma<T, H, 2>(pa, m, b2 + q * qs, gC, scale, four_pi2, ks))) return e;
+        }
+        break;
+      case kPencilY2:  // B2 (buf1) -> Y (buf2), per quadrant
+        if (!has_k) break;
+        pa.nchunks = a.Pr;
+        for (int q = 0; q < 4; ++q) {
+          ks.fci = q >> 1;
+          ks.fcj = q & 1;
+          if ((e = encode_map<T, H>(&m, b1 + q * qs, gB2, a.Pr, true, ks.kc, ks.kq))) return e;
+          if ((e = launch_strided_tma<T, H, 1>(pa, m, b1 + q * qs, gB2, scale, four_pi2, ks, b2 + q * qs, &gY))) return e;
+        }
+        break;
+      case kPencilZ2:
+        k_zinv_qpencil<T, NR><<<unsigned(ni) * nj, QC::THREADS, QC::SMEM, a.stream>>>(
+            b1, static_cast<T*>(a.u), tw, stw_ptr<T>(pa, 0, QC::E), gz, a.r * ni, a.c * nj, a.kq, qs);
+        break;
+      default:
+        return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+  }
+}
+
 template <typename T>
 cudaError_t pencil_phase(const PencilArgs& a, int phase) {
+  if (a.fold) {
+    switch (a.n) {
+      case 64: return pencil_fold_phase_n<T, 64>(a, phase);
+      case 128: return pencil_fold_phase_n<T, 128>(a, phase);
+      case 256: return pencil_fold_phase_n<T, 256>(a, phase);
+      case 512: return pencil_fold_phase_n<T, 512>(a, phase);
+      case 1024: return pencil_fold_phase_n<T, 1024>(a, phase);
+      case 2048: return pencil_fold_phase_n<T, 2048>(a, phase);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (a.n) {
     case 64: return pencil_phase_n<T, 64>(a, phase);
     case 128: return pencil_phase_n<T, 128>(a, phase);

@@ -863,3 +863,49 @@ def test_x_pass_tmem_staging_1024(cuda, xtmem, monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(u, u2)
     p.close()
+
+
+@pytest.mark.parametrize("n,pr,pc", [(64, 1, 1), (64, 2, 2), (128, 1, 2), (128, 2, 4), (256, 4, 2), (256, 2, 2)])
+@pytest.mark.parametrize("precision", [64, 32])
+def test_folded_pencil_loopback_vs_oracle(cuda, n, pr, pc, precision):
+    """Folded pencil (config 5's decomposition with the quadrant z passes): all ranks on one
+    GPU, copy exchanges, vs the oracle."""
+    torch = cuda
+    f_np = np.random.default_rng(n + 10 * pr + pc).uniform(-1, 1, (n, n, n))
+    dt = torch.float64 if precision == 64 else torch.float32
+    f = torch.from_numpy(f_np).to(dtype=dt, device="cuda")
+    u = torch.empty_like(f)
+    s = arena.Pencil(n, pr, pc, loopback=True, precision=precision, folded=True)
+    s.solve_device(f, u)
+    torch.cuda.synchronize()
+    ref = oracle.poisson_solve(f_np if precision == 64 else f.double().cpu().numpy())
+    assert _rel(u.double().cpu().numpy(), ref) <= (TOL64 if precision == 64 else TOL32)
+    s.close()
+
+
+def test_folded_pencil_nccl_single_rank(cuda):
+    """The folded pencil's NCCL path (four quadrant pieces per peer) with a 1 x 1 grid."""
+    torch = cuda
+    n = 128
+    f_np = np.random.default_rng(9).uniform(-1, 1, (n, n, n))
+    f = torch.from_numpy(f_np).cuda()
+    u = torch.empty_like(f)
+    s = arena.Pencil(n, 1, 1, rank=0, nccl_id=arena.nccl_unique_id(), folded=True)
+    s.solve_device(f, u)
+    torch.cuda.synchronize()
+    assert _rel(u.cpu().numpy(), oracle.poisson_solve(f_np)) <= TOL64
+    s.close()
+
+
+@pytest.mark.parametrize("pr,pc", [(2, 2), (2, 4)])
+def test_folded_pencil_1024_analytic(cuda, pr, pc):
+    """Config-4 source at 1024^3 through the folded 2x2 / 2x4 pencil (loopback) vs analytic."""
+    torch = cuda
+    src, f, ua = _config_device(torch, 4)
+    u = torch.empty_like(f)
+    s = arena.Pencil(1024, pr, pc, loopback=True, folded=True)
+    s.solve_device(f, u)
+    torch.cuda.synchronize()
+    e = (torch.linalg.vector_norm(u - ua) / torch.linalg.vector_norm(ua)).item()
+    s.close()
+    assert e <= 1e-12, e

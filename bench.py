@@ -59,7 +59,7 @@ def _args():
     ap.add_argument("--decomp", default="slab", choices=("slab", "pencil"), help="multi-GPU decomposition")
     ap.add_argument("--pgrid", default=None, help="pencil process grid RxC (default: near-square, R <= C)")
     ap.add_argument("--fold", action="store_true",
-                    help="pencil: folded distribution (quadrant z passes, n/2-point strided passes; NCCL exchange)")
+                    help="pencil: folded distribution (quadrant z passes, n/2-point strided passes; default at n >= 2048)")
     ap.add_argument("--xchg", default="peer", choices=("peer", "nccl"),
                     help="exchange: peer = fused into the passes as NVLink stores (CUDA IPC), nccl = send/recv")
     return ap.parse_args()
@@ -549,7 +549,9 @@ def run_slab(args, rank, world, local):
 
     # this rank's block of f, global mean removed
     f64 = torch.empty((ni, nj, n), dtype=torch.float64, device="cuda")
-    fold = pencil and args.fold
+    # folded pencil (quadrant z passes, n/2-point strided tiles): default at n >= 2048, where the
+    # plain pencil's n-point y / x tiles no longer fit 128-byte rows
+    fold = pencil and (args.fold or n >= 2048)
 
     def fill_block(which, out):
         if not fold:
@@ -600,7 +602,7 @@ def run_slab(args, rank, world, local):
         s, err = None, None
         try:
             if pencil:
-                s = arena.Pencil(n, pr, pc, rank=rank, peer=True, precision=prec, device=local)
+                s = arena.Pencil(n, pr, pc, rank=rank, peer=True, precision=prec, device=local, folded=fold)
             else:
                 s = arena.Slab(n, world, rank=rank, peer=True, precision=prec, device=local)
             hb = s.peer_handles()
@@ -634,8 +636,6 @@ def run_slab(args, rank, world, local):
     xchg = args.xchg
     note = None
     slab = None
-    if fold and xchg == "peer":
-        xchg, note = "nccl", "the folded pencil runs the NCCL exchange"
     if xchg == "peer":
         slab, err = try_peer()
         if slab is None:  # fall back to the NCCL exchange, and say so

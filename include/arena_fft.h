@@ -229,7 +229,8 @@ arena_status arena_pencil_barrier_status(arena_fft_pencil* pencil);
  * (n/Pr) x (n/Pc) x n block whose local i < n/(2 Pr) is I_r and the rest I_r + n/2
  * (j alike).  The first radix-2 steps of the i and j transforms then run in the
  * rank's z passes and the strided passes are n/2-point (128-byte-row tiles at
- * 2048^3).  Set before the first solve; COPY (NCCL / loopback) exchange only. */
+ * 2048^3).  Set before the first solve (and before arena_pencil_peer_attach); both
+ * exchanges (COPY, PEER) are supported. */
 enum { ARENA_PENCIL_PLAIN = 0, ARENA_PENCIL_FOLDED = 1 };
 arena_status arena_pencil_set_layout(arena_fft_pencil* pencil, int layout);
 

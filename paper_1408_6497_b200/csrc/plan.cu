@@ -1793,8 +1793,10 @@ struct arena_fft_pencil {
   bool attached = false;
   PeerSync sync;
   int fold = 0;  // ARENA_PENCIL_FOLDED (poisson_qpencil.cuh)
-  size_t row_chunk_bytes() const { return size_t(n / Pr) * (n / Pc) * kq * 2 * base->elem; }
-  size_t col_chunk_bytes() const { return size_t(n / Pr) * (n / Pr) * kq * 2 * base->elem; }
+  // bytes of one exchange chunk (folded: of one quadrant's H problem, at the same offset in
+  // each quadrant region)
+  size_t row_chunk_bytes() const { return size_t(n / Pr) * (n / Pc) * kq * 2 * base->elem / (fold ? 4 : 1); }
+  size_t col_chunk_bytes() const { return size_t(n / Pr) * (n / Pr) * kq * 2 * base->elem / (fold ? 4 : 1); }
 };
 
 namespace {
@@ -2143,7 +2145,6 @@ arena_status arena_pencil_set_exchange(arena_fft_pencil* s, int mode) {
   }
   if (mode != ARENA_XCHG_PEER) return fail(ARENA_EINVAL, "unknown exchange mode");
   if (s->Pr * s->Pc > kMaxPeers) return fail(ARENA_EUNSUPPORTED, "peer exchange supports at most 8 ranks");
-  if (s->fold) return fail(ARENA_EUNSUPPORTED, "the folded pencil runs the COPY (NCCL) exchange");
   if (s->loopback) {
     std::vector<std::vector<void*>> bufs;
     for (PencilRank& r : s->ranks) bufs.push_back({r.buf1, r.buf2});
@@ -2158,12 +2159,15 @@ arena_status arena_pencil_set_exchange(arena_fft_pencil* s, int mode) {
 arena_status arena_pencil_set_layout(arena_fft_pencil* s, int layout) {
   if (!s) return fail(ARENA_EINVAL, "pencil is NULL");
   if (layout != ARENA_PENCIL_PLAIN && layout != ARENA_PENCIL_FOLDED) return fail(ARENA_EINVAL, "unknown pencil layout");
-  if (layout == ARENA_PENCIL_FOLDED) {
-    if (s->xmode == ARENA_XCHG_PEER) return fail(ARENA_EUNSUPPORTED, "the folded pencil runs the COPY (NCCL) exchange");
-    if (s->n / 2 / s->Pr < 1 || s->n / 2 / s->Pc < 1 || s->n < 64)
-      return fail(ARENA_EUNSUPPORTED, "folded pencil needs n >= 64 and n/2 divisible by the grid");
-  }
+  if (layout == ARENA_PENCIL_FOLDED && (s->n / 2 / s->Pr < 1 || s->n / 2 / s->Pc < 1 || s->n < 64))
+    return fail(ARENA_EUNSUPPORTED, "folded pencil needs n >= 64 and n/2 divisible by the grid");
+  if (s->attached) return fail(ARENA_EINVAL, "set the pencil layout before arena_pencil_peer_attach");
   s->fold = layout == ARENA_PENCIL_FOLDED ? 1 : 0;
+  if (s->loopback && s->xmode == ARENA_XCHG_PEER) {  // peer chunk offsets depend on the layout
+    std::vector<std::vector<void*>> bufs;
+    for (PencilRank& r : s->ranks) bufs.push_back({r.buf1, r.buf2});
+    for (int rk = 0; rk < int(s->ranks.size()); ++rk) pencil_fill_peers(s, s->ranks[rk], rk, bufs);
+  }
   return ARENA_OK;
 }
 

@@ -27,10 +27,13 @@ namespace arena_fft {
 
 // K1q (folded pencil): r2c of the quad's four rows of the rank's block, the 2x2
 // step with the GLOBAL twiddle W_n^{ci i' + cj j'}, k-split stores into quadrant q's R.
-template <typename T, int NR>
+// PEER: k-chunk c of quadrant q goes straight to row peer c's Y buffer (po.base[c], advanced
+// to this rank's chunk) at quadrant offset q qstride — the row all-to-all fused into K1q.
+template <typename T, int NR, bool PEER = false>
 __global__ void __launch_bounds__(QuadZCfg<T, NR>::THREADS, 2)
     k_zfwd_qpencil(const T* __restrict__ f, vec2_t<T>* __restrict__ R, const vec2_t<T>* __restrict__ tw,
-                   const vec2_t<T>* __restrict__ stw, Layout gz, int i0, int j0, int kq, size_t qstride) {
+                   const vec2_t<T>* __restrict__ stw, Layout gz, int i0, int j0, int kq, size_t qstride,
+                   const __grid_constant__ PeerOut<vec2_t<T>> po) {
   using V = vec2_t<T>;
   using C = QuadZCfg<T, NR>;
   constexpr int M = C::M, E = C::E, P = C::P, TH = C::THREADS, RW = C::RW;
@@ -58,7 +61,11 @@ __global__ void __launch_bounds__(QuadZCfg<T, NR>::THREADS, 2)
   const size_t chunk = size_t(ni) * nj;
   auto put = [&](int q, int k, V x) {
     const int c = k / kq;
-    st_out(R + q * qstride + (size_t(c) * chunk + rin) * kq + (k - c * kq), x);
+    if constexpr (PEER) {
+      po.base[c][q * qstride + rin * kq + (k - c * kq)] = x;
+    } else {
+      st_out(R + q * qstride + (size_t(c) * chunk + rin) * kq + (k - c * kq), x);
+    }
   };
 #pragma unroll
   for (int m = 0; m < M / TH; ++m) {
@@ -88,6 +95,7 @@ __global__ void __launch_bounds__(QuadZCfg<T, NR>::THREADS, 2)
 #pragma unroll
     for (int q = 0; q < 4; ++q) put(q, M, cmul(x[q], wq[q]));
   }
+  if constexpr (PEER) __threadfence_system();  // peer stores performed before the ranks' barrier
 }
 
 // K5q (folded pencil): gather the four quadrants' k-chunked rows, the conjugate

@@ -705,41 +705,78 @@ cudaError_t pencil_fold_phase_n(const PencilArgs& a, int phase) {
     const V* tw = static_cast<const V*>(a.tw);
     cudaError_t e;
     if ((e = ensure_smem<k_zfwd_qpencil<T, NR>>(QC::SMEM, QC::THREADS))) return e;
+    if ((e = ensure_smem<k_zfwd_qpencil<T, NR, true>>(QC::SMEM, QC::THREADS))) return e;
     if ((e = ensure_smem<k_zinv_qpencil<T, NR>>(QC::SMEM, QC::THREADS))) return e;
     alignas(64) CUtensorMap m;
+    // Peer exchange (as the plain pencil: K1 -> row peers' buf2, K2 -> column peers' buf1,
+    // K3 -> column peers' buf2, K4 -> row peers' buf1), quadrant q at q qs in every buffer.
+    const bool peer = a.pz != nullptr;
+    const size_t rows_row = size_t(ni) * nj, rows_col = size_t(ni) * nj2;
+    auto qtable = [&](void* const* peers, int np, size_t chunk_rows, int q) {
+      void* adv[kMaxPeers] = {};
+      for (int c = 0; c < np && c < kMaxPeers; ++c) adv[c] = static_cast<V*>(peers[c]) + q * qs;
+      return peer_table<V>(adv, np, chunk_rows);
+    };
     switch (phase) {
       case kPencilZ1:
-        k_zfwd_qpencil<T, NR><<<unsigned(ni) * nj, QC::THREADS, QC::SMEM, a.stream>>>(
-            static_cast<const T*>(a.f), b1, tw, stw_ptr<T>(pa, 0, QC::E), gz, a.r * ni, a.c * nj, a.kq, qs);
+        if (peer) {
+          k_zfwd_qpencil<T, NR, true><<<unsigned(ni) * nj, QC::THREADS, QC::SMEM, a.stream>>>(
+              static_cast<const T*>(a.f), nullptr, tw, stw_ptr<T>(pa, 0, QC::E), gz, a.r * ni, a.c * nj, a.kq, qs,
+              qtable(a.pz, a.Pc, rows_row, 0));
+        } else {
+          k_zfwd_qpencil<T, NR><<<unsigned(ni) * nj, QC::THREADS, QC::SMEM, a.stream>>>(
+              static_cast<const T*>(a.f), b1, tw, stw_ptr<T>(pa, 0, QC::E), gz, a.r * ni, a.c * nj, a.kq, qs,
+              PeerOut<V>{});
+        }
         break;
-      case kPencilY1:  // Y (buf2) -> B2 (buf1), per quadrant
+      case kPencilY1:  // Y (buf2) -> B2 (buf1); peer: -> column peers' C (buf1), per quadrant
         if (!has_k) break;
         pa.nchunks = a.Pc;
         for (int q = 0; q < 4; ++q) {
           ks.fci = q >> 1;
           ks.fcj = q & 1;
           if ((e = encode_map<T, H>(&m, b2 + q * qs, gY, a.Pc, true, ks.kc, ks.kq))) return e;
-          if ((e = launch_strided_tma<T, H, 0>(pa, m, b2 + q * qs, gY, scale, four_pi2, ks, b1 + q * qs, &gB2))) return e;
+          if (peer) {
+            const PeerOut<V> po = qtable(a.py1, a.Pr, rows_col, q);
+            e = launch_strided_tma<T, H, 0, true>(pa, m, b2 + q * qs, gY, scale, four_pi2, ks, nullptr, &gB2, &po);
+          } else {
+            e = launch_strided_tma<T, H, 0>(pa, m, b2 + q * qs, gY, scale, four_pi2, ks, b1 + q * qs, &gB2);
+          }
+          if (e) return e;
         }
         break;
-      case kPencilX:  // C (buf2) in place, per quadrant
+      case kPencilX:  // C (buf2) in place; peer: C (buf1) -> column peers' B2 (buf2), per quadrant
         if (!has_k) break;
         pa.nchunks = a.Pr;
         for (int q = 0; q < 4; ++q) {
           ks.fci = q >> 1;
           ks.fcj = q & 1;
-          if ((e = encode_map<T, H>(&m, b2 + q * qs, gC, a.Pr, false, ks.kc, ks.kq))) return e;
-          if ((e = launch_strided_tma<T, H, 2>(pa, m, b2 + q * qs, gC, scale, four_pi2, ks))) return e;
+          V* cq = (peer ? b1 : b2) + q * qs;
+          if ((e = encode_map<T, H>(&m, cq, gC, a.Pr, false, ks.kc, ks.kq))) return e;
+          if (peer) {
+            const PeerOut<V> po = qtable(a.px, a.Pr, rows_col, q);
+            e = launch_strided_tma<T, H, 2, true>(pa, m, cq, gC, scale, four_pi2, ks, nullptr, nullptr, &po);
+          } else {
+            e = launch_strided_tma<T, H, 2>(pa, m, cq, gC, scale, four_pi2, ks);
+          }
+          if (e) return e;
         }
         break;
-      case kPencilY2:  // B2 (buf1) -> Y (buf2), per quadrant
+      case kPencilY2:  // B2 (buf1) -> Y (buf2); peer: B2 (buf2) -> row peers' R (buf1), per quadrant
         if (!has_k) break;
         pa.nchunks = a.Pr;
         for (int q = 0; q < 4; ++q) {
           ks.fci = q >> 1;
           ks.fcj = q & 1;
-          if ((e = encode_map<T, H>(&m, b1 + q * qs, gB2, a.Pr, true, ks.kc, ks.kq))) return e;
-          if ((e = launch_strided_tma<T, H, 1>(pa, m, b1 + q * qs, gB2, scale, four_pi2, ks, b2 + q * qs, &gY))) return e;
+          V* bq = (peer ? b2 : b1) + q * qs;
+          if ((e = encode_map<T, H>(&m, bq, gB2, a.Pr, true, ks.kc, ks.kq))) return e;
+          if (peer) {
+            const PeerOut<V> po = qtable(a.py2, a.Pc, rows_row, q);
+            e = launch_strided_tma<T, H, 1, true>(pa, m, bq, gB2, scale, four_pi2, ks, nullptr, &gY, &po);
+          } else {
+            e = launch_strided_tma<T, H, 1>(pa, m, bq, gB2, scale, four_pi2, ks, b2 + q * qs, &gY);
+          }
+          if (e) return e;
         }
         break;
       case kPencilZ2:

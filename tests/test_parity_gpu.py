@@ -562,14 +562,16 @@ def test_pencil_loopback_vs_oracle(cuda, n, pr, pc):
 
 @pytest.mark.parametrize("n,pr,pc", [(64, 2, 2), (64, 1, 4), (128, 2, 4), (128, 4, 2), (256, 2, 2), (256, 2, 1),
                                      (64, 1, 1)])
-def test_pencil_peer_loopback_vs_oracle(cuda, n, pr, pc):
+@pytest.mark.parametrize("folded", [False, True])
+def test_pencil_peer_loopback_vs_oracle(cuda, n, pr, pc, folded):
     """Pencil with the exchanges fused into K1-K4 (peer stores into the row / column
-    peers' buffers), Pr x Pc virtual ranks on one GPU, against the oracle."""
+    peers' buffers), Pr x Pc virtual ranks on one GPU, plain and folded layouts,
+    against the oracle."""
     torch = cuda
     f_np = np.random.default_rng(7 * n + 10 * pr + pc).uniform(-1, 1, (n, n, n))
     f = torch.from_numpy(f_np).cuda()
     u = torch.empty_like(f)
-    p = arena.Pencil(n, pr, pc, loopback=True)
+    p = arena.Pencil(n, pr, pc, loopback=True, folded=folded)
     p.set_exchange(arena.XCHG_PEER)
     p.solve_device(f, u)
     torch.cuda.synchronize()
@@ -587,7 +589,7 @@ def test_pencil_peer_loopback_1024_2x4_analytic(cuda):
     assert r["rel_l2"] <= 1e-12, r
 
 
-def _pencil_ipc_rank(rank, world, port, n, pr, pc, f_np, out):
+def _pencil_ipc_rank(rank, world, port, n, pr, pc, f_np, out, folded=False):
     import os
 
     import torch
@@ -599,10 +601,15 @@ def _pencil_ipc_rank(rank, world, port, n, pr, pc, f_np, out):
     torch.cuda.set_device(0)
     ni, nj = n // pr, n // pc
     r, c = rank // pc, rank % pc
-    blk = np.ascontiguousarray(f_np[r * ni:(r + 1) * ni, c * nj:(c + 1) * nj])
+    if folded:  # the rank's four (I_r or I_r + H) x (J_c or J_c + H) sub-blocks
+        blk = np.empty((ni, nj, n))
+        for gi, gj, li, lj, bi, bj in arena.fold_blocks(n, pr, pc, r, c):
+            blk[li:li + bi, lj:lj + bj] = f_np[gi:gi + bi, gj:gj + bj]
+    else:
+        blk = np.ascontiguousarray(f_np[r * ni:(r + 1) * ni, c * nj:(c + 1) * nj])
     f = torch.from_numpy(blk).cuda()
     u = torch.empty_like(f)
-    p = arena.Pencil(n, pr, pc, rank=rank, peer=True, device=0)
+    p = arena.Pencil(n, pr, pc, rank=rank, peer=True, device=0, folded=folded)
     hs = [None] * world
     dist.all_gather_object(hs, p.peer_handles())
     p.peer_attach(b"".join(hs))
@@ -616,17 +623,22 @@ def _pencil_ipc_rank(rank, world, port, n, pr, pc, f_np, out):
         full = np.empty((n, n, n))
         for q, b in enumerate(us):
             rr, cc = q // pc, q % pc
-            full[rr * ni:(rr + 1) * ni, cc * nj:(cc + 1) * nj] = b
+            if folded:
+                for gi, gj, li, lj, bi, bj in arena.fold_blocks(n, pr, pc, rr, cc):
+                    full[gi:gi + bi, gj:gj + bj] = b[li:li + bi, lj:lj + bj]
+            else:
+                full[rr * ni:(rr + 1) * ni, cc * nj:(cc + 1) * nj] = b
         out.copy_(torch.from_numpy(full.ravel()))
     dist.barrier()
     p.close()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("pr,pc", [(1, 2), (2, 1)])
-def test_pencil_peer_ipc_two_processes(cuda, pr, pc):
-    """Two processes sharing this GPU as a 1x2 / 2x1 pencil grid, buffers mapped
-    with CUDA IPC, peer-store kernels, host barriers between the phases."""
+@pytest.mark.parametrize("pr,pc,folded", [(1, 2, False), (2, 1, False), (1, 2, True), (2, 1, True)])
+def test_pencil_peer_ipc_two_processes(cuda, pr, pc, folded):
+    """Two processes sharing this GPU as a 1x2 / 2x1 pencil grid (plain and folded
+    layouts), buffers mapped with CUDA IPC, peer-store kernels, host barriers between
+    the phases."""
     import socket
 
     import torch.multiprocessing as mp
@@ -639,7 +651,7 @@ def test_pencil_peer_ipc_two_processes(cuda, pr, pc):
     sock.bind(("127.0.0.1", 0))
     port = sock.getsockname()[1]
     sock.close()
-    mp.spawn(_pencil_ipc_rank, args=(2, port, n, pr, pc, f_np, out), nprocs=2, join=True)
+    mp.spawn(_pencil_ipc_rank, args=(2, port, n, pr, pc, f_np, out, folded), nprocs=2, join=True)
     assert _rel(out.numpy().reshape(n, n, n), oracle.poisson_solve(f_np)) <= TOL64
 
 
@@ -897,13 +909,15 @@ def test_folded_pencil_nccl_single_rank(cuda):
     s.close()
 
 
-@pytest.mark.parametrize("pr,pc", [(2, 2), (2, 4)])
-def test_folded_pencil_1024_analytic(cuda, pr, pc):
+@pytest.mark.parametrize("pr,pc,xchg", [(2, 2, "copy"), (2, 4, "copy"), (2, 4, "peer")])
+def test_folded_pencil_1024_analytic(cuda, pr, pc, xchg):
     """Config-4 source at 1024^3 through the folded 2x2 / 2x4 pencil (loopback) vs analytic."""
     torch = cuda
     src, f, ua = _config_device(torch, 4)
     u = torch.empty_like(f)
     s = arena.Pencil(1024, pr, pc, loopback=True, folded=True)
+    if xchg == "peer":
+        s.set_exchange(arena.XCHG_PEER)
     s.solve_device(f, u)
     torch.cuda.synchronize()
     e = (torch.linalg.vector_norm(u - ua) / torch.linalg.vector_norm(ua)).item()

@@ -75,3 +75,21 @@ def test_host_field_matches_direct_evaluation(n):
         for which in "fu":
             a, b = problems.host_field(src, which), problems.eval_host(src, which)
             assert np.abs(a - b).max() <= 1e-14 * np.abs(b).max()
+
+
+def test_bench_reference_arm_small():
+    """--impl reference at a small n: one JSON line, the same workload as the GPU arm
+    (same_config), a 1-core and a pocketfft line, and no repo CUDA library mapped."""
+    r = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference", "--n", "80",
+                        "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=REPO)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["config"]["same_config"] and d["config"]["n"] == 80
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"] > 0
+    cb = d["cpu_baseline"]
+    assert cb["value"] == d["value"] and cb["one_core"]["cores"] == 1 and cb["b_all"]["rel_l2_vs_reference"] < 1e-13
+    assert d["parity"]["rel_l2_vs_analytic"] < 1e-12
+    assert not any(m.startswith("paper_1408_6497_b200") for m in d["repo_libs_mapped"])
+    assert "invalid" not in d

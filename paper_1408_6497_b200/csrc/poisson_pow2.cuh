@@ -221,6 +221,25 @@ __device__ __forceinline__ V* smem_base() {
 }
 
 
+// W_n^k, k = t + P e, for the r2c / c2r split of an n = 2 P E point row: the thread's
+// W_n^t times the compile-time root W_{2E}^e (e is constant once the caller's loop is
+// unrolled) — one complex product instead of a table load per element, off the
+// L1TEX pipe the z kernels are bound by (ncu: l1tex 88%).  ARENA_Z_TWREC = 0: loads.
+#ifndef ARENA_Z_TWREC
+#define ARENA_Z_TWREC 1
+#endif
+template <int E, typename V>
+__device__ __forceinline__ V split_twiddle(const V* __restrict__ tw, V wt, int k, int e) {
+  if constexpr (ARENA_Z_TWREC && E <= 32) {
+    using T = decltype(wt.x);
+    const int m = (e * (32 / E)) & 63;  // W_{2E}^e = W_64^{e 32 / E}
+    const T c = T(cos64(m)), s = T(-sin64(m));
+    return V{fma(wt.x, c, -wt.y * s), fma(wt.x, s, wt.y * c)};
+  } else {
+    return tw_load(tw, k);
+  }
+}
+
 // ------------------------------------------------------------------- K1 zfwd
 // Rows of NR reals: z[m] = f[2m] + i f[2m+1] (one vector load), M-point FFT,
 // then X[k] = 1/2 (A + B) - 1/2 i W_n^k (A - B), A = Z[k], B = conj(Z[M-k]),
@@ -246,13 +265,14 @@ __device__ __forceinline__ void zfwd_rows(const T* __restrict__ f, vec2_t<T>* __
   for (int e = 0; e < E; ++e) sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
   xbarrier<SYNC>();
   V* dst = S + rowB(g, int(row / NR), int(row % NR)) * ncp;
+  const V wt = tw_load(tw, t);  // W_n^t (split_twiddle)
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int k = t + P * e;
     const V A = v[e];
     const V Bc = sm[smem_idx<L, SW, V>((M - k) & (M - 1), l)];
     const V B{Bc.x, -Bc.y};
-    const V W = tw_load(tw, k);  // W_n^k
+    const V W = split_twiddle<E>(tw, wt, k, e);  // W_n^k
     const V WD = cmul(W, csub(A, B));
     dst[k] = V{T(0.5) * (A.x + B.x + WD.y), T(0.5) * (A.y + B.y - WD.x)};
     if (k == 0) dst[M] = V{A.x - A.y, T(0)};
@@ -308,6 +328,7 @@ __device__ __forceinline__ void zinv_rows(const vec2_t<T>* __restrict__ S, T* __
     constexpr int LINES = ncp * int(sizeof(V)) / 128;
     for (int q = t; q < LINES; q += P) l2_discard(reinterpret_cast<const char*>(src) + size_t(q) * 128);
   }
+  const V wt = tw_load(tw, t);  // W_n^t (split_twiddle)
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int k = t + P * e;
@@ -318,7 +339,7 @@ __device__ __forceinline__ void zinv_rows(const vec2_t<T>* __restrict__ S, T* __
       Bs.y = T(0);
     }
     const V B{Bs.x, -Bs.y};
-    const V W = tw_load(tw, k);
+    const V W = split_twiddle<E>(tw, wt, k, e);
     const V Ep = cadd(A, B);
     const V Op = cmulc(csub(A, B), W);
     v[e] = V{Ep.x - Op.y, Ep.y + Op.x};
@@ -868,13 +889,14 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::M
       R[(size_t(c) * chunk + rin) * kq + (k - c * kq)] = x;
     }
   };
+  const V wt = tw_load(tw, t);  // W_n^t (split_twiddle)
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int k = t + P * e;
     const V A = v[e];
     const V Bc = sm[smem_idx<L, SW, V>((M - k) & (M - 1), l)];
     const V B{Bc.x, -Bc.y};
-    const V W = tw_load(tw, k);
+    const V W = split_twiddle<E>(tw, wt, k, e);
     const V WD = cmul(W, csub(A, B));
     put(k, V{T(0.5) * (A.x + B.x + WD.y), T(0.5) * (A.y + B.y - WD.x)});
     if (k == 0) put(M, V{A.x - A.y, T(0)});
@@ -918,6 +940,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::M
   }
   if (t == 0) xm[l] = get(M);
   __syncthreads();
+  const V wt = tw_load(tw, t);  // W_n^t (split_twiddle)
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int k = t + P * e;
@@ -928,7 +951,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::M
       Bs.y = T(0);
     }
     const V B{Bs.x, -Bs.y};
-    const V W = tw_load(tw, k);
+    const V W = split_twiddle<E>(tw, wt, k, e);
     const V Ep = cadd(A, B);
     const V Op = cmulc(csub(A, B), W);
     v[e] = V{Ep.x - Op.y, Ep.y + Op.x};

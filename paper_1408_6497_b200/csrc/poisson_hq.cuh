@@ -45,7 +45,7 @@ struct HqZCfg {
   static constexpr int L = 2 * JR;
   static constexpr int THREADS = L * P;
   static constexpr int SYNC = THREADS <= 32 ? kSyncWarp : kSyncCta;
-  static constexpr int MINB = imax(1, ContigCfg<T, NR>::MINB * ContigCfg<T, NR>::THREADS / THREADS);
+  static constexpr int MINB = imin(32, imax(1, ContigCfg<T, NR>::MINB * ContigCfg<T, NR>::THREADS / THREADS));
   static constexpr int SMEM = (M * L + L) * 2 * int(sizeof(T));
   static constexpr int PF = ARENA_Z_PF * ARENA_SMS * MINB;  // L2 prefetch distance (CTAs)
   static constexpr bool OK = NR >= 16 && THREADS <= 1024;

@@ -228,13 +228,37 @@ __device__ __forceinline__ V* smem_base() {
 #ifndef ARENA_Z_TWREC
 #define ARENA_Z_TWREC 1
 #endif
+// W_64^m = exp(-2 pi i m / 64) in the constant cache: split_twiddle's index is warp-uniform
+// (the unrolled loop's e), so each read is one broadcast LDC, not an L1TEX request.
+#define ARENA_W64(m) {cos64(m), -sin64(m)}
+static __constant__ double2 kW64d[64] = {
+    ARENA_W64(0), ARENA_W64(1), ARENA_W64(2), ARENA_W64(3), ARENA_W64(4), ARENA_W64(5), ARENA_W64(6), ARENA_W64(7),
+    ARENA_W64(8), ARENA_W64(9), ARENA_W64(10), ARENA_W64(11), ARENA_W64(12), ARENA_W64(13), ARENA_W64(14), ARENA_W64(15),
+    ARENA_W64(16), ARENA_W64(17), ARENA_W64(18), ARENA_W64(19), ARENA_W64(20), ARENA_W64(21), ARENA_W64(22), ARENA_W64(23),
+    ARENA_W64(24), ARENA_W64(25), ARENA_W64(26), ARENA_W64(27), ARENA_W64(28), ARENA_W64(29), ARENA_W64(30), ARENA_W64(31),
+    ARENA_W64(32), ARENA_W64(33), ARENA_W64(34), ARENA_W64(35), ARENA_W64(36), ARENA_W64(37), ARENA_W64(38), ARENA_W64(39),
+    ARENA_W64(40), ARENA_W64(41), ARENA_W64(42), ARENA_W64(43), ARENA_W64(44), ARENA_W64(45), ARENA_W64(46), ARENA_W64(47),
+    ARENA_W64(48), ARENA_W64(49), ARENA_W64(50), ARENA_W64(51), ARENA_W64(52), ARENA_W64(53), ARENA_W64(54), ARENA_W64(55),
+    ARENA_W64(56), ARENA_W64(57), ARENA_W64(58), ARENA_W64(59), ARENA_W64(60), ARENA_W64(61), ARENA_W64(62), ARENA_W64(63)};
+static __constant__ float2 kW64f[64] = {
+    ARENA_W64(0), ARENA_W64(1), ARENA_W64(2), ARENA_W64(3), ARENA_W64(4), ARENA_W64(5), ARENA_W64(6), ARENA_W64(7),
+    ARENA_W64(8), ARENA_W64(9), ARENA_W64(10), ARENA_W64(11), ARENA_W64(12), ARENA_W64(13), ARENA_W64(14), ARENA_W64(15),
+    ARENA_W64(16), ARENA_W64(17), ARENA_W64(18), ARENA_W64(19), ARENA_W64(20), ARENA_W64(21), ARENA_W64(22), ARENA_W64(23),
+    ARENA_W64(24), ARENA_W64(25), ARENA_W64(26), ARENA_W64(27), ARENA_W64(28), ARENA_W64(29), ARENA_W64(30), ARENA_W64(31),
+    ARENA_W64(32), ARENA_W64(33), ARENA_W64(34), ARENA_W64(35), ARENA_W64(36), ARENA_W64(37), ARENA_W64(38), ARENA_W64(39),
+    ARENA_W64(40), ARENA_W64(41), ARENA_W64(42), ARENA_W64(43), ARENA_W64(44), ARENA_W64(45), ARENA_W64(46), ARENA_W64(47),
+    ARENA_W64(48), ARENA_W64(49), ARENA_W64(50), ARENA_W64(51), ARENA_W64(52), ARENA_W64(53), ARENA_W64(54), ARENA_W64(55),
+    ARENA_W64(56), ARENA_W64(57), ARENA_W64(58), ARENA_W64(59), ARENA_W64(60), ARENA_W64(61), ARENA_W64(62), ARENA_W64(63)};
+#undef ARENA_W64
+__device__ __forceinline__ double2 w64(int m, double) { return kW64d[m]; }
+__device__ __forceinline__ float2 w64(int m, float) { return kW64f[m]; }
+
 template <int E, typename V>
 __device__ __forceinline__ V split_twiddle(const V* __restrict__ tw, V wt, int k, int e) {
   if constexpr (ARENA_Z_TWREC && E <= 32) {
     using T = decltype(wt.x);
-    const int m = (e * (32 / E)) & 63;  // W_{2E}^e = W_64^{e 32 / E}
-    const T c = T(cos64(m)), s = T(-sin64(m));
-    return V{fma(wt.x, c, -wt.y * s), fma(wt.x, s, wt.y * c)};
+    const V r = w64((e * (32 / E)) & 63, T(0));  // W_{2E}^e = W_64^{e 32 / E}
+    return cmul(wt, r);
   } else {
     return tw_load(tw, k);
   }

@@ -325,11 +325,15 @@ __device__ __forceinline__ void stage_compute(V (&v)[E], int t, TW stw) {
 
 // Barrier scope of the exchanges: the whole CTA, or one warp when a warp owns
 // its lines and their shared-memory region exclusively.
+// SYNC >= 32: a group of SYNC consecutive threads of the CTA on its own named barrier
+// (id 1 + group index), the groups running independently of each other.
 enum { kSyncCta = 0, kSyncWarp = 1 };
 template <int SYNC>
 __device__ __forceinline__ void xbarrier() {
   if constexpr (SYNC == kSyncWarp) {
     __syncwarp();
+  } else if constexpr (SYNC >= 32) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + int(threadIdx.x) / SYNC), "r"(SYNC) : "memory");
   } else {
     __syncthreads();
   }
@@ -343,26 +347,57 @@ struct NoHook {
 
 // Write stage outputs to shared memory at their Stockham destinations and
 // read back the natural-order inputs of the next stage.
-template <int N, int E, int L, int R, int NS, int SW, int SYNC, typename V, typename HK = NoHook>
+// XS = 1 ("split exchange"): `sm` holds only N*L real scalars — half a tile — and
+// the real and the imaginary parts go through it one after the other.  The
+// strided passes then keep their full-size TMA tile buffer as a pure landing
+// zone, free for the next tile's load as soon as the tile is in registers.
+template <int N, int E, int L, int R, int NS, int SW, int SYNC, typename V, typename HK = NoHook, int XS = 0>
 __device__ __forceinline__ void stage_exchange(V (&v)[E], V* sm, int t, int l, const HK& hook = HK{}) {
   constexpr int P = N / E, NB = E / R;
+  if constexpr (XS) {
+    using T = decltype(v[0].x);
+    T* ss = reinterpret_cast<T*>(sm);
 #pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    const int b = t + P * q;
-    const int dst = (b & ~(NS - 1)) * R + (b & (NS - 1));
+    for (int q = 0; q < NB; ++q) {
+      const int b = t + P * q;
+      const int dst = (b & ~(NS - 1)) * R + (b & (NS - 1));
 #pragma unroll
-    for (int r = 0; r < R; ++r) sm[smem_idx<L, SW, V>(dst + r * NS, l)] = v[q + NB * r];
+      for (int r = 0; r < R; ++r) ss[smem_idx<L, SW, T>(dst + r * NS, l)] = v[q + NB * r].x;
+    }
+    xbarrier<SYNC>();
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e].x = ss[smem_idx<L, SW, T>(t + P * e, l)];
+    xbarrier<SYNC>();
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      const int b = t + P * q;
+      const int dst = (b & ~(NS - 1)) * R + (b & (NS - 1));
+#pragma unroll
+      for (int r = 0; r < R; ++r) ss[smem_idx<L, SW, T>(dst + r * NS, l)] = v[q + NB * r].y;
+    }
+    xbarrier<SYNC>();
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e].y = ss[smem_idx<L, SW, T>(t + P * e, l)];
+    xbarrier<SYNC>();
+  } else {
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      const int b = t + P * q;
+      const int dst = (b & ~(NS - 1)) * R + (b & (NS - 1));
+#pragma unroll
+      for (int r = 0; r < R; ++r) sm[smem_idx<L, SW, V>(dst + r * NS, l)] = v[q + NB * r];
+    }
+    xbarrier<SYNC>();
+    hook();
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = sm[smem_idx<L, SW, V>(t + P * e, l)];
+    xbarrier<SYNC>();
+    hook();
   }
-  xbarrier<SYNC>();
-  hook();
-#pragma unroll
-  for (int e = 0; e < E; ++e) v[e] = sm[smem_idx<L, SW, V>(t + P * e, l)];
-  xbarrier<SYNC>();
-  hook();
 }
 
 template <int N, int E, int L, int S, int SYNC, int STAGE, typename V, typename TW, int STOP = num_stages(N, E),
-          typename HK = NoHook>
+          typename HK = NoHook, int XS = 0>
 __device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, TW stw, int t, int l, const HK& hook = HK{}) {
   constexpr int NSTAGE = num_stages(N, E);
   if constexpr (STAGE < STOP) {
@@ -370,9 +405,15 @@ __device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, TW stw, int t, int 
     constexpr int NS = stage_ns(N, E, STAGE);
     constexpr int SW = stage_log2(N, E, 0);
     stage_compute<N, E, R, NS, S>(v, t, stw + (STAGE >= 1 ? stage_tw_offset(N, E, STAGE) : 0));
-    if constexpr (STAGE + 1 < NSTAGE) stage_exchange<N, E, L, R, NS, SW, SYNC>(v, sm, t, l, hook);
-    fft_stages<N, E, L, S, SYNC, STAGE + 1, V, TW, STOP>(v, sm, stw, t, l, hook);
+    if constexpr (STAGE + 1 < NSTAGE) stage_exchange<N, E, L, R, NS, SW, SYNC, V, HK, XS>(v, sm, t, l, hook);
+    fft_stages<N, E, L, S, SYNC, STAGE + 1, V, TW, STOP, HK, XS>(v, sm, stw, t, l, hook);
   }
+}
+
+// Line FFT with the split exchange (XS above): `sm` is a scratch of N*L real scalars.
+template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V, typename TW>
+__device__ __forceinline__ void line_fft_xs(V (&v)[E], V* sm, TW stw, int t, int l) {
+  fft_stages<N, E, L, S, SYNC, 0, V, TW, num_stages(N, E), NoHook, 1>(v, sm, stw, t, l);
 }
 
 // Full N-point line FFT of the tile.  On entry and exit thread (l, t) holds

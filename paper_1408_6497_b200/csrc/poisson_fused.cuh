@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(FusedCfg<T, N>::THREADS, FusedCfg<T, N>::MINB)
         fence_proxy_async_global();  // acquired generic-proxy writes before the TMA read
         fence_proxy_async_smem();    // this CTA's generic shared accesses before the TMA write
         mbar_arrive_expect_tx(bar, TILE_BYTES);
-        tma_load_5d(sm, &tmap, bar, 2 * kt * L, 0, il, 0, 0);
+        ytile_half_load(sm, &tmap, bar, g, 1, 2 * kt * L, il, 0, 0, TILE_BYTES);
+        ytile_half_load(sm, &tmap, bar, g, 1, 2 * kt * L, il, 0, 1, TILE_BYTES);
       }
       mbar_wait(bar, phase);
       phase ^= 1;

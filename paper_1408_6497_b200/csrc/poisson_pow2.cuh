@@ -517,6 +517,21 @@ namespace arena_fft {
 #ifndef ARENA_TMA_NBUF_Y
 #define ARENA_TMA_NBUF_Y ARENA_TMA_NBUF
 #endif
+#ifndef ARENA_TMA_HX_X
+#define ARENA_TMA_HX_X 0  // x pass: split exchange for tiles of at least this many bytes (0: never; B200 1024^3
+                          // fp64 at 131072: x 4.35 -> 4.50 ms, y at 131072: 3.23 -> 3.87 ms — the passes are not
+                          // waiting for their loads, and the exchange costs twice the LDS/STS and barriers)
+#endif
+#ifndef ARENA_TMA_HX_Y
+#define ARENA_TMA_HX_Y 0  // y passes: same
+#endif
+#ifndef ARENA_TMA_E2S_X
+#define ARENA_TMA_E2S_X 1  // x pass: last exchange shifted into spare shared memory, first half of the next
+#endif                     // tile requested before it
+#ifndef ARENA_TMA_E2S_Y
+#define ARENA_TMA_E2S_Y 0  // y passes: same (B200 1024^3 fp64: y 3.06 -> 3.21 ms — they run at ~90% of their access
+                           // pattern's bandwidth cap and wait on DRAM, not on a late request)
+#endif
 #ifndef ARENA_TMA_EARLY_Y
 #define ARENA_TMA_EARLY_Y 1  // y passes: request the next tile right after the last exchange
 #endif
@@ -595,7 +610,22 @@ struct TmaCfg {
   static constexpr int NB0 = YP ? ARENA_TMA_NBUF_Y : ARENA_TMA_NBUF;
   static constexpr int NBUF = (NB0 * TILE * VB <= 200 * 1024) ? NB0 : imin(2, NB0);
   static constexpr int TW = stage_tw_total(N, E);  // staged twiddle entries (x pass)
-  static constexpr int SMEM = NBUF * TILE * VB + 8 * NBUF;
+  // Split exchange (fft_engine.cuh, XS): a separate half-tile scratch takes the real and
+  // the imaginary parts in turn, so the tile buffer is only the TMA landing zone and the
+  // next tile is requested as soon as this one is in registers — its load overlaps the
+  // whole transform instead of the last stage only.
+  static constexpr int HXW = YP ? ARENA_TMA_HX_Y : ARENA_TMA_HX_X;
+  static constexpr bool HX = HXW != 0 && NBUF == 1 && num_stages(N, E) > 1 && TILE * VB >= HXW &&
+                             MINB * (TILE * VB * 3 / 2 + (!YP && ARENA_TMA_TWSMEM_X ? TW * VB : 0) + 1024 + 64) <= 228 * 1024;
+  // Shifted last exchange (E2S): half a tile of spare shared memory behind the tile buffer.
+  // The pass's last exchange runs in [TILE/2, 3 TILE/2) instead of [0, TILE), so the first
+  // half of the next tile is requested before it (right after the previous exchange, or
+  // after the tile read when there is none) and only the second half has to wait for it:
+  // the strided passes spent 9% (x) / 13% (y) of their time waiting for the tile (ncu).
+  static constexpr int E2SW = YP ? ARENA_TMA_E2S_Y : ARENA_TMA_E2S_X;
+  static constexpr bool E2S = E2SW != 0 && !HX && NBUF == 1 && num_stages(N, E) > 1 && N >= 4 &&
+                              MINB * (TILE * VB * 3 / 2 + (!YP && ARENA_TMA_TWSMEM_X ? TW * VB : 0) + 1024 + 64) <= 228 * 1024;
+  static constexpr int SMEM = NBUF * TILE * VB + 16 * NBUF + ((HX || E2S) ? TILE * VB / 2 : 0);
   static constexpr int SMEM_X = SMEM + (ARENA_TMA_TWSMEM_X ? TW * VB : 0);
   static constexpr int SMEM_Y = SMEM + (ARENA_TMA_TWSMEM_Y ? TW * VB : 0);
 };
@@ -605,6 +635,34 @@ struct TmaCfg {
 // y tile (fixed il): box {2L, JB, 1, nj/JB, P}  -> all j in natural order.
 // x tile (fixed jl): boxes {2L, 1, IB, 1, 1} over il blocks and chunks -> all i.
 __host__ __device__ constexpr int tma_ib(int ni) { return ni < 256 ? ni : 256; }
+
+// A y tile is fetched as two half boxes (so the first half can be requested ahead of the
+// second, E2S): split over the chunks (dimension 4) when it spans several, else over the
+// j blocks (dimension 3) when there are at least two, else one whole box (returns 0).
+// nch = chunks a y tile spans (1 for the chunked single-GPU layouts).  encode_map builds
+// the box by the same rule.
+__host__ __device__ __forceinline__ int ytile_split(const Layout& g, int nch) {
+  return nch >= 2 ? 4 : ((g.nj >> g.jbs) >= 2 ? 3 : 0);
+}
+// Half h (0 / 1) of y tile (k offset c0 reals, line `outer`, chunk qd) into dst_tile; with an
+// unsplit box, half 1 is the whole tile and half 0 empty (half 0 may be requested while the
+// upper half of the tile buffer is still exchange scratch).  The caller posts the bytes
+// (ytile_half_bytes) on `bar` first.
+__host__ __device__ __forceinline__ uint32_t ytile_half_bytes(const Layout& g, int nch, int h, uint32_t tile_bytes) {
+  return ytile_split(g, nch) ? tile_bytes / 2 : (h ? tile_bytes : 0u);
+}
+template <typename V>
+__device__ __forceinline__ void ytile_half_load(V* dst_tile, const CUtensorMap* tmap, uint64_t* bar, const Layout& g,
+                                                int nch, int c0, int outer, int qd, int h, uint32_t tile_bytes) {
+  const int sd = ytile_split(g, nch);
+  if (sd == 0) {
+    if (h == 1) tma_load_5d(dst_tile, tmap, bar, c0, 0, outer, 0, qd);
+  } else {
+    const int c3 = sd == 3 ? h * ((g.nj >> g.jbs) / 2) : 0;
+    const int c4 = sd == 4 ? h * (nch / 2) : qd;
+    tma_load_5d(reinterpret_cast<char*>(dst_tile) + size_t(h) * (tile_bytes / 2), tmap, bar, c0, 0, outer, c3, c4);
+  }
+}
 
 // The k range a workspace holds: local k in [0, kc), row pitch kq complex,
 // global k = k0 + local k.  One GPU and slab: {nc, ncp, 0}; pencil: the rank's
@@ -692,15 +750,19 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
   const int NL = (ks.no ? ks.no : (PASS < 2 ? g.ni : g.nj)) * KT;  // tiles per chunk (QUAD) / in all
   const int NT = NL * NCH;
   constexpr bool TWS = PASS == 2 ? bool(ARENA_TMA_TWSMEM_X) : bool(ARENA_TMA_TWSMEM_Y);
+  constexpr bool HX = C::HX;
+  constexpr bool E2S = C::E2S;
+  constexpr int NST = num_stages(N, E);
   V* bufs = smem_base<V>();
-  V* tws = bufs + NBUF * TILE;
+  V* scratch = bufs + NBUF * TILE;  // HX: TILE real scalars; E2S: half a tile behind the tile buffer
+  V* tws = scratch + ((HX || C::E2S) ? TILE / 2 : 0);
   uint64_t* bar = reinterpret_cast<uint64_t*>(tws + (TWS ? C::TW : 0));
   const int tid = threadIdx.x;
   const int l = tid % L, t = tid / L;
 
   if (tid == 0) {
 #pragma unroll
-    for (int b = 0; b < NBUF; ++b) mbar_init(&bar[b], 1);
+    for (int b = 0; b < NBUF + (E2S ? 1 : 0); ++b) mbar_init(&bar[b], 1);
     fence_mbar_init();
   }
   if constexpr (TWS) {
@@ -718,14 +780,37 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
     if constexpr (QUAD) gt -= qd * NL;
     const int outer = gt / KT, kt = gt % KT;
     mbar_arrive_expect_tx(b, TILE_BYTES);
-    if constexpr (PASS < 2) {  // y tile: fixed il = outer, all j (QUAD: of chunk qd)
-      tma_load_5d(dst, &tmap, b, 2 * kt * L, 0, outer, 0, qd);
+    if constexpr (PASS < 2) {  // y tile: fixed il = outer, all j (QUAD: of chunk qd), two half boxes
+      ytile_half_load(dst, &tmap, b, g, QUAD ? 1 : nchunks, 2 * kt * L, outer, qd, 0, TILE_BYTES);
+      ytile_half_load(dst, &tmap, b, g, QUAD ? 1 : nchunks, 2 * kt * L, outer, qd, 1, TILE_BYTES);
     } else {  // x tile: fixed jl = outer, all i (chunk c, il blocks of IB)
       const int IB = tma_ib(g.ni);
       const int jb = (1 << g.jbs) - 1;
       for (int c = qd; c < (QUAD ? qd + 1 : nchunks); ++c)
         for (int q = 0; q < g.ni; q += IB)
           tma_load_5d(dst + (size_t(c - qd) * g.ni + q) * L, &tmap, b, 2 * kt * L, outer & jb, q, outer >> g.jbs, c);
+    }
+  };
+  // E2S (x pass): half h of a tile = boxes [h NBX/2, (h + 1) NBX/2) of its NBX = chunks * ni/IB
+  // boxes, completing bar[h]; with an odd box count (one box) the whole tile is half 1.
+  auto issue_half = [&](int gt, int h) {
+    const int qd = QUAD ? gt / NL : 0;
+    if constexpr (QUAD) gt -= qd * NL;
+    const int outer = gt / KT, kt = gt % KT;
+    if constexpr (PASS < 2) {
+      mbar_arrive_expect_tx(&bar[h], ytile_half_bytes(g, QUAD ? 1 : nchunks, h, TILE_BYTES));
+      ytile_half_load(bufs, &tmap, &bar[h], g, QUAD ? 1 : nchunks, 2 * kt * L, outer, qd, h, TILE_BYTES);
+      return;
+    }
+    const int IB = tma_ib(g.ni);
+    const int jb = (1 << g.jbs) - 1;
+    const int nbq = g.ni / IB, nbx = (QUAD ? 1 : nchunks) * nbq;
+    const bool split = (nbx & 1) == 0;
+    const int lo = split ? h * (nbx / 2) : (h ? 0 : nbx), hi = split ? lo + nbx / 2 : nbx;
+    mbar_arrive_expect_tx(&bar[h], uint32_t(hi - lo) * uint32_t(IB * L * sizeof(V)));
+    for (int bx = lo; bx < hi; ++bx) {
+      const int c = bx / nbq, q = (bx - c * nbq) * IB;
+      tma_load_5d(bufs + (size_t(c) * g.ni + q) * L, &tmap, &bar[h], 2 * kt * L, outer & jb, q, outer >> g.jbs, qd + c);
     }
   };
   auto prefetch = [&](int gt) {  // same boxes, into L2 only
@@ -758,8 +843,13 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
   // the load overlaps that iteration's last FFT stage and stores (B200: x 4.95
   // -> 4.32 ms).  The y passes measured 40% slower that way and request their
   // tile at the top of each iteration instead.
-  constexpr bool EARLY = NBUF == 1 && (PASS == 2 || ARENA_TMA_EARLY_Y);
-  if constexpr (EARLY) {
+  constexpr bool EARLY = NBUF == 1 && (PASS == 2 || ARENA_TMA_EARLY_Y || HX || E2S);
+  if constexpr (E2S) {
+    if (tid == 0 && gt < NT) {
+      issue_half(gt, 0);
+      issue_half(gt, 1);
+    }
+  } else if constexpr (EARLY) {
     if (tid == 0 && gt < NT) issue(gt, bufs, &bar[0]);
   }
   for (int it = 0; gt < NT; ++it, gt += gridDim.x) {
@@ -783,16 +873,31 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
       }
     }
     mbar_wait(&bar[b], (it / NBUF) & 1);
+    if constexpr (E2S) mbar_wait(&bar[1], it & 1);
     V v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = cur[(t + P * e) * L + l];
-    __syncthreads();  // the tile buffer becomes exchange scratch
+    __syncthreads();  // the tile buffer becomes exchange scratch (HX: is free for the next tile)
+    if constexpr (HX) {
+      const int gn = gt + gridDim.x;
+      if (tid == 0 && gn < NT) {
+        fence_proxy_async_smem();
+        issue(gn, bufs, &bar[0]);
+      }
+    }
     const int qd = QUAD ? gt / NL : 0;
     const int gl = QUAD ? gt - qd * NL : gt;
     const int outer = gl / KT;
     const int k = (gl % KT) * L + l;
+    auto release_half = [&](int h) {  // E2S: the half's region is free
+      const int gn = gt + gridDim.x;
+      if (tid == 0 && gn < NT) {
+        fence_proxy_async_smem();
+        issue_half(gn, h);
+      }
+    };
     auto release = [&]() {  // buffer free (all exchange reads done): request the next tile
-      if constexpr (EARLY) {
+      if constexpr (EARLY && !HX && !E2S) {
         const int gn = gt + gridDim.x;
         if (tid == 0 && gn < NT) {
           fence_proxy_async_smem();
@@ -800,7 +905,21 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
         }
       }
     };
-    if constexpr (PASS == 0) {
+    if constexpr (PASS == 0 && HX) {
+      line_fft_xs<N, E, L, -1>(v, scratch, twp, t, l);
+    } else if constexpr (PASS == 1 && HX) {
+      line_fft_xs<N, E, L, +1>(v, scratch, twp, t, l);
+    } else if constexpr (PASS < 2 && E2S) {
+      // every exchange but the last in the tile buffer, then the first half of the next tile is
+      // requested; the last exchange in the upper half + the spare half tile, then the second half
+      constexpr int SG = PASS == 0 ? -1 : +1;
+      V* sm2 = cur + TILE / 2;
+      if constexpr (NST > 2) fft_stages<N, E, L, SG, kSyncCta, 0, V, decltype(twp), NST - 2>(v, cur, twp, t, l);
+      release_half(0);
+      fft_stages<N, E, L, SG, kSyncCta, NST - 2, V, decltype(twp), NST - 1>(v, sm2, twp, t, l);
+      release_half(1);
+      fft_stages<N, E, L, SG, kSyncCta, NST - 1, V, decltype(twp), NST>(v, sm2, twp, t, l);
+    } else if constexpr (PASS == 0) {
       line_fft_head<N, E, L, -1>(v, cur, twp, t, l);
       release();
       line_fft_tail<N, E, L, -1>(v, cur, twp, t, l);
@@ -809,7 +928,15 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
       release();
       line_fft_tail<N, E, L, +1>(v, cur, twp, t, l);
     } else {
-      line_fft<N, E, L, -1>(v, cur, twp, t, l);
+      if constexpr (HX) {
+        line_fft_xs<N, E, L, -1>(v, scratch, twp, t, l);
+      } else if constexpr (E2S && NST == 2) {  // the forward exchange is the last use of the whole tile buffer
+        fft_stages<N, E, L, -1, kSyncCta, 0, V, decltype(twp), 1>(v, cur, twp, t, l);
+        release_half(0);
+        fft_stages<N, E, L, -1, kSyncCta, 1, V, decltype(twp), 2>(v, cur, twp, t, l);
+      } else {
+        line_fft<N, E, L, -1>(v, cur, twp, t, l);
+      }
       // full-grid frequencies: SPL > 0: (ki, kj) = (SPL i'' + ci, SPL j'' + cj), chunk SPL ci + cj;
       // kSplitI: ki = 2 i'' + chunk, kj = j (lines of N = n/2 points)
       constexpr int NG = SPL > 0 ? SPL * N : QUAD ? 2 * N : N;
@@ -838,10 +965,23 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
       if constexpr (LEAN) {
         if (c == T(0) && t == 0 && kiof(0) == T(0)) v[0] = V{T(0), T(0)};  // k = 0: the mean, dropped
       }
-      line_fft_head<N, E, L, +1>(v, cur, twp, t, l);
-      if constexpr (num_stages(N, E) == 1) __syncthreads();  // no exchange: make the buffer reads complete
-      release();
-      line_fft_tail<N, E, L, +1>(v, cur, twp, t, l);
+      if constexpr (HX) {
+        line_fft_xs<N, E, L, +1>(v, scratch, twp, t, l);
+      } else if constexpr (E2S) {
+        V* sm2 = cur + TILE / 2;  // last exchange: upper half of the tile buffer + the spare half tile
+        if constexpr (NST > 2) {
+          fft_stages<N, E, L, +1, kSyncCta, 0, V, decltype(twp), NST - 2>(v, cur, twp, t, l);
+          release_half(0);
+        }
+        fft_stages<N, E, L, +1, kSyncCta, NST - 2, V, decltype(twp), NST - 1>(v, sm2, twp, t, l);
+        release_half(1);
+        fft_stages<N, E, L, +1, kSyncCta, NST - 1, V, decltype(twp), NST>(v, sm2, twp, t, l);
+      } else {
+        line_fft_head<N, E, L, +1>(v, cur, twp, t, l);
+        if constexpr (num_stages(N, E) == 1) __syncthreads();  // no exchange: make the buffer reads complete
+        release();
+        line_fft_tail<N, E, L, +1>(v, cur, twp, t, l);
+      }
     }
     if (k < ks.kc) {
       auto dst = [&](V* base, size_t row) -> V* {

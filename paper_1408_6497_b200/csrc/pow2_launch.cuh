@@ -11,6 +11,7 @@
 #include "poisson_fused.cuh"
 #include "poisson_hq.cuh"
 #include "poisson_xtmem.cuh"
+#include "poisson_xpp.cuh"
 #include "poisson_quad.cuh"
 #include "poisson_qpencil.cuh"
 #include "poisson_split3.cuh"
@@ -79,8 +80,11 @@ cudaError_t encode_map(void* out, void* spec, const Layout& g, int nchunks, bool
   const cuuint64_t strides[4] = {row, row * JB, row * JB * g.ni, row * g.ni * g.nj};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   cuuint32_t box[5];
-  if (ybox) {
-    box[0] = 2 * LY; box[1] = JB; box[2] = 1; box[3] = g.nj / JB; box[4] = one_chunk ? 1 : nchunks;
+  if (ybox) {  // half a y tile (ytile_split; the kernels fetch a tile as two boxes)
+    const int nch = one_chunk ? 1 : nchunks;
+    const int sd = ytile_split(g, nch);
+    if (sd == 4 && (nch & 1)) return cudaErrorInvalidValue;
+    box[0] = 2 * LY; box[1] = JB; box[2] = 1; box[3] = (g.nj / JB) / (sd == 3 ? 2 : 1); box[4] = nch / (sd == 4 ? 2 : 1);
   } else {
     box[0] = 2 * LX; box[1] = 1; box[2] = tma_ib(g.ni); box[3] = 1; box[4] = 1;
   }
@@ -121,6 +125,19 @@ cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* 
   kern<<<grid, C::THREADS, SMEM, a.stream>>>(map, static_cast<V*>(spec), stw_ptr<T>(a, N == a.n ? 1 : 0, C::E), scale, four_pi2, g,
                                                a.nchunks, a.j0, ks, static_cast<V*>(out ? out : spec),
                                                gout ? *gout : g, pov);
+  return cudaGetLastError();
+}
+
+template <typename T, int N, int SPL>
+cudaError_t launch_xpp(const Pow2Args& a, const CUtensorMap& map, void* spec, T scale, T four_pi2) {
+  using C = XppCfg<T, N>;
+  using V = vec2_t<T>;
+  cudaError_t e = ensure_smem<k_xpass_pp<T, N, SPL>>(C::SMEM, C::THREADS);
+  if (e) return e;
+  constexpr KSpan ks = fixed_kspan<N, SPL, 2>();
+  const int tiles = N * ((ks.kc + C::L - 1) / C::L) * spl_chunks(SPL);
+  k_xpass_pp<T, N, SPL><<<imin(a.sm_count, tiles), C::THREADS, C::SMEM, a.stream>>>(
+      map, static_cast<V*>(spec), stw_ptr<T>(a, N == a.n ? 1 : 0, C::E), scale, four_pi2);
   return cudaGetLastError();
 }
 
@@ -209,7 +226,14 @@ cudaError_t launch_quad(const Pow2Args& a) {
     if (a.phases & kPhaseX) {
       mark(a, mk++);
       // compile-time quadrant geometry for the x pass, as the single-GPU x pass (FIXED)
-      if ((e = launch_strided_tma<T, H, 2, false, true, 2>(a, *mx, a.spec, gq, scale, four_pi2, ks))) return e;
+      bool done = false;
+      if constexpr (XppCfg<T, H>::OK && XppCfg<T, H>::L == TmaCfg<T, H, false, x_wide<T, true>()>::L) {
+        if (a.xpp) {
+          if ((e = launch_xpp<T, H, 2>(a, *mx, a.spec, scale, four_pi2))) return e;
+          done = true;
+        }
+      }
+      if (!done && (e = launch_strided_tma<T, H, 2, false, true, 2>(a, *mx, a.spec, gq, scale, four_pi2, ks))) return e;
     }
     if (a.phases & kPhaseYZ) {
       mark(a, mk++);
@@ -528,6 +552,12 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
           k_xpass_tmem<T, NR><<<imin(a.sm_count, tiles), XTmemCfg::THREADS, XTmemCfg::SMEM, a.stream>>>(
               *mx, static_cast<V*>(a.specC), stw_ptr<T>(a, 1, XTmemCfg::E), scale, four_pi2);
           if ((e = cudaGetLastError())) return e;
+          done = true;
+        }
+      }
+      if constexpr (XppCfg<T, NR>::OK && XppCfg<T, NR>::L == TmaCfg<T, NR, false, x_wide<T, false>()>::L) {
+        if (!done && single && a.xpp) {  // two out-of-phase groups per CTA (poisson_xpp.cuh)
+          if ((e = launch_xpp<T, NR, 0>(a, *mx, a.specC, scale, four_pi2))) return e;
           done = true;
         }
       }

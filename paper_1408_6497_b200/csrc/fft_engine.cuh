@@ -136,17 +136,20 @@ __device__ __forceinline__ V cmul_const(V a) {
 // in and out.  R = 1, 2, 4 directly; larger powers of two by one radix-4 (or
 // radix-2) decimation-in-time step over recursive sub-DFTs, all indices and
 // twiddles compile-time so everything stays in registers.
-template <int R, int S>
+// FMA: the twiddled radix-4 steps in FMA form (bfly4_tw below) — on for the 32-point
+// butterflies of the fp64 x pass and z passes; the 16- / 8-point stages of the y passes
+// (128-register kernels) measured 1.5% slower with it (a 32-byte spill).
+template <int R, int S, bool FMA = (R >= 32)>
 struct Dft;
 
-template <int S>
-struct Dft<1, S> {
+template <int S, bool FMA>
+struct Dft<1, S, FMA> {
   template <typename V>
   __device__ __forceinline__ static void run(V*) {}
 };
 
-template <int S>
-struct Dft<2, S> {
+template <int S, bool FMA>
+struct Dft<2, S, FMA> {
   template <typename V>
   __device__ __forceinline__ static void run(V* x) {
     const V t = x[1];
@@ -155,8 +158,8 @@ struct Dft<2, S> {
   }
 };
 
-template <int S>
-struct Dft<4, S> {
+template <int S, bool FMA>
+struct Dft<4, S, FMA> {
   template <typename V>
   __device__ __forceinline__ static void run(V* x) {
     const V s02 = cadd(x[0], x[2]), d02 = csub(x[0], x[2]);
@@ -168,7 +171,85 @@ struct Dft<4, S> {
   }
 };
 
-template <int R, int S>
+// FMA form of the twiddled radix-4 step (Linzer & Feig style): a constant twiddle is
+// written W = rho * C * (1 + i T) with rho in {1, S i}, |T| <= 1 (the angle reduced to
+// (-pi/4, pi/4] by quarter turns, a half turn folded into the sign of C), so W a = C a'
+// with a' = rho (a.x - T a.y, a.y + T a.x) — two FMAs instead of the four operations of a
+// complex product — and the scale C rides on the butterfly's additions, which become FMAs:
+//   s02 = a0 + C2 a2', d02 = a0 - C2 a2', u = a1' + (C3/C1) a3', v = a1' - (C3/C1) a3',
+//   x0 = s02 + C1 u, x2 = s02 - C1 u, x1 = d02 + C1 (S i) v, x3 = d02 - C1 (S i) v.
+// A 32-point DFT takes 376 fp64 instructions instead of 436 (FFTW's n1_32 codelet: 372).
+#ifndef ARENA_DFT_FMA
+#define ARENA_DFT_FMA 1  // 0: separate complex products (cmul_const) and additions
+#endif
+template <int R, int EX, int S>
+struct CTw {  // exp(S 2 pi i EX / R)
+  static constexpr int M = ((EX * (64 / R)) % 64 + 64) % 64;
+  static constexpr int QT = (M + 7) / 16;         // quarter turns taken out (0..4)
+  static constexpr int RM = M - 16 * QT;          // residual angle in 64ths of a turn, [-7, 8]
+  static constexpr bool ROT = (QT & 1) != 0;      // rho = S i (else 1)
+  static constexpr double C = ((QT & 2) ? -1.0 : 1.0) * cos64(RM);
+  static constexpr double T = S * sin64(RM) / cos64(RM);
+};
+// a' = rho (1 + i T) a
+template <typename W, int S, typename V>
+__device__ __forceinline__ V tw_rot(V a) {
+  using T = decltype(a.x);
+  V r;
+  if constexpr (W::RM == 0) {
+    r = a;
+  } else if constexpr (W::RM == 8) {  // T = S
+    r = S > 0 ? V{a.x - a.y, a.y + a.x} : V{a.x + a.y, a.y - a.x};
+  } else {
+    constexpr T tau = T(W::T);
+    r = V{fma(-tau, a.y, a.x), fma(tau, a.x, a.y)};
+  }
+  if constexpr (W::ROT) return cmul_si<S>(r);
+  else return r;
+}
+// y + c x, y - c x with a compile-time real c (plain sums when c = +-1)
+template <typename V>
+__device__ __forceinline__ void axpy_pm(double c, V x, V y, V& plus, V& minus) {
+  using T = decltype(x.x);
+  if (c == 1.0) {
+    plus = cadd(y, x);
+    minus = csub(y, x);
+  } else if (c == -1.0) {
+    plus = csub(y, x);
+    minus = cadd(y, x);
+  } else {
+    const T cc = T(c);
+    plus = V{fma(cc, x.x, y.x), fma(cc, x.y, y.y)};
+    minus = V{fma(-cc, x.x, y.x), fma(-cc, x.y, y.y)};
+  }
+}
+// Radix-4 butterfly over inputs a0, W^{K1} a1, W^{2 K1} a2, W^{3 K1} a3 (W = exp(S 2 pi i / R)).
+template <int R, int K1, int S, typename V>
+__device__ __forceinline__ void bfly4_tw(V a0, V a1, V a2, V a3, V& x0, V& x1, V& x2, V& x3) {
+  using W1 = CTw<R, K1, S>;
+  using W2 = CTw<R, 2 * K1, S>;
+  using W3 = CTw<R, 3 * K1, S>;
+  const V p1 = tw_rot<W1, S>(a1), p2 = tw_rot<W2, S>(a2), p3 = tw_rot<W3, S>(a3);
+  V s02, d02, u, v;
+  axpy_pm(W2::C, p2, a0, s02, d02);
+  axpy_pm(W3::C / W1::C, p3, p1, u, v);
+  axpy_pm(W1::C, u, s02, x0, x2);
+  axpy_pm(W1::C, cmul_si<S>(v), d02, x1, x3);
+}
+template <int R, int S, int K1, typename V, int Q>
+__device__ __forceinline__ void bfly4_all(V (&a)[4][Q], V* x) {
+  if constexpr (K1 < Q) {
+    V b0, b1, b2, b3;
+    bfly4_tw<R, K1, S>(a[0][K1], a[1][K1], a[2][K1], a[3][K1], b0, b1, b2, b3);
+    x[K1] = b0;
+    x[K1 + Q] = b1;
+    x[K1 + 2 * Q] = b2;
+    x[K1 + 3 * Q] = b3;
+    bfly4_all<R, S, K1 + 1>(a, x);
+  }
+}
+
+template <int R, int S, bool FMA>
 struct Dft {
   static_assert(R % 4 == 0 && R <= 64, "power-of-two radix <= 64");
   template <typename V>
@@ -180,14 +261,18 @@ struct Dft {
 #pragma unroll
       for (int n2 = 0; n2 < Q; ++n2) a[n1][n2] = x[4 * n2 + n1];
 #pragma unroll
-    for (int n1 = 0; n1 < 4; ++n1) Dft<Q, S>::run(a[n1]);
-    twiddle_all<1, 0>(a);
+    for (int n1 = 0; n1 < 4; ++n1) Dft<Q, S, FMA>::run(a[n1]);
+    if constexpr (ARENA_DFT_FMA && FMA && sizeof(x[0].x) == 8) {
+      bfly4_all<R, S, 0>(a, x);
+    } else {
+      twiddle_all<1, 0>(a);
 #pragma unroll
-    for (int k1 = 0; k1 < Q; ++k1) {
-      V b[4] = {a[0][k1], a[1][k1], a[2][k1], a[3][k1]};
-      Dft<4, S>::run(b);
+      for (int k1 = 0; k1 < Q; ++k1) {
+        V b[4] = {a[0][k1], a[1][k1], a[2][k1], a[3][k1]};
+        Dft<4, S, false>::run(b);
 #pragma unroll
-      for (int k2 = 0; k2 < 4; ++k2) x[k1 + Q * k2] = b[k2];
+        for (int k2 = 0; k2 < 4; ++k2) x[k1 + Q * k2] = b[k2];
+      }
     }
   }
   // compile-time loop applying W_R^{S n1 k1}
@@ -325,15 +410,11 @@ __device__ __forceinline__ void stage_compute(V (&v)[E], int t, TW stw) {
 
 // Barrier scope of the exchanges: the whole CTA, or one warp when a warp owns
 // its lines and their shared-memory region exclusively.
-// SYNC >= 32: a group of SYNC consecutive threads of the CTA on its own named barrier
-// (id 1 + group index), the groups running independently of each other.
 enum { kSyncCta = 0, kSyncWarp = 1 };
 template <int SYNC>
 __device__ __forceinline__ void xbarrier() {
   if constexpr (SYNC == kSyncWarp) {
     __syncwarp();
-  } else if constexpr (SYNC >= 32) {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + int(threadIdx.x) / SYNC), "r"(SYNC) : "memory");
   } else {
     __syncthreads();
   }
@@ -347,57 +428,28 @@ struct NoHook {
 
 // Write stage outputs to shared memory at their Stockham destinations and
 // read back the natural-order inputs of the next stage.
-// XS = 1 ("split exchange"): `sm` holds only N*L real scalars — half a tile — and
-// the real and the imaginary parts go through it one after the other.  The
-// strided passes then keep their full-size TMA tile buffer as a pure landing
-// zone, free for the next tile's load as soon as the tile is in registers.
-template <int N, int E, int L, int R, int NS, int SW, int SYNC, typename V, typename HK = NoHook, int XS = 0>
+template <int N, int E, int L, int R, int NS, int SW, int SYNC, typename V, typename HK = NoHook>
 __device__ __forceinline__ void stage_exchange(V (&v)[E], V* sm, int t, int l, const HK& hook = HK{}) {
   constexpr int P = N / E, NB = E / R;
-  if constexpr (XS) {
-    using T = decltype(v[0].x);
-    T* ss = reinterpret_cast<T*>(sm);
 #pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      const int b = t + P * q;
-      const int dst = (b & ~(NS - 1)) * R + (b & (NS - 1));
+  for (int q = 0; q < NB; ++q) {
+    const int b = t + P * q;
+    const int dst = (b & ~(NS - 1)) * R + (b & (NS - 1));
 #pragma unroll
-      for (int r = 0; r < R; ++r) ss[smem_idx<L, SW, T>(dst + r * NS, l)] = v[q + NB * r].x;
-    }
-    xbarrier<SYNC>();
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e].x = ss[smem_idx<L, SW, T>(t + P * e, l)];
-    xbarrier<SYNC>();
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      const int b = t + P * q;
-      const int dst = (b & ~(NS - 1)) * R + (b & (NS - 1));
-#pragma unroll
-      for (int r = 0; r < R; ++r) ss[smem_idx<L, SW, T>(dst + r * NS, l)] = v[q + NB * r].y;
-    }
-    xbarrier<SYNC>();
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e].y = ss[smem_idx<L, SW, T>(t + P * e, l)];
-    xbarrier<SYNC>();
-  } else {
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      const int b = t + P * q;
-      const int dst = (b & ~(NS - 1)) * R + (b & (NS - 1));
-#pragma unroll
-      for (int r = 0; r < R; ++r) sm[smem_idx<L, SW, V>(dst + r * NS, l)] = v[q + NB * r];
-    }
-    xbarrier<SYNC>();
-    hook();
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = sm[smem_idx<L, SW, V>(t + P * e, l)];
-    xbarrier<SYNC>();
-    hook();
+    for (int r = 0; r < R; ++r) sm[smem_idx<L, SW, V>(dst + r * NS, l)] = v[q + NB * r];
   }
+  xbarrier<SYNC>();
+  hook();
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = sm[smem_idx<L, SW, V>(t + P * e, l)];
+  xbarrier<SYNC>();
+  hook();
 }
 
+// Stages STAGE .. STOP-1 of the N-point transform, each followed by its exchange through
+// `sm` unless it is the transform's last stage.
 template <int N, int E, int L, int S, int SYNC, int STAGE, typename V, typename TW, int STOP = num_stages(N, E),
-          typename HK = NoHook, int XS = 0>
+          typename HK = NoHook>
 __device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, TW stw, int t, int l, const HK& hook = HK{}) {
   constexpr int NSTAGE = num_stages(N, E);
   if constexpr (STAGE < STOP) {
@@ -405,15 +457,9 @@ __device__ __forceinline__ void fft_stages(V (&v)[E], V* sm, TW stw, int t, int 
     constexpr int NS = stage_ns(N, E, STAGE);
     constexpr int SW = stage_log2(N, E, 0);
     stage_compute<N, E, R, NS, S>(v, t, stw + (STAGE >= 1 ? stage_tw_offset(N, E, STAGE) : 0));
-    if constexpr (STAGE + 1 < NSTAGE) stage_exchange<N, E, L, R, NS, SW, SYNC, V, HK, XS>(v, sm, t, l, hook);
-    fft_stages<N, E, L, S, SYNC, STAGE + 1, V, TW, STOP, HK, XS>(v, sm, stw, t, l, hook);
+    if constexpr (STAGE + 1 < NSTAGE) stage_exchange<N, E, L, R, NS, SW, SYNC>(v, sm, t, l, hook);
+    fft_stages<N, E, L, S, SYNC, STAGE + 1, V, TW, STOP>(v, sm, stw, t, l, hook);
   }
-}
-
-// Line FFT with the split exchange (XS above): `sm` is a scratch of N*L real scalars.
-template <int N, int E, int L, int S, int SYNC = kSyncCta, typename V, typename TW>
-__device__ __forceinline__ void line_fft_xs(V (&v)[E], V* sm, TW stw, int t, int l) {
-  fft_stages<N, E, L, S, SYNC, 0, V, TW, num_stages(N, E), NoHook, 1>(v, sm, stw, t, l);
 }
 
 // Full N-point line FFT of the tile.  On entry and exit thread (l, t) holds

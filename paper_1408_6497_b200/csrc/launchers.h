@@ -77,8 +77,6 @@ struct Pow2Args {
   int sub0 = 0, subn = 0;
   // Single GPU fp64 n = 1024: the x pass with the next tile staged in TMEM (poisson_xtmem.cuh).
   int xtmem = 0;
-  // Single GPU: the x pass as two out-of-phase half-CTA groups (poisson_xpp.cuh).
-  int xpp = 0;
   // Single GPU: 1 = quadrant formulation (poisson_quad.cuh, H = n/2-point y / x lines), 2 = i-split (poisson_hq.cuh).
   int quad = 0;
 };

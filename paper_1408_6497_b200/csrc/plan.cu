@@ -100,7 +100,6 @@ struct arena_fft_plan {
   int fuse = 0;             // kFuseFwd | kFuseInv
   int quad = 0;             // quadrant formulation (poisson_quad.cuh)
   int xtmem = 0;            // x pass with TMEM-staged tiles (poisson_xtmem.cuh)
-  int xpp = 0;              // x pass as two out-of-phase half-CTA groups (poisson_xpp.cuh)
   bool split3 = false;      // generic n = 3M: radix-3 split onto the power-of-two passes (poisson_split3.cuh)
   void* Q = nullptr;        // split3: nine-chunk workspace
   void* stwz = nullptr;     // split3: stage tables of the M/2-point z sub-FFTs (nullptr: generic z passes)
@@ -291,7 +290,6 @@ arena_status enqueue_kernels(arena_fft_plan* p, const void* d_f, void* d_u, cuda
                /*ni*/ p->n, /*nj*/ p->n, /*nchunks*/ 1, /*j0*/ 0, /*specC*/ p->spec, kPhaseAll, p->ctrs, p->lag, p->fuse};
     a.quad = p->quad;
     a.xtmem = p->xtmem;
-    a.xpp = p->xpp;
     e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
   } else if (p->split3) {
     const int R = split_radix(p->n);
@@ -454,12 +452,6 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
       const char* xt = std::getenv("ARENA_FFT_XTMEM");
       const bool want = xt ? std::string(xt) == "1" : false;
       p->xtmem = (want && p->tma && !p->quad && n == 1024 && precision_bits == 64) ? 1 : 0;
-    }
-    // x pass as two out-of-phase half-CTA groups (128 KB x tiles).  ARENA_FFT_XPP = 0 | 1.
-    {
-      const char* xp = std::getenv("ARENA_FFT_XPP");
-      const bool want = xp ? std::string(xp) == "1" : false;
-      p->xpp = (want && p->tma && !p->xtmem) ? 1 : 0;
     }
   } else {
     p->path = ARENA_PATH_GENERIC;

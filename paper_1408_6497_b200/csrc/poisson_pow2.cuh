@@ -517,14 +517,6 @@ namespace arena_fft {
 #ifndef ARENA_TMA_NBUF_Y
 #define ARENA_TMA_NBUF_Y ARENA_TMA_NBUF
 #endif
-#ifndef ARENA_TMA_HX_X
-#define ARENA_TMA_HX_X 0  // x pass: split exchange for tiles of at least this many bytes (0: never; B200 1024^3
-                          // fp64 at 131072: x 4.35 -> 4.50 ms, y at 131072: 3.23 -> 3.87 ms — the passes are not
-                          // waiting for their loads, and the exchange costs twice the LDS/STS and barriers)
-#endif
-#ifndef ARENA_TMA_HX_Y
-#define ARENA_TMA_HX_Y 0  // y passes: same
-#endif
 #ifndef ARENA_TMA_E2S_X
 #define ARENA_TMA_E2S_X 1  // x pass: last exchange shifted into spare shared memory, first half of the next
 #endif                     // tile requested before it
@@ -610,22 +602,15 @@ struct TmaCfg {
   static constexpr int NB0 = YP ? ARENA_TMA_NBUF_Y : ARENA_TMA_NBUF;
   static constexpr int NBUF = (NB0 * TILE * VB <= 200 * 1024) ? NB0 : imin(2, NB0);
   static constexpr int TW = stage_tw_total(N, E);  // staged twiddle entries (x pass)
-  // Split exchange (fft_engine.cuh, XS): a separate half-tile scratch takes the real and
-  // the imaginary parts in turn, so the tile buffer is only the TMA landing zone and the
-  // next tile is requested as soon as this one is in registers — its load overlaps the
-  // whole transform instead of the last stage only.
-  static constexpr int HXW = YP ? ARENA_TMA_HX_Y : ARENA_TMA_HX_X;
-  static constexpr bool HX = HXW != 0 && NBUF == 1 && num_stages(N, E) > 1 && TILE * VB >= HXW &&
-                             MINB * (TILE * VB * 3 / 2 + (!YP && ARENA_TMA_TWSMEM_X ? TW * VB : 0) + 1024 + 64) <= 228 * 1024;
   // Shifted last exchange (E2S): half a tile of spare shared memory behind the tile buffer.
   // The pass's last exchange runs in [TILE/2, 3 TILE/2) instead of [0, TILE), so the first
   // half of the next tile is requested before it (right after the previous exchange, or
   // after the tile read when there is none) and only the second half has to wait for it:
   // the strided passes spent 9% (x) / 13% (y) of their time waiting for the tile (ncu).
   static constexpr int E2SW = YP ? ARENA_TMA_E2S_Y : ARENA_TMA_E2S_X;
-  static constexpr bool E2S = E2SW != 0 && !HX && NBUF == 1 && num_stages(N, E) > 1 && N >= 4 &&
+  static constexpr bool E2S = E2SW != 0 && NBUF == 1 && num_stages(N, E) > 1 && N >= 4 &&
                               MINB * (TILE * VB * 3 / 2 + (!YP && ARENA_TMA_TWSMEM_X ? TW * VB : 0) + 1024 + 64) <= 228 * 1024;
-  static constexpr int SMEM = NBUF * TILE * VB + 16 * NBUF + ((HX || E2S) ? TILE * VB / 2 : 0);
+  static constexpr int SMEM = NBUF * TILE * VB + 16 * NBUF + (E2S ? TILE * VB / 2 : 0);
   static constexpr int SMEM_X = SMEM + (ARENA_TMA_TWSMEM_X ? TW * VB : 0);
   static constexpr int SMEM_Y = SMEM + (ARENA_TMA_TWSMEM_Y ? TW * VB : 0);
 };
@@ -750,12 +735,10 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
   const int NL = (ks.no ? ks.no : (PASS < 2 ? g.ni : g.nj)) * KT;  // tiles per chunk (QUAD) / in all
   const int NT = NL * NCH;
   constexpr bool TWS = PASS == 2 ? bool(ARENA_TMA_TWSMEM_X) : bool(ARENA_TMA_TWSMEM_Y);
-  constexpr bool HX = C::HX;
   constexpr bool E2S = C::E2S;
   constexpr int NST = num_stages(N, E);
   V* bufs = smem_base<V>();
-  V* scratch = bufs + NBUF * TILE;  // HX: TILE real scalars; E2S: half a tile behind the tile buffer
-  V* tws = scratch + ((HX || C::E2S) ? TILE / 2 : 0);
+  V* tws = bufs + NBUF * TILE + (E2S ? TILE / 2 : 0);  // E2S: half a tile of spare behind the tile buffer
   uint64_t* bar = reinterpret_cast<uint64_t*>(tws + (TWS ? C::TW : 0));
   const int tid = threadIdx.x;
   const int l = tid % L, t = tid / L;
@@ -843,7 +826,7 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
   // the load overlaps that iteration's last FFT stage and stores (B200: x 4.95
   // -> 4.32 ms).  The y passes measured 40% slower that way and request their
   // tile at the top of each iteration instead.
-  constexpr bool EARLY = NBUF == 1 && (PASS == 2 || ARENA_TMA_EARLY_Y || HX || E2S);
+  constexpr bool EARLY = NBUF == 1 && (PASS == 2 || ARENA_TMA_EARLY_Y || E2S);
   if constexpr (E2S) {
     if (tid == 0 && gt < NT) {
       issue_half(gt, 0);
@@ -877,14 +860,7 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
     V v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = cur[(t + P * e) * L + l];
-    __syncthreads();  // the tile buffer becomes exchange scratch (HX: is free for the next tile)
-    if constexpr (HX) {
-      const int gn = gt + gridDim.x;
-      if (tid == 0 && gn < NT) {
-        fence_proxy_async_smem();
-        issue(gn, bufs, &bar[0]);
-      }
-    }
+    __syncthreads();  // the tile buffer becomes exchange scratch
     const int qd = QUAD ? gt / NL : 0;
     const int gl = QUAD ? gt - qd * NL : gt;
     const int outer = gl / KT;
@@ -897,7 +873,7 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
       }
     };
     auto release = [&]() {  // buffer free (all exchange reads done): request the next tile
-      if constexpr (EARLY && !HX && !E2S) {
+      if constexpr (EARLY && !E2S) {
         const int gn = gt + gridDim.x;
         if (tid == 0 && gn < NT) {
           fence_proxy_async_smem();
@@ -905,11 +881,7 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
         }
       }
     };
-    if constexpr (PASS == 0 && HX) {
-      line_fft_xs<N, E, L, -1>(v, scratch, twp, t, l);
-    } else if constexpr (PASS == 1 && HX) {
-      line_fft_xs<N, E, L, +1>(v, scratch, twp, t, l);
-    } else if constexpr (PASS < 2 && E2S) {
+    if constexpr (PASS < 2 && E2S) {
       // every exchange but the last in the tile buffer, then the first half of the next tile is
       // requested; the last exchange in the upper half + the spare half tile, then the second half
       constexpr int SG = PASS == 0 ? -1 : +1;
@@ -928,9 +900,7 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
       release();
       line_fft_tail<N, E, L, +1>(v, cur, twp, t, l);
     } else {
-      if constexpr (HX) {
-        line_fft_xs<N, E, L, -1>(v, scratch, twp, t, l);
-      } else if constexpr (E2S && NST == 2) {  // the forward exchange is the last use of the whole tile buffer
+      if constexpr (E2S && NST == 2) {  // the forward exchange is the last use of the whole tile buffer
         fft_stages<N, E, L, -1, kSyncCta, 0, V, decltype(twp), 1>(v, cur, twp, t, l);
         release_half(0);
         fft_stages<N, E, L, -1, kSyncCta, 1, V, decltype(twp), 2>(v, cur, twp, t, l);
@@ -965,9 +935,7 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
       if constexpr (LEAN) {
         if (c == T(0) && t == 0 && kiof(0) == T(0)) v[0] = V{T(0), T(0)};  // k = 0: the mean, dropped
       }
-      if constexpr (HX) {
-        line_fft_xs<N, E, L, +1>(v, scratch, twp, t, l);
-      } else if constexpr (E2S) {
+      if constexpr (E2S) {
         V* sm2 = cur + TILE / 2;  // last exchange: upper half of the tile buffer + the spare half tile
         if constexpr (NST > 2) {
           fft_stages<N, E, L, +1, kSyncCta, 0, V, decltype(twp), NST - 2>(v, cur, twp, t, l);

@@ -11,7 +11,6 @@
 #include "poisson_fused.cuh"
 #include "poisson_hq.cuh"
 #include "poisson_xtmem.cuh"
-#include "poisson_xpp.cuh"
 #include "poisson_quad.cuh"
 #include "poisson_qpencil.cuh"
 #include "poisson_split3.cuh"
@@ -128,19 +127,6 @@ cudaError_t launch_strided_tma(const Pow2Args& a, const CUtensorMap& map, void* 
   return cudaGetLastError();
 }
 
-template <typename T, int N, int SPL>
-cudaError_t launch_xpp(const Pow2Args& a, const CUtensorMap& map, void* spec, T scale, T four_pi2) {
-  using C = XppCfg<T, N>;
-  using V = vec2_t<T>;
-  cudaError_t e = ensure_smem<k_xpass_pp<T, N, SPL>>(C::SMEM, C::THREADS);
-  if (e) return e;
-  constexpr KSpan ks = fixed_kspan<N, SPL, 2>();
-  const int tiles = N * ((ks.kc + C::L - 1) / C::L) * spl_chunks(SPL);
-  k_xpass_pp<T, N, SPL><<<imin(a.sm_count, tiles), C::THREADS, C::SMEM, a.stream>>>(
-      map, static_cast<V*>(spec), stw_ptr<T>(a, N == a.n ? 1 : 0, C::E), scale, four_pi2);
-  return cudaGetLastError();
-}
-
 // Peer destinations of a scattering pass: chunk c -> peers[c] (rank c's
 // workspace, already advanced to this rank's chunk); chunk_rows = ni * nj.
 constexpr int kPeerMinN = 16;
@@ -226,14 +212,7 @@ cudaError_t launch_quad(const Pow2Args& a) {
     if (a.phases & kPhaseX) {
       mark(a, mk++);
       // compile-time quadrant geometry for the x pass, as the single-GPU x pass (FIXED)
-      bool done = false;
-      if constexpr (XppCfg<T, H>::OK && XppCfg<T, H>::L == TmaCfg<T, H, false, x_wide<T, true>()>::L) {
-        if (a.xpp) {
-          if ((e = launch_xpp<T, H, 2>(a, *mx, a.spec, scale, four_pi2))) return e;
-          done = true;
-        }
-      }
-      if (!done && (e = launch_strided_tma<T, H, 2, false, true, 2>(a, *mx, a.spec, gq, scale, four_pi2, ks))) return e;
+      if ((e = launch_strided_tma<T, H, 2, false, true, 2>(a, *mx, a.spec, gq, scale, four_pi2, ks))) return e;
     }
     if (a.phases & kPhaseYZ) {
       mark(a, mk++);
@@ -552,12 +531,6 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
           k_xpass_tmem<T, NR><<<imin(a.sm_count, tiles), XTmemCfg::THREADS, XTmemCfg::SMEM, a.stream>>>(
               *mx, static_cast<V*>(a.specC), stw_ptr<T>(a, 1, XTmemCfg::E), scale, four_pi2);
           if ((e = cudaGetLastError())) return e;
-          done = true;
-        }
-      }
-      if constexpr (XppCfg<T, NR>::OK && XppCfg<T, NR>::L == TmaCfg<T, NR, false, x_wide<T, false>()>::L) {
-        if (!done && single && a.xpp) {  // two out-of-phase groups per CTA (poisson_xpp.cuh)
-          if ((e = launch_xpp<T, NR, 0>(a, *mx, a.specC, scale, four_pi2))) return e;
           done = true;
         }
       }

@@ -57,6 +57,9 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+#ifndef ARENA_Y_FIXED
+#define ARENA_Y_FIXED 0  // single GPU: compile-time geometry for the y passes too (as the x pass)
+#endif
 #ifndef ARENA_TMA_PROMO
 #define ARENA_TMA_PROMO 0  // L2 promotion of the TMA boxes: 0 none, 1 64B, 2 128B, 3 256B
 #endif
@@ -504,7 +507,8 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
       }
       if (e) return e;
     } else if (tma) {
-      e = launch_strided_tma<T, NR, 0>(a, *my, a.spec, gB, scale, four_pi2);
+      if (ARENA_Y_FIXED && single) e = launch_strided_tma<T, NR, 0, false, true>(a, *my, a.spec, gB, scale, four_pi2);
+      else e = launch_strided_tma<T, NR, 0>(a, *my, a.spec, gB, scale, four_pi2);
       if (e) return e;
     } else {
       if ((e = ensure_smem<k_ypass<T, NR, -1>>(SC::SMEM, SC::THREADS))) return e;
@@ -554,7 +558,8 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
   } else if (a.phases & kPhaseYZ) {
     mark(a, mk++);
     if (tma) {
-      e = launch_strided_tma<T, NR, 1>(a, *my, a.spec, gB, scale, four_pi2);
+      if (ARENA_Y_FIXED && single) e = launch_strided_tma<T, NR, 1, false, true>(a, *my, a.spec, gB, scale, four_pi2);
+      else e = launch_strided_tma<T, NR, 1>(a, *my, a.spec, gB, scale, four_pi2);
       if (e) return e;
     } else {
       if ((e = ensure_smem<k_ypass<T, NR, +1>>(SC::SMEM, SC::THREADS))) return e;

@@ -609,7 +609,7 @@ struct TmaCfg {
   // the strided passes spent 9% (x) / 13% (y) of their time waiting for the tile (ncu).
   static constexpr int E2SW = YP ? ARENA_TMA_E2S_Y : ARENA_TMA_E2S_X;
   static constexpr bool E2S = E2SW != 0 && NBUF == 1 && num_stages(N, E) > 1 && N >= 4 &&
-                              MINB * (TILE * VB * 3 / 2 + (!YP && ARENA_TMA_TWSMEM_X ? TW * VB : 0) + 1024 + 64) <= 228 * 1024;
+                              MINB * (TILE * VB * 3 / 2 + ((YP ? ARENA_TMA_TWSMEM_Y : ARENA_TMA_TWSMEM_X) ? TW * VB : 0) + 1024 + 64) <= 228 * 1024;
   static constexpr int SMEM = NBUF * TILE * VB + 16 * NBUF + (E2S ? TILE * VB / 2 : 0);
   static constexpr int SMEM_X = SMEM + (ARENA_TMA_TWSMEM_X ? TW * VB : 0);
   static constexpr int SMEM_Y = SMEM + (ARENA_TMA_TWSMEM_Y ? TW * VB : 0);

@@ -114,3 +114,69 @@ def test_fused_schedule_is_a_deadlock_free_permutation(planes, c1, c2, lag):
         else:
             assert last_first.get(p, -1) >= 0 and p in last_first
     assert len(seen) == total
+
+
+# ---- FMA form of the twiddled radix-4 step (fft_engine.cuh: CTw / tw_rot / bfly4_tw) -------------
+def _ctw(R, ex, S):
+    """Restates CTw<R, EX, S>: exp(S 2 pi i ex / R) = rho * C * (1 + i T), rho in {1, S i}, |T| <= 1."""
+    m = (ex * (64 // R)) % 64
+    qt = (m + 7) // 16
+    rm = m - 16 * qt
+    assert -7 <= rm <= 8
+    ang = 2 * np.pi * rm / 64
+    return bool(qt & 1), (-1.0 if qt & 2 else 1.0) * np.cos(ang), S * np.tan(ang)
+
+
+def _tw_rot(a, R, ex, S):
+    rot, _, T = _ctw(R, ex, S)
+    r = (a.real - T * a.imag) + 1j * (a.imag + T * a.real)
+    return r * (S * 1j) if rot else r
+
+
+def _dft_fma(x, S):
+    """Restates Dft<R, S, FMA = true>::run on the last axis (R = 2, 4 direct, else one radix-4 DIT step)."""
+    R = x.shape[-1]
+    if R == 1:
+        return x
+    if R == 2:
+        return np.stack([x[..., 0] + x[..., 1], x[..., 0] - x[..., 1]], -1)
+    if R == 4:
+        s02, d02 = x[..., 0] + x[..., 2], x[..., 0] - x[..., 2]
+        s13, d13 = x[..., 1] + x[..., 3], (S * 1j) * (x[..., 1] - x[..., 3])
+        return np.stack([s02 + s13, d02 + d13, s02 - s13, d02 - d13], -1)
+    Q = R // 4
+    a = [_dft_fma(x[..., n1::4], S) for n1 in range(4)]
+    out = np.empty_like(x)
+    for k1 in range(Q):
+        c = [_ctw(R, n * k1, S)[1] for n in range(4)]
+        p = [a[0][..., k1]] + [_tw_rot(a[n][..., k1], R, n * k1, S) for n in (1, 2, 3)]
+        s02, d02 = p[0] + c[2] * p[2], p[0] - c[2] * p[2]
+        r31 = c[3] / c[1]
+        u, v = p[1] + r31 * p[3], p[1] - r31 * p[3]
+        out[..., k1] = s02 + c[1] * u
+        out[..., k1 + 2 * Q] = s02 - c[1] * u
+        out[..., k1 + Q] = d02 + c[1] * (S * 1j) * v
+        out[..., k1 + 3 * Q] = d02 - c[1] * (S * 1j) * v
+    return out
+
+
+@pytest.mark.parametrize("S", [-1, +1])
+@pytest.mark.parametrize("R", [8, 16, 32, 64])
+def test_fma_twiddle_form_is_the_twiddle(R, S):
+    rng = np.random.default_rng(R + S)
+    a = rng.standard_normal(16) + 1j * rng.standard_normal(16)
+    for ex in range(0, 3 * (R // 4)):
+        rot, C, T = _ctw(R, ex, S)
+        assert abs(T) <= 1.0 + 1e-15 and abs(C) >= np.cos(np.pi / 4) - 1e-15
+        w = np.exp(S * 2j * np.pi * ex / R)
+        np.testing.assert_allclose(C * _tw_rot(a, R, ex, S), w * a, rtol=0, atol=2e-15 * np.abs(a).max())
+
+
+@pytest.mark.parametrize("S", [-1, +1])
+@pytest.mark.parametrize("R", [8, 16, 32, 64])
+def test_fma_form_dft_matches_numpy(R, S):
+    rng = np.random.default_rng(7 * R + S)
+    x = rng.standard_normal((5, R)) + 1j * rng.standard_normal((5, R))
+    ref = np.fft.fft(x, axis=-1) if S < 0 else np.fft.ifft(x, axis=-1) * R
+    got = _dft_fma(x, S)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 5e-16

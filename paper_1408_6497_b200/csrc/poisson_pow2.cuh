@@ -566,12 +566,15 @@ namespace arena_fft {
 #define ARENA_X_WIDE64 1  // fp64 x pass: 128-byte rows too (1024^3: one 8-warp CTA per SM, 4.35 -> 4.30 ms;
                           // fp32 measured slower that way, 2.31 -> 2.50 ms)
 #endif
+#ifndef ARENA_X_WIDE32
+#define ARENA_X_WIDE32 0  // fp32 x pass: 16-line tiles (128-byte rows), one 512-thread CTA per SM
+#endif
 template <typename T, int N, bool YP = false, bool XW = false>
 struct TmaCfg;
 // XW of the x pass (TmaCfg<T, N, false, x_wide<T, QUAD>()>)
 template <typename T, bool QUAD>
 constexpr bool x_wide() {
-  return QUAD ? bool(ARENA_QUAD_XW) : (sizeof(T) == 8 && bool(ARENA_X_WIDE64));
+  return QUAD ? bool(ARENA_QUAD_XW) : (sizeof(T) == 8 ? bool(ARENA_X_WIDE64) : bool(ARENA_X_WIDE32));
 }
 template <typename T, int N, bool YP, bool XW>
 struct TmaCfg {

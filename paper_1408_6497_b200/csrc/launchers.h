@@ -75,9 +75,7 @@ struct Pow2Args {
   // Slab chunked exchange: with subn > 0 and phases == kPhaseZY (kPhaseX) only local i
   // planes (local j lines, whole JB blocks) [sub0, sub0 + subn) are transformed.
   int sub0 = 0, subn = 0;
-  // Single GPU fp64 n = 1024: the x pass with the next tile staged in TMEM (poisson_xtmem.cuh).
-  int xtmem = 0;
-  // Single GPU: 1 = quadrant formulation (poisson_quad.cuh, H = n/2-point y / x lines), 2 = i-split (poisson_hq.cuh).
+  // Single GPU: 1 = quadrant formulation (poisson_quad.cuh, H = n/2-point y / x lines).
   int quad = 0;
 };
 enum : int { kFuseFwd = 1, kFuseInv = 2 };

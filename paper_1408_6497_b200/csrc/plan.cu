@@ -99,7 +99,6 @@ struct arena_fft_plan {
   int lag = 2;
   int fuse = 0;             // kFuseFwd | kFuseInv
   int quad = 0;             // quadrant formulation (poisson_quad.cuh)
-  int xtmem = 0;            // x pass with TMEM-staged tiles (poisson_xtmem.cuh)
   bool split3 = false;      // generic n = 3M: radix-3 split onto the power-of-two passes (poisson_split3.cuh)
   void* Q = nullptr;        // split3: nine-chunk workspace
   void* stwz = nullptr;     // split3: stage tables of the M/2-point z sub-FFTs (nullptr: generic z passes)
@@ -289,7 +288,6 @@ arena_status enqueue_kernels(arena_fft_plan* p, const void* d_f, void* d_u, cuda
     Pow2Args a{d_f, d_u, p->spec, p->tw, p->stw, p->n, p->nc, p->ncp, s, ev, p->tma, p->sm_count,
                /*ni*/ p->n, /*nj*/ p->n, /*nchunks*/ 1, /*j0*/ 0, /*specC*/ p->spec, kPhaseAll, p->ctrs, p->lag, p->fuse};
     a.quad = p->quad;
-    a.xtmem = p->xtmem;
     e = p->prec == 64 ? launch_pow2_f64(a) : launch_pow2_f32(a);
   } else if (p->split3) {
     const int R = split_radix(p->n);
@@ -433,25 +431,16 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
     // B200 A/B (ms per solve, plain / quadrant): 2048^3 fp64 178 / 148, fp32 95 / 84;
     // 1024^3 17.5 / 18.2; 512^3 fp64 2.10 / 2.01, fp32 1.10 / 1.10; 256^3 0.295 / 0.307.
     // ARENA_FFT_QUAD = 0 | 1 overrides (any n >= 32 with the TMA kernels).
-    // i-split formulation (poisson_hq.cuh): only the i transform's first radix-2 step
-    // moves into the z passes, so the x pass runs n/2-point lines at twice the
-    // occupancy while the y lines keep all n points.  ARENA_FFT_QUAD = hq selects it.
     {
       const char* qz = std::getenv("ARENA_FFT_QUAD");
       int want = 0;
       if (qz) {
         const std::string v(qz);
-        want = v == "1" ? 1 : (v == "hq" || v == "2") ? 2 : 0;
+        want = v == "1" ? 1 : 0;
       } else {
         want = (n >= 2048 || (n == 512 && precision_bits == 64)) ? 1 : 0;
       }
       p->quad = (want && p->tma && n >= 32 && !p->fuse) ? want : 0;
-    }
-    // x pass with the next tile staged in tensor memory (fp64 n = 1024).  ARENA_FFT_XTMEM = 0 | 1.
-    {
-      const char* xt = std::getenv("ARENA_FFT_XTMEM");
-      const bool want = xt ? std::string(xt) == "1" : false;
-      p->xtmem = (want && p->tma && !p->quad && n == 1024 && precision_bits == 64) ? 1 : 0;
     }
   } else {
     p->path = ARENA_PATH_GENERIC;

@@ -667,25 +667,17 @@ struct KSpan {
 // Chunked ("split") layouts of the single-GPU path, selected by the SPL template
 // argument of the strided kernels: SPL = R > 0 splits both i and j by R (R*R
 // chunks of (n/R)^2 rows: the quadrant formulation R = 2, poisson_quad.cuh; the
-// radix-3/5 splits, poisson_split3.cuh); SPL = kSplitI splits only i by 2 (two
-// chunks of (n/2) x n rows: poisson_hq.cuh), so the y lines keep all n points
-// and only the x lines are halved.
-constexpr int kSplitI = -2;
-__host__ __device__ constexpr int spl_chunks(int spl) { return spl > 0 ? spl * spl : spl == kSplitI ? 2 : 1; }
+// radix-3/5 splits, poisson_split3.cuh).
+__host__ __device__ constexpr int spl_chunks(int spl) { return spl > 0 ? spl * spl : 1; }
 // Compile-time geometry of a FIXED (single-GPU) strided pass on N-point lines.
 template <int N, int SPL, int PASS>
 __host__ __device__ constexpr Layout fixed_geom() {
-  if constexpr (SPL == kSplitI) {
-    return PASS == 2 ? Layout{N, 2 * N, ilog2_c(N), ilog2_c(2 * N), ilog2_c(2 * N < ARENA_JBLOCK ? 2 * N : ARENA_JBLOCK)}
-                     : Layout{N / 2, N, ilog2_c(N / 2), ilog2_c(N), ilog2_c(N < ARENA_JBLOCK ? N : ARENA_JBLOCK)};
-  } else {
-    return fixed_layout<N>();
-  }
+  return fixed_layout<N>();
 }
 template <int N, int SPL, int PASS>
 __host__ __device__ constexpr KSpan fixed_kspan() {
   // the n of the grid the N-point lines belong to
-  constexpr int NG = SPL > 0 ? SPL * N : (SPL == kSplitI && PASS == 2) ? 2 * N : N;
+  constexpr int NG = SPL > 0 ? SPL * N : N;
   return KSpan{NG / 2 + 1, spec_pitch(NG), 0};
 }
 
@@ -718,7 +710,7 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
                   const vec2_t<T>* __restrict__ stw, T scale, T four_pi2, Layout g_, int nchunks_, int j0_, KSpan ks_,
                   vec2_t<T>* __restrict__ out_, Layout gout_, const __grid_constant__ PeerOut<vec2_t<T>> po) {
   static_assert(!(FIXED && PEER), "the fixed geometry is the single-GPU one");
-  constexpr bool QUAD = SPL != 0;  // chunked split layout (SPL > 0: i and j split by SPL; kSplitI: i by 2)
+  constexpr bool QUAD = SPL != 0;  // chunked split layout (i and j split by SPL)
   constexpr int NCH = spl_chunks(SPL);
   static_assert(!(QUAD && PEER), "the quadrant layout is single-GPU");
   const Layout g = FIXED ? fixed_geom<N, SPL, PASS>() : g_;
@@ -910,9 +902,8 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
       } else {
         line_fft<N, E, L, -1>(v, cur, twp, t, l);
       }
-      // full-grid frequencies: SPL > 0: (ki, kj) = (SPL i'' + ci, SPL j'' + cj), chunk SPL ci + cj;
-      // kSplitI: ki = 2 i'' + chunk, kj = j (lines of N = n/2 points)
-      constexpr int NG = SPL > 0 ? SPL * N : QUAD ? 2 * N : N;
+      // full-grid frequencies: SPL > 0: (ki, kj) = (SPL i'' + ci, SPL j'' + cj), chunk SPL ci + cj
+      constexpr int NG = SPL > 0 ? SPL * N : N;
       const T kj = SPL > 0 ? T(signed_freq(SPL * outer + qd % imax(SPL, 1), NG))
                    : ks.fm ? T(signed_freq(2 * (j0 + outer) + ks.fcj, 2 * N))
                            : T(signed_freq(j0 + outer, NG));
@@ -920,7 +911,6 @@ __global__ void __launch_bounds__(TmaCfg<T, N, (PASS < 2), PASS == 2 && x_wide<T
       const T c = kj * kj + kk * kk;
       auto kiof = [&](int e) {
         return SPL > 0 ? T(signed_freq(SPL * (t + P * e) + qd / imax(SPL, 1), NG))
-               : QUAD  ? T(signed_freq(2 * (t + P * e) + qd, NG))
                : ks.fm ? T(signed_freq(2 * (t + P * e) + ks.fci, 2 * N))
                        : T(signed_freq(t + P * e, NG));
       };

@@ -9,8 +9,6 @@
 
 #include "launchers.h"
 #include "poisson_fused.cuh"
-#include "poisson_hq.cuh"
-#include "poisson_xtmem.cuh"
 #include "poisson_quad.cuh"
 #include "poisson_qpencil.cuh"
 #include "poisson_split3.cuh"
@@ -229,68 +227,6 @@ cudaError_t launch_quad(const Pow2Args& a) {
   }
 }
 
-// Single-GPU i-split path (poisson_hq.cuh): K1h, the n-point y passes and the
-// H-point x pass on the two i-parity chunks, K5h.
-constexpr int kTmaTagHq = 102;  // TmaCache::quad tag of the i-split maps
-template <typename T, int NR>
-cudaError_t launch_hq(const Pow2Args& a) {
-  if constexpr (!(HqZCfg<T, NR>::OK && NR >= 16)) {
-    return cudaErrorNotSupported;
-  } else {
-    constexpr int H = NR / 2;
-    using V = vec2_t<T>;
-    using ZC = HqZCfg<T, NR>;
-    cudaError_t e;
-    if (!a.tma || a.nchunks != 1 || a.specC != a.spec || a.ni != NR || a.nj != NR) return cudaErrorNotSupported;
-    if (a.ncp != spec_pitch(NR) || a.nc != NR / 2 + 1) return cudaErrorInvalidValue;
-    if ((e = ensure_smem<k_zfwd_hq<T, NR>>(ZC::SMEM, ZC::THREADS))) return e;
-    if ((e = ensure_smem<k_zinv_hq<T, NR>>(ZC::SMEM, ZC::THREADS))) return e;
-    const Layout gh = make_layout(H, NR);
-    const KSpan ks{NR / 2 + 1, spec_pitch(NR), 0};
-    TmaCache* c = a.tma;
-    if (c->specB != a.spec || c->specC != a.spec || c->n != NR || c->nchunks != 2 || c->quad != kTmaTagHq) {
-      if ((e = encode_map<T, NR>(c->maps[0], a.spec, gh, 2, true, ks.kc, ks.kq, TmaCfg<T, NR, true>::L, true))) return e;
-      if ((e = encode_map<T, H>(c->maps[1], a.spec, gh, 2, false, ks.kc, ks.kq, TmaCfg<T, H, true>::L, false,
-                                TmaCfg<T, H, false, x_wide<T, true>()>::L)))
-        return e;
-      c->specB = c->specC = a.spec;
-      c->n = NR;
-      c->ni = H;
-      c->nj = NR;
-      c->nchunks = 2;
-      c->quad = kTmaTagHq;
-    }
-    const CUtensorMap* my = reinterpret_cast<const CUtensorMap*>(c->maps[0]);
-    const CUtensorMap* mx = reinterpret_cast<const CUtensorMap*>(c->maps[1]);
-    const T scale = T(1.0 / (double(NR) * NR * NR));  // fft_solver.cpp:67
-    const T four_pi2 = T(4.0 * M_PI * M_PI);           // fft_solver.cpp:66
-    const V* tw = static_cast<const V*>(a.tw);
-    V* S = static_cast<V*>(a.spec);
-    const unsigned zgrid = unsigned(H) * (NR / ZC::JR);
-    int mk = 0;
-    if (a.phases & kPhaseZY) {
-      mark(a, mk++);
-      k_zfwd_hq<T, NR><<<zgrid, ZC::THREADS, ZC::SMEM, a.stream>>>(static_cast<const T*>(a.f), S, tw,
-                                                                   stw_ptr<T>(a, 0, ZC::E));
-      mark(a, mk++);
-      if ((e = launch_strided_tma<T, NR, 0, false, false, kSplitI>(a, *my, a.spec, gh, scale, four_pi2, ks))) return e;
-    }
-    if (a.phases & kPhaseX) {
-      mark(a, mk++);
-      if ((e = launch_strided_tma<T, H, 2, false, true, kSplitI>(a, *mx, a.spec, gh, scale, four_pi2, ks))) return e;
-    }
-    if (a.phases & kPhaseYZ) {
-      mark(a, mk++);
-      if ((e = launch_strided_tma<T, NR, 1, false, false, kSplitI>(a, *my, a.spec, gh, scale, four_pi2, ks))) return e;
-      mark(a, mk++);
-      k_zinv_hq<T, NR><<<zgrid, ZC::THREADS, ZC::SMEM, a.stream>>>(S, static_cast<T*>(a.u), tw,
-                                                                   stw_ptr<T>(a, 0, ZC::E));
-      mark(a, mk++);
-    }
-    return cudaGetLastError();
-  }
-}
-
 // Radix-3 split path (poisson_split3.cuh): generic z r2c, split, M-point y / x / y
 // TMA passes on the nine chunks, merge, generic z c2r.
 template <typename T, int R, int M>
@@ -396,7 +332,6 @@ cudaError_t launch_split3(const Split3Args& s) {
 template <typename T, int NR>
 cudaError_t launch_pow2_n(const Pow2Args& a) {
   if (a.quad == 1) return launch_quad<T, NR>(a);
-  if (a.quad == 2) return launch_hq<T, NR>(a);
   using V = vec2_t<T>;
   using CC = ContigCfg<T, NR>;
   using SC = StridedCfg<T, NR, 0>;
@@ -527,22 +462,9 @@ cudaError_t launch_pow2_n(const Pow2Args& a) {
       }
       if (e) return e;
     } else if (tma) {
-      bool done = false;
-      if constexpr (sizeof(T) == 8 && NR == XTmemCfg::N) {
-        if (single && a.xtmem) {  // next tile staged in TMEM (poisson_xtmem.cuh)
-          if ((e = ensure_smem<k_xpass_tmem<T, NR>>(XTmemCfg::SMEM, XTmemCfg::THREADS))) return e;
-          const int tiles = NR * ((NR / 2 + 1 + XTmemCfg::L - 1) / XTmemCfg::L);
-          k_xpass_tmem<T, NR><<<imin(a.sm_count, tiles), XTmemCfg::THREADS, XTmemCfg::SMEM, a.stream>>>(
-              *mx, static_cast<V*>(a.specC), stw_ptr<T>(a, 1, XTmemCfg::E), scale, four_pi2);
-          if ((e = cudaGetLastError())) return e;
-          done = true;
-        }
-      }
-      if (!done) {
-        if (single) e = launch_strided_tma<T, NR, 2, false, true>(a, *mx, a.specC, gC, scale, four_pi2);
-        else e = launch_strided_tma<T, NR, 2>(a, *mx, a.specC, gC, scale, four_pi2);
-        if (e) return e;
-      }
+      if (single) e = launch_strided_tma<T, NR, 2, false, true>(a, *mx, a.specC, gC, scale, four_pi2);
+      else e = launch_strided_tma<T, NR, 2>(a, *mx, a.specC, gC, scale, four_pi2);
+      if (e) return e;
     } else {
       if ((e = ensure_smem<k_xmid<T, NR>>(XC::SMEM, XC::THREADS))) return e;
       k_xmid<T, NR><<<dim3((a.nc + XC::L - 1) / XC::L, NR), XC::THREADS, XC::SMEM, a.stream>>>(

@@ -207,6 +207,37 @@ __device__ __forceinline__ V tw_rot(V a) {
   if constexpr (W::ROT) return cmul_si<S>(r);
   else return r;
 }
+#ifndef ARENA_DFT_FMA32
+#define ARENA_DFT_FMA32 1  // the FMA form for fp32 too, on packed pairs (FFMA2)
+#endif
+#if ARENA_F32X2 >= 2
+// fp32: a' = a + (-T, T) (a.y, a.x), one packed FFMA2 on the swapped pair
+template <typename W, int S>
+__device__ __forceinline__ float2 tw_rot(float2 a) {
+  float2 r;
+  if constexpr (W::RM == 0) {
+    r = a;
+  } else {
+    constexpr float tau = W::RM == 8 ? float(S) : float(W::T);
+    r = __ffma2_rn(make_float2(-tau, tau), make_float2(a.y, a.x), a);
+  }
+  if constexpr (W::ROT) return cmul_si<S>(r);
+  else return r;
+}
+__device__ __forceinline__ void axpy_pm(double c, float2 x, float2 y, float2& plus, float2& minus) {
+  if (c == 1.0) {
+    plus = cadd(y, x);
+    minus = csub(y, x);
+  } else if (c == -1.0) {
+    plus = csub(y, x);
+    minus = cadd(y, x);
+  } else {
+    const float cc = float(c);
+    plus = __ffma2_rn(make_float2(cc, cc), x, y);
+    minus = __ffma2_rn(make_float2(-cc, -cc), x, y);
+  }
+}
+#endif
 // y + c x, y - c x with a compile-time real c (plain sums when c = +-1)
 template <typename V>
 __device__ __forceinline__ void axpy_pm(double c, V x, V y, V& plus, V& minus) {
@@ -262,7 +293,7 @@ struct Dft {
       for (int n2 = 0; n2 < Q; ++n2) a[n1][n2] = x[4 * n2 + n1];
 #pragma unroll
     for (int n1 = 0; n1 < 4; ++n1) Dft<Q, S, FMA>::run(a[n1]);
-    if constexpr (ARENA_DFT_FMA && FMA && sizeof(x[0].x) == 8) {
+    if constexpr (ARENA_DFT_FMA && FMA && (sizeof(x[0].x) == 8 || (ARENA_DFT_FMA32 && ARENA_F32X2 >= 2))) {
       bfly4_all<R, S, 0>(a, x);
     } else {
       twiddle_all<1, 0>(a);

@@ -210,6 +210,9 @@ __device__ __forceinline__ V tw_rot(V a) {
 #ifndef ARENA_DFT_FMA32
 #define ARENA_DFT_FMA32 1  // the FMA form for fp32 too, on packed pairs (FFMA2)
 #endif
+#ifndef ARENA_DFT_FMA32_ALL
+#define ARENA_DFT_FMA32_ALL 0  // fp32: also the 16- / 8-point stages (y passes)
+#endif
 #if ARENA_F32X2 >= 2
 // fp32: a' = a + (-T, T) (a.y, a.x), one packed FFMA2 on the swapped pair
 template <typename W, int S>
@@ -293,7 +296,9 @@ struct Dft {
       for (int n2 = 0; n2 < Q; ++n2) a[n1][n2] = x[4 * n2 + n1];
 #pragma unroll
     for (int n1 = 0; n1 < 4; ++n1) Dft<Q, S, FMA>::run(a[n1]);
-    if constexpr (ARENA_DFT_FMA && FMA && (sizeof(x[0].x) == 8 || (ARENA_DFT_FMA32 && ARENA_F32X2 >= 2))) {
+    constexpr bool F32 = sizeof(x[0].x) == 4;
+    constexpr bool kFmaForm = ARENA_DFT_FMA && (F32 ? (ARENA_DFT_FMA32 && ARENA_F32X2 >= 2 && (FMA || ARENA_DFT_FMA32_ALL)) : FMA);
+    if constexpr (kFmaForm) {
       bfly4_all<R, S, 0>(a, x);
     } else {
       twiddle_all<1, 0>(a);

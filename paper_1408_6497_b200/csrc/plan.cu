@@ -399,6 +399,10 @@ static arena_status create_plan(arena_fft_plan** out, int n, int precision_bits,
   p->nc = n / 2 + 1;
   p->ncp = spec_pitch(n);  // poisson_pow2.cuh (the kernels check it)
   p->sm_count = prop.multiProcessorCount;
+  if (const char* sms = std::getenv("ARENA_FFT_SMS")) {  // experiments: persistent kernels on fewer SMs
+    const int v = std::atoi(sms);
+    if (v >= 1 && v < p->sm_count) p->sm_count = v;
+  }
   {
     const char* gr = std::getenv("ARENA_FFT_GRAPHS");  // "0" disables graph replay
     p->use_graphs = n <= 256 && !(gr && std::string(gr) == "0");

@@ -225,6 +225,9 @@ __device__ __forceinline__ V* smem_base() {
 // W_n^t times the compile-time root W_{2E}^e (e is constant once the caller's loop is
 // unrolled) — one complex product instead of a table load per element, off the
 // L1TEX pipe the z kernels are bound by (ncu: l1tex 88%).  ARENA_Z_TWREC = 0: loads.
+#ifndef ARENA_Z_PAIRS
+#define ARENA_Z_PAIRS 1  // r2c split: both outputs of a pair (k, M - k) from one thread
+#endif
 #ifndef ARENA_Z_TWREC
 #define ARENA_Z_TWREC 1
 #endif
@@ -290,16 +293,40 @@ __device__ __forceinline__ void zfwd_rows(const T* __restrict__ f, vec2_t<T>* __
   xbarrier<SYNC>();
   V* dst = S + rowB(g, int(row / NR), int(row % NR)) * ncp;
   const V wt = tw_load(tw, t);  // W_n^t (split_twiddle)
+  if constexpr (ARENA_Z_PAIRS && E >= 2 && (E % 2) == 0 && ARENA_Z_TWREC && E <= 32) {
+    // Both members of a pair from one thread: with A = Z[k], B = conj(Z[M-k]), S = (A + B)/2 and
+    // U = (i/2) W_n^k (A - B),  X[k] = S - U  and  X[M-k] = conj(S + U)  (W_n^{M-k} = -conj W_n^k),
+    // so the difference and its product with the twiddle are formed once per pair: 8 fp64
+    // operations per output instead of 16, and half the mirror reads.  k = t + P e, e < E/2,
+    // covers [0, M/2); k = 0 pairs with the Nyquist output X[M]; X[M/2] = conj(Z[M/2]).
+    const V wh{T(-0.5) * wt.y, T(0.5) * wt.x};  // (i/2) W_n^t
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int k = t + P * e;
-    const V A = v[e];
-    const V Bc = sm[smem_idx<L, SW, V>((M - k) & (M - 1), l)];
-    const V B{Bc.x, -Bc.y};
-    const V W = split_twiddle<E>(tw, wt, k, e);  // W_n^k
-    const V WD = cmul(W, csub(A, B));
-    dst[k] = V{T(0.5) * (A.x + B.x + WD.y), T(0.5) * (A.y + B.y - WD.x)};
-    if (k == 0) dst[M] = V{A.x - A.y, T(0)};
+    for (int e = 0; e < E / 2; ++e) {
+      const int k = t + P * e;
+      const V A = v[e];
+      const V Bc = sm[smem_idx<L, SW, V>((M - k) & (M - 1), l)];
+      const V B{Bc.x, -Bc.y};
+      const V Wh = split_twiddle<E>(tw, wh, k, e);  // (i/2) W_n^k
+      const V U = cmul(Wh, csub(A, B));
+      const V Sm = cadd(A, B);
+      dst[k] = V{fma(T(0.5), Sm.x, -U.x), fma(T(0.5), Sm.y, -U.y)};
+      V Xm{fma(T(0.5), Sm.x, U.x), -fma(T(0.5), Sm.y, U.y)};
+      if (k == 0) Xm.y = T(0);  // X[M] = Re Z0 - Im Z0, real
+      dst[M - k] = Xm;
+    }
+    if (t == 0) dst[M / 2] = V{v[E / 2].x, -v[E / 2].y};
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int k = t + P * e;
+      const V A = v[e];
+      const V Bc = sm[smem_idx<L, SW, V>((M - k) & (M - 1), l)];
+      const V B{Bc.x, -Bc.y};
+      const V W = split_twiddle<E>(tw, wt, k, e);  // W_n^k
+      const V WD = cmul(W, csub(A, B));
+      dst[k] = V{T(0.5) * (A.x + B.x + WD.y), T(0.5) * (A.y + B.y - WD.x)};
+      if (k == 0) dst[M] = V{A.x - A.y, T(0)};
+    }
   }
 }
 
@@ -341,12 +368,55 @@ __device__ __forceinline__ void zinv_rows(const vec2_t<T>* __restrict__ S, T* __
   const size_t row = row0 + l;
   const V* src = S + rowB(g, int(row / NR), int(row % NR)) * ncp;
   V v[E];
+  auto ld = [&](int k) { return DISCARD ? __ldcg(src + k) : __ldcs(src + k); };
+  if constexpr (ARENA_Z_PAIRS && E >= 2 && (E % 2) == 0 && ARENA_Z_TWREC && E <= 32) {
+    // Both members of a pair from one thread (the mirror of zfwd_rows' split): with A = X[k],
+    // B = conj(X[M-k]), Ep = A + B and Op = i conj(W_n^k) (A - B),  Z[k] = Ep + Op  and
+    // Z[M-k] = conj(Ep - Op).  The thread loads X[k] and X[M-k] itself (k = t + P e, e < E/2;
+    // k = 0 pairs X[0] with X[M], imaginary parts ignored as FFTW's c2r does), keeps Z[k]
+    // and hands Z[M-k] to its owner through shared memory: half the staging traffic and
+    // 8 instead of 14 fp64 operations per element.  Z[M/2] = 2 conj(X[M/2]).
+    const V wt = tw_load(tw, t);
+    const V wi{wt.y, wt.x};  // i conj(W_n^t)
+#pragma unroll
+    for (int e = 0; e < E / 2; ++e) {
+      const int k = t + P * e;
+      V A = ld(k);
+      V C = ld(M - k);
+      if (k == 0) {
+        A.y = T(0);
+        C.y = T(0);
+      }
+      const V B{C.x, -C.y};
+      const V Wi = cmulc(wi, w64((e * (32 / E)) & 63, T(0)));  // i conj(W_n^k), W_n^{P e} = W_64^{e 32 / E}
+      const V Ep = cadd(A, B);
+      const V Op = cmul(csub(A, B), Wi);
+      v[e] = cadd(Ep, Op);
+      if (k != 0) sm[smem_idx<L, SW, V>(M - k, l)] = V{Ep.x - Op.x, Op.y - Ep.y};
+    }
+    if (t == 0) {
+      const V h = ld(M / 2);
+      sm[smem_idx<L, SW, V>(M / 2, l)] = V{T(2) * h.x, T(-2) * h.y};
+    }
+    xbarrier<SYNC>();
+    if constexpr (DISCARD) {
+      constexpr int LINES = ncp * int(sizeof(V)) / 128;
+      for (int q = t; q < LINES; q += P) l2_discard(reinterpret_cast<const char*>(src) + size_t(q) * 128);
+    }
+#pragma unroll
+    for (int e = E / 2; e < E; ++e) v[e] = sm[smem_idx<L, SW, V>(t + P * e, l)];
+    xbarrier<SYNC>();
+    line_fft<M, E, L, +1, SYNC>(v, sm, stw, t, l);
+    V* dstp = reinterpret_cast<V*>(u + row * NR);
+#pragma unroll
+    for (int e = 0; e < E; ++e) st_out(dstp + t + P * e, v[e]);
+  } else {
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    v[e] = DISCARD ? __ldcg(src + t + P * e) : __ldcs(src + t + P * e);
+    v[e] = ld(t + P * e);
     sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
   }
-  if (t == 0) xm[l] = DISCARD ? __ldcg(src + M) : __ldcs(src + M);
+  if (t == 0) xm[l] = ld(M);
   xbarrier<SYNC>();
   if constexpr (DISCARD) {
     constexpr int LINES = ncp * int(sizeof(V)) / 128;
@@ -373,6 +443,7 @@ __device__ __forceinline__ void zinv_rows(const vec2_t<T>* __restrict__ S, T* __
   V* dst = reinterpret_cast<V*>(u + row * NR);
 #pragma unroll
   for (int e = 0; e < E; ++e) st_out(dst + t + P * e, v[e]);
+  }
 }
 
 template <typename T, int NR, bool FIXED = false>

@@ -288,12 +288,14 @@ __device__ __forceinline__ void zfwd_rows(const T* __restrict__ f, vec2_t<T>* __
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = __ldcs(src + t + P * e);
   line_fft<M, E, L, -1, SYNC>(v, sm, stw, t, l);
+  constexpr bool PAIRS = ARENA_Z_PAIRS && E >= 2 && (E % 2) == 0 && ARENA_Z_TWREC && E <= 32;
+  // staging for the mirror reads: the paired split only reads positions > M/2 (and Z[0] from its owner)
 #pragma unroll
-  for (int e = 0; e < E; ++e) sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
+  for (int e = PAIRS ? E / 2 : 0; e < E; ++e) sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
   xbarrier<SYNC>();
   V* dst = S + rowB(g, int(row / NR), int(row % NR)) * ncp;
   const V wt = tw_load(tw, t);  // W_n^t (split_twiddle)
-  if constexpr (ARENA_Z_PAIRS && E >= 2 && (E % 2) == 0 && ARENA_Z_TWREC && E <= 32) {
+  if constexpr (PAIRS) {
     // Both members of a pair from one thread: with A = Z[k], B = conj(Z[M-k]), S = (A + B)/2 and
     // U = (i/2) W_n^k (A - B),  X[k] = S - U  and  X[M-k] = conj(S + U)  (W_n^{M-k} = -conj W_n^k),
     // so the difference and its product with the twiddle are formed once per pair: 8 fp64
@@ -304,7 +306,7 @@ __device__ __forceinline__ void zfwd_rows(const T* __restrict__ f, vec2_t<T>* __
     for (int e = 0; e < E / 2; ++e) {
       const int k = t + P * e;
       const V A = v[e];
-      const V Bc = sm[smem_idx<L, SW, V>((M - k) & (M - 1), l)];
+      const V Bc = k == 0 ? A : sm[smem_idx<L, SW, V>(M - k, l)];
       const V B{Bc.x, -Bc.y};
       const V Wh = split_twiddle<E>(tw, wh, k, e);  // (i/2) W_n^k
       const V U = cmul(Wh, csub(A, B));
@@ -1072,8 +1074,9 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::M
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = __ldcs(src + t + P * e);
   line_fft<M, E, L, -1>(v, sm, stw, t, l);
+  constexpr bool PAIRS = ARENA_Z_PAIRS && E >= 2 && (E % 2) == 0 && ARENA_Z_TWREC && E <= 32;
 #pragma unroll
-  for (int e = 0; e < E; ++e) sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
+  for (int e = PAIRS ? E / 2 : 0; e < E; ++e) sm[smem_idx<L, SW, V>(t + P * e, l)] = v[e];
   __syncthreads();
   const size_t rin = lrow(gz, 0, int(row >> gz.njs), int(row & (gz.nj - 1)));
   const size_t chunk = size_t(gz.ni) * gz.nj;
@@ -1086,16 +1089,35 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::M
     }
   };
   const V wt = tw_load(tw, t);  // W_n^t (split_twiddle)
+  if constexpr (PAIRS) {  // Hermitian pairs (k, M - k) from one thread, as zfwd_rows
+    const V wh{T(-0.5) * wt.y, T(0.5) * wt.x};  // (i/2) W_n^t
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int k = t + P * e;
-    const V A = v[e];
-    const V Bc = sm[smem_idx<L, SW, V>((M - k) & (M - 1), l)];
-    const V B{Bc.x, -Bc.y};
-    const V W = split_twiddle<E>(tw, wt, k, e);
-    const V WD = cmul(W, csub(A, B));
-    put(k, V{T(0.5) * (A.x + B.x + WD.y), T(0.5) * (A.y + B.y - WD.x)});
-    if (k == 0) put(M, V{A.x - A.y, T(0)});
+    for (int e = 0; e < E / 2; ++e) {
+      const int k = t + P * e;
+      const V A = v[e];
+      const V Bc = k == 0 ? A : sm[smem_idx<L, SW, V>(M - k, l)];
+      const V B{Bc.x, -Bc.y};
+      const V Wh = split_twiddle<E>(tw, wh, k, e);  // (i/2) W_n^k
+      const V U = cmul(Wh, csub(A, B));
+      const V Sm = cadd(A, B);
+      put(k, V{fma(T(0.5), Sm.x, -U.x), fma(T(0.5), Sm.y, -U.y)});
+      V Xm{fma(T(0.5), Sm.x, U.x), -fma(T(0.5), Sm.y, U.y)};
+      if (k == 0) Xm.y = T(0);
+      put(M - k, Xm);
+    }
+    if (t == 0) put(M / 2, V{v[E / 2].x, -v[E / 2].y});
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int k = t + P * e;
+      const V A = v[e];
+      const V Bc = sm[smem_idx<L, SW, V>((M - k) & (M - 1), l)];
+      const V B{Bc.x, -Bc.y};
+      const V W = split_twiddle<E>(tw, wt, k, e);
+      const V WD = cmul(W, csub(A, B));
+      put(k, V{T(0.5) * (A.x + B.x + WD.y), T(0.5) * (A.y + B.y - WD.x)});
+      if (k == 0) put(M, V{A.x - A.y, T(0)});
+    }
   }
   if constexpr (PEER) __threadfence_system();
 }
@@ -1129,6 +1151,34 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::M
     return __ldcs(R + (size_t(c) * chunk + rin) * kq + (k - c * kq));
   };
   V v[E];
+  constexpr bool PAIRS = ARENA_Z_PAIRS && E >= 2 && (E % 2) == 0 && ARENA_Z_TWREC && E <= 32;
+  if constexpr (PAIRS) {  // Hermitian pairs (k, M - k) from one thread, as zinv_rows
+    const V wt = tw_load(tw, t);
+    const V wi{wt.y, wt.x};  // i conj(W_n^t)
+#pragma unroll
+    for (int e = 0; e < E / 2; ++e) {
+      const int k = t + P * e;
+      V A = get(k);
+      V C = get(M - k);
+      if (k == 0) {
+        A.y = T(0);
+        C.y = T(0);
+      }
+      const V B{C.x, -C.y};
+      const V Wi = cmulc(wi, w64((e * (32 / E)) & 63, T(0)));  // i conj(W_n^k)
+      const V Ep = cadd(A, B);
+      const V Op = cmul(csub(A, B), Wi);
+      v[e] = cadd(Ep, Op);
+      if (k != 0) sm[smem_idx<L, SW, V>(M - k, l)] = V{Ep.x - Op.x, Op.y - Ep.y};
+    }
+    if (t == 0) {
+      const V h = get(M / 2);
+      sm[smem_idx<L, SW, V>(M / 2, l)] = V{T(2) * h.x, T(-2) * h.y};
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = E / 2; e < E; ++e) v[e] = sm[smem_idx<L, SW, V>(t + P * e, l)];
+  } else {
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     v[e] = get(t + P * e);
@@ -1151,6 +1201,7 @@ __global__ void __launch_bounds__(ContigCfg<T, NR>::THREADS, ContigCfg<T, NR>::M
     const V Ep = cadd(A, B);
     const V Op = cmulc(csub(A, B), W);
     v[e] = V{Ep.x - Op.y, Ep.y + Op.x};
+  }
   }
   __syncthreads();
   line_fft<M, E, L, +1>(v, sm, stw, t, l);

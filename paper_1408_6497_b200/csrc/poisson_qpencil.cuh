@@ -67,33 +67,74 @@ __global__ void __launch_bounds__(QuadZCfg<T, NR>::THREADS, 2)
       st_out(R + q * qstride + (size_t(c) * chunk + rin) * kq + (k - c * kq), x);
     }
   };
+  constexpr int NM = M / TH;
+  if constexpr (ARENA_Z_PAIRS && NM >= 2 && NM % 2 == 0) {
+    // columns in Hermitian pairs (k, M - k), as k_zfwd_quad; column 0 pairs with the Nyquist column M
 #pragma unroll
-  for (int m = 0; m < M / TH; ++m) {
-    const int k = threadIdx.x + TH * m;
-    const V W = tw_load(tw, k);  // W_n^k
-    V x[4];
+    for (int m = 0; m < NM / 2; ++m) {
+      const int k = threadIdx.x + TH * m;
+      const V Wt = tw_load(tw, k);
+      const V Wh{T(-0.5) * Wt.y, T(0.5) * Wt.x};  // (i/2) W_n^k
+      V x[4], xr[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const V A = sm[r * M + k];
-      const V Bc = sm[r * M + ((M - k) & (M - 1))];
-      const V B{Bc.x, -Bc.y};
-      const V WD = cmul(W, csub(A, B));
-      x[r] = V{T(0.5) * (A.x + B.x + WD.y), T(0.5) * (A.y + B.y - WD.x)};
+      for (int r = 0; r < 4; ++r) {
+        const V A = sm[r * M + k];
+        const V Bc = sm[r * M + ((M - k) & (M - 1))];
+        const V B{Bc.x, -Bc.y};
+        const V U = cmul(Wh, csub(A, B));
+        const V Sm = cadd(A, B);
+        x[r] = V{fma(T(0.5), Sm.x, -U.x), fma(T(0.5), Sm.y, -U.y)};
+        xr[r] = V{fma(T(0.5), Sm.x, U.x), -fma(T(0.5), Sm.y, U.y)};
+        if (k == 0) xr[r].y = T(0);
+      }
+      quad_hadamard(x);
+      quad_hadamard(xr);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        put(q, k, cmul(x[q], wq[q]));
+        put(q, M - k, cmul(xr[q], wq[q]));
+      }
     }
-    quad_hadamard(x);
+    if (threadIdx.x == 0) {  // X[M/2] = conj(Z[M/2]) of each row
+      V x[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) put(q, k, cmul(x[q], wq[q]));
-  }
-  if (threadIdx.x == 0) {  // X[M] = Re Z0 - Im Z0 of each row
-    V x[4];
+      for (int r = 0; r < 4; ++r) {
+        const V z = sm[r * M + M / 2];
+        x[r] = V{z.x, -z.y};
+      }
+      quad_hadamard(x);
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const V z = sm[r * M];
-      x[r] = V{z.x - z.y, T(0)};
+      for (int q = 0; q < 4; ++q) put(q, M / 2, cmul(x[q], wq[q]));
     }
-    quad_hadamard(x);
+  } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) put(q, M, cmul(x[q], wq[q]));
+    for (int m = 0; m < M / TH; ++m) {
+      const int k = threadIdx.x + TH * m;
+      const V W = tw_load(tw, k);  // W_n^k
+      V x[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const V A = sm[r * M + k];
+        const V Bc = sm[r * M + ((M - k) & (M - 1))];
+        const V B{Bc.x, -Bc.y};
+        const V WD = cmul(W, csub(A, B));
+        x[r] = V{T(0.5) * (A.x + B.x + WD.y), T(0.5) * (A.y + B.y - WD.x)};
+      }
+      quad_hadamard(x);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) put(q, k, cmul(x[q], wq[q]));
+    }
+    if (threadIdx.x == 0) {  // X[M] = Re Z0 - Im Z0 of each row
+      V x[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const V z = sm[r * M];
+        x[r] = V{z.x - z.y, T(0)};
+      }
+      quad_hadamard(x);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) put(q, M, cmul(x[q], wq[q]));
+    }
   }
   if constexpr (PEER) __threadfence_system();  // peer stores performed before the ranks' barrier
 }
@@ -153,20 +194,47 @@ __global__ void __launch_bounds__(QuadZCfg<T, NR>::THREADS, 2)
   }
   __syncthreads();
   V v[E];
+  if constexpr (ARENA_Z_PAIRS && E >= 2 && E % 2 == 0) {  // Hermitian pairs, as k_zinv_quad
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int k = t + P * e;
-    V A = sm[l * M + k];
-    V Bs = (k == 0) ? xm[l] : sm[l * M + M - k];
-    if (k == 0) {  // FFTW c2r: imaginary parts of X[0] and X[M] ignored
-      A.y = T(0);
-      Bs.y = T(0);
+    for (int e = 0; e < E / 2; ++e) {
+      const int k = t + P * e;
+      V A = sm[l * M + k];
+      V C = (k == 0) ? xm[l] : sm[l * M + M - k];
+      if (k == 0) {  // FFTW c2r: imaginary parts of X[0] and X[M] ignored
+        A.y = T(0);
+        C.y = T(0);
+      }
+      const V B{C.x, -C.y};
+      const V W = tw_load(tw, k);
+      const V Wi{W.y, W.x};  // i conj(W_n^k)
+      const V Ep = cadd(A, B);
+      const V Op = cmul(csub(A, B), Wi);
+      v[e] = cadd(Ep, Op);
+      if (k != 0) sm[l * M + M - k] = V{Ep.x - Op.x, Op.y - Ep.y};
     }
-    const V B{Bs.x, -Bs.y};
-    const V W = tw_load(tw, k);
-    const V Ep = cadd(A, B);
-    const V Op = cmulc(csub(A, B), W);
-    v[e] = V{Ep.x - Op.y, Ep.y + Op.x};
+    if (t == 0) {
+      const V h = sm[l * M + M / 2];
+      sm[l * M + M / 2] = V{T(2) * h.x, T(-2) * h.y};
+    }
+    xbarrier<C::SYNC>();
+#pragma unroll
+    for (int e = E / 2; e < E; ++e) v[e] = sm[l * M + t + P * e];
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int k = t + P * e;
+      V A = sm[l * M + k];
+      V Bs = (k == 0) ? xm[l] : sm[l * M + M - k];
+      if (k == 0) {  // FFTW c2r: imaginary parts of X[0] and X[M] ignored
+        A.y = T(0);
+        Bs.y = T(0);
+      }
+      const V B{Bs.x, -Bs.y};
+      const V W = tw_load(tw, k);
+      const V Ep = cadd(A, B);
+      const V Op = cmulc(csub(A, B), W);
+      v[e] = V{Ep.x - Op.y, Ep.y + Op.x};
+    }
   }
   xbarrier<C::SYNC>();
   line_fft<M, E, RW, +1, C::SYNC>(v, gsm, stw, t, gi % RW);

@@ -180,3 +180,53 @@ def test_fma_form_dft_matches_numpy(R, S):
     ref = np.fft.fft(x, axis=-1) if S < 0 else np.fft.ifft(x, axis=-1) * R
     got = _dft_fma(x, S)
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 5e-16
+
+
+# ---- Hermitian pairs in the z passes (poisson_pow2.cuh zfwd_rows / zinv_rows, ARENA_Z_PAIRS) ---------
+@pytest.mark.parametrize("n", [4, 8, 32, 64, 1024])
+def test_r2c_split_in_hermitian_pairs(n):
+    """X[k] = S - U, X[M-k] = conj(S + U) with A = Z[k], B = conj(Z[M-k]), S = (A + B)/2,
+    U = (i/2) W_n^k (A - B): one pair per k in [0, M/2) (k = 0 pairs with the Nyquist output),
+    X[M/2] = conj(Z[M/2]) — against numpy's rfft."""
+    rng = np.random.default_rng(n)
+    f = rng.standard_normal(n)
+    M = n // 2
+    Z = np.fft.fft(f[0::2] + 1j * f[1::2])
+    X = np.zeros(M + 1, dtype=complex)
+    for k in range(M // 2):
+        A, B = Z[k], np.conj(Z[(M - k) % M])
+        S, U = 0.5 * (A + B), 0.5j * np.exp(-2j * np.pi * k / n) * (A - B)
+        X[k] = S - U
+        X[M - k] = np.conj(S + U)
+    X[M // 2] = np.conj(Z[M // 2])
+    ref = np.fft.rfft(f)
+    assert np.linalg.norm(X - ref) <= 1e-14 * np.linalg.norm(ref)
+    assert X[0].imag == 0 or abs(X[0].imag) < 1e-15 * abs(X[0])
+
+
+@pytest.mark.parametrize("n", [4, 8, 32, 64, 1024])
+def test_c2r_preprocessing_in_hermitian_pairs(n):
+    """Z[k] = Ep + Op, Z[M-k] = conj(Ep - Op) with A = X[k], B = conj(X[M-k]), Ep = A + B,
+    Op = i conj(W_n^k) (A - B); Z[M/2] = 2 conj(X[M/2]); the imaginary parts of X[0] and X[M]
+    ignored (FFTW c2r) — the M-point backward FFT of Z is then n * irfft(X), interleaved."""
+    rng = np.random.default_rng(n + 1)
+    M = n // 2
+    X = rng.standard_normal(M + 1) + 1j * rng.standard_normal(M + 1)  # junk imaginary parts at 0 and M too
+    Z = np.zeros(M, dtype=complex)
+    for k in range(M // 2):
+        A, C = X[k], X[M - k]
+        if k == 0:
+            A, C = A.real + 0j, C.real + 0j
+        B = np.conj(C)
+        Ep, Op = A + B, 1j * np.exp(2j * np.pi * k / n) * (A - B)
+        Z[k] = Ep + Op
+        if k:
+            Z[M - k] = np.conj(Ep - Op)
+    Z[M // 2] = 2 * np.conj(X[M // 2])
+    z = np.fft.ifft(Z) * M
+    u = np.empty(n)
+    u[0::2], u[1::2] = z.real, z.imag
+    Xc = X.copy()
+    Xc[0], Xc[M] = X[0].real, X[M].real
+    ref = np.fft.irfft(Xc, n) * n
+    assert np.linalg.norm(u - ref) <= 1e-13 * np.linalg.norm(ref)
